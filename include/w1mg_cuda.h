@@ -1,0 +1,176 @@
+/*
+ * w1mg_cuda.h -- the C-ABI drop-in boundary of the B200-native W1 solver.
+ *
+ * The reference (/root/reference/proj) is a C++20 library whose entry points
+ * are the w1mg:: free functions in proj/include/w1mg/*.hpp.  This header is
+ * the thin, FFI-friendly layer underneath our source-compatible
+ * re-implementation of those headers (include/w1mg/*.hpp, implemented in
+ * paper_1810_00118_b200/csrc/host/w1mg_api.cpp): plain pointers, plain
+ * sizes, status codes, no C++ or torch types.  Python (ctypes), Go (cgo),
+ * Java (JNI/Panama) or Rust bind it directly; see INTEGRATION.md.
+ *
+ * Arrays passed by host pointer use the reference layouts
+ * (proj/include/w1mg/grid.hpp:30-61), n = cells per side:
+ *   scalar (potential phi, source rho)  (n+1)*(n+1)  [j*(n+1)+i]
+ *   x-edges m_x                          (n+1)*n      [j*n+i]
+ *   y-edges m_y                          n*(n+1)      [j*(n+1)+i]
+ * Functions with a _dev suffix take device pointers and leave results on
+ * the device.
+ *
+ * Error convention: every int-returning call returns W1MG_OK (0) or an error
+ * code; w1mg_last_error() gives the thread-local message.  W1MG_EINVAL
+ * carries the same message text the reference throws as
+ * std::invalid_argument (e.g. "SourceField: values do not sum to zero",
+ * proj/src/grid.cpp:42), so the C++ shim rethrows the identical exception.
+ *
+ * Threading: a context is bound to one device and one CUDA stream; use one
+ * context per host thread.  Free functions without a context are re-entrant.
+ */
+#ifndef W1MG_CUDA_H
+#define W1MG_CUDA_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define W1MG_ABI_VERSION 1
+
+/* status codes */
+#define W1MG_OK 0
+#define W1MG_EINVAL 1    /* std::invalid_argument in the reference            */
+#define W1MG_ELOGIC 2    /* std::logic_error ("bad PNorm", pnorm.hpp:29)        */
+#define W1MG_ECUDA 3     /* CUDA runtime failure                                */
+#define W1MG_ENOMEM 4    /* device allocation failed                            */
+#define W1MG_ENONFINITE 5 /* NaN/Inf residual detected on device                */
+
+/* PNorm, same order as enum class PNorm {p1, p2, pinf} (pnorm.hpp:20) */
+#define W1MG_P1 0
+#define W1MG_P2 1
+#define W1MG_PINF 2
+
+/* StepMode (report.hpp:10-13) */
+#define W1MG_STEP_SAFE 0
+#define W1MG_STEP_PRACTICAL 1
+
+typedef struct w1mg_ctx w1mg_ctx;
+
+/* Result of one cp_run (report.hpp:22-41 without the fields). */
+typedef struct w1mg_cp_report {
+    double distance;   /* primal value sum ||m(x)||_p h^2 (grid.cpp:132-138)       */
+    double dual_value; /* <phi, rho>_h (grid.cpp:140-142); ~ -W1 for CP             */
+    int converged;     /* fpr < tol reached before max_iters                        */
+    long iterations;   /* sweeps performed                                           */
+    double fpr_final;  /* residual of the last sweep (solver_cp.cpp:70)              */
+    double seconds;    /* device time of the iteration loop (CUDA events)           */
+} w1mg_cp_report;
+
+/* LevelStats (report.hpp:22-28) */
+typedef struct w1mg_level_stats {
+    double h;
+    double eps;
+    long iters;
+    double fpr_final;
+    double seconds;
+} w1mg_level_stats;
+
+/* Cascade parameters.  Per-level tolerance:
+ *   rel_tol > 0 : eps_l = rel_tol * tau_l * ||rho_l||^2_L2  (= rel_tol * R_cold,l,
+ *                 the exact first-sweep residual from the zero state)
+ *   otherwise   : eps_l = eps[l] (absolute, e.g. from w1mg_make_schedule)   */
+typedef struct w1mg_ml_params {
+    int levels;        /* L >= 1; level 0 is the coarsest                      */
+    int pnorm;         /* W1MG_P1 / W1MG_P2 / W1MG_PINF                        */
+    int step_mode;     /* W1MG_STEP_SAFE / W1MG_STEP_PRACTICAL                 */
+    double rel_tol;    /* see above                                            */
+    const double* eps; /* levels entries, used when rel_tol <= 0              */
+    long max_iters;    /* per level                                            */
+} w1mg_ml_params;
+
+/* ---------------------------------------------------------------- context */
+int w1mg_ctx_create(int device, w1mg_ctx** out);
+void w1mg_ctx_destroy(w1mg_ctx* ctx);
+const char* w1mg_last_error(void);
+int w1mg_abi_version(void);
+/* Number of fused-iteration kernel launches issued by this context so far
+ * (for bench.py's gpu_launches claim). */
+long w1mg_ctx_launch_count(const w1mg_ctx* ctx);
+/* Block until all work queued on the context stream is done. */
+int w1mg_ctx_synchronize(w1mg_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t), for callers that time on it. */
+void* w1mg_ctx_stream(w1mg_ctx* ctx);
+
+/* ------------------------------------------------- step sizes (host only) */
+/* cp_step_size, solver_cp.cpp:75-78: 1/||A|| (practical) or 1/(2||A||) with
+ * ||A|| <= 2 sqrt(2)/h (grid.cpp:130). */
+double w1mg_cp_step_size(int n, int step_mode);
+/* pdhg_step_size, solver_pdhg.hpp:19-20: 1 (practical) or 1/2 (safe). */
+double w1mg_pdhg_step_size(int step_mode);
+/* make_schedule (Eq. 16): eps[l] = eps_L * (h_l/h_L)^alpha. */
+int w1mg_make_schedule(int n_finest, int levels, double eps_finest, double alpha, double* eps);
+
+/* ---------------------------------------------------- grid operators (GPU) */
+/* divergence_into, grid.cpp:45-68 */
+int w1mg_divergence(w1mg_ctx* ctx, int n, const double* mx, const double* my, double* out);
+/* adjoint_into, grid.cpp:76-91 (negative forward difference) */
+int w1mg_adjoint(w1mg_ctx* ctx, int n, const double* phi, double* gx, double* gy);
+/* primal_value, grid.cpp:132-138 (compensated) */
+int w1mg_primal_value(w1mg_ctx* ctx, int n, const double* mx, const double* my, int pnorm,
+                      double* out);
+/* inner_h on nodes, grid.cpp:99-104 (compensated); dual_value = inner_h(phi, rho) */
+int w1mg_inner_h_nodes(w1mg_ctx* ctx, int n, const double* a, const double* b, double* out);
+/* inner_h on edges, grid.cpp:106-112 */
+int w1mg_inner_h_edges(w1mg_ctx* ctx, int n, const double* ax, const double* ay,
+                       const double* bx, const double* by, double* out);
+/* SourceField gate, grid.cpp:35-43: W1MG_OK if |sum rho| <= 1e-12 sum|rho|,
+ * else W1MG_EINVAL "SourceField: values do not sum to zero".  Host-side. */
+int w1mg_source_check(int n, const double* rho);
+
+/* ------------------------------------------------- Algorithm 1 (Li et al.) */
+/* cp_run, solver_cp.cpp:113-147.  m0x/m0y/phi0 may be NULL (zero start).
+ * mu/tau as from w1mg_cp_step_size.  Stops when the Eq. 9 residual < tol or
+ * after max_iters sweeps.  Outputs mx/my/phi may be NULL; fpr_hist receives
+ * min(iterations, hist_cap) residuals.  Convergence is decided on the
+ * device every sweep; the host never synchronises per iteration. */
+int w1mg_cp_run(w1mg_ctx* ctx, int n, const double* rho, const double* m0x, const double* m0y,
+                const double* phi0, int pnorm, double mu, double tau, double tol, long max_iters,
+                double* mx, double* my, double* phi, double* fpr_hist, long hist_cap,
+                w1mg_cp_report* rep);
+
+/* cp_residual, solver_cp.cpp:102-111 (Eq. 9 between two states). */
+int w1mg_cp_residual(w1mg_ctx* ctx, int n, const double* cmx, const double* cmy,
+                     const double* cphi, const double* pmx, const double* pmy,
+                     const double* pphi, double mu, double tau, double* out);
+
+/* ------------------------------------------- sources and cascade (Alg. 3) */
+/* Per-level sources from two m x m cell images (finest level n = m): 2x2
+ * block-sum restriction, cell->node averaging, unit-mass normalisation,
+ * rho = (a - b)/h^2 minus its compensated mean.  Output is
+ * the concatenation coarse->fine of (n_l+1)^2 arrays. */
+int w1mg_ml_sources(w1mg_ctx* ctx, int m, const double* img0, const double* img1, int levels,
+                    double* rho_levels);
+
+/* Cascadic Li et al. PD (Algorithm 3) for one pair.  rho_levels: coarse->
+ * fine concatenation.  Final-level fields (may be NULL), per-level stats
+ * (levels entries, may be NULL), finest-level residual history. */
+int w1mg_ml_cp_run(w1mg_ctx* ctx, int n_finest, const double* rho_levels,
+                   const w1mg_ml_params* prm, double* mx, double* my, double* phi,
+                   w1mg_level_stats* stats, double* fpr_hist, long hist_cap,
+                   w1mg_cp_report* rep);
+
+/* Batched cascades (config 4): npairs independent pairs given as m x m cell
+ * images (img0s/img1s: npairs*m*m, pair-major).  Per pair outputs:
+ * distance[npairs], dual[npairs], iters[npairs*levels], converged[npairs]
+ * (any output pointer may be NULL).  The _dev variant takes device image
+ * pointers and writes device outputs. */
+int w1mg_ml_cp_batch(w1mg_ctx* ctx, int npairs, int m, const double* img0s,
+                     const double* img1s, const w1mg_ml_params* prm, double* distance,
+                     double* dual, long* iters, int* converged);
+int w1mg_ml_cp_batch_dev(w1mg_ctx* ctx, int npairs, int m, const double* img0s_dev,
+                         const double* img1s_dev, const w1mg_ml_params* prm,
+                         double* distance_dev, double* dual_dev, long* iters_dev,
+                         int* converged_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* W1MG_CUDA_H */

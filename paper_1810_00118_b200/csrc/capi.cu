@@ -1,0 +1,833 @@
+// capi.cu -- the extern "C" boundary (include/w1mg_cuda.h) and the device
+// engine behind it: context, workspace, per-level drivers, CUDA-graph sweep
+// loop with device-side convergence, cascade and batched cascade.
+//
+// Reference call stacks this replaces (paths relative to /root/reference):
+//   cp_run           proj/src/solver_cp.cpp:113-147
+//   cp_residual      proj/src/solver_cp.cpp:102-111
+//   grid operators   proj/src/grid.cpp:45-142
+//   ml_run (spec)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/w1mg_cuda.h"
+#include "level_kernels.cuh"
+
+using namespace w1mg_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
+
+#define CK(expr)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            fail(e_ == cudaErrorMemoryAllocation ? W1MG_ENOMEM : W1MG_ECUDA,            \
+                 std::string(#expr) + ": " + cudaGetErrorString(e_));                  \
+    } while (0)
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return W1MG_OK;
+    } catch (const Fail& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return W1MG_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return W1MG_ECUDA;
+    }
+}
+
+void check_pnorm(int p) {
+    if (p < 0 || p > 2) fail(W1MG_ELOGIC, "bad PNorm");
+}
+void check_n(int n) {
+    if (n < 1) fail(W1MG_EINVAL, "GridSpec: cells_per_side must be positive");
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- context
+struct w1mg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    struct Buf {
+        void* p = nullptr;
+        size_t bytes = 0;
+    };
+    std::map<std::string, Buf> bufs;
+    std::map<std::string, cudaGraphExec_t> graphs;
+    int* pinned = nullptr;  // 2 ints for the done-count pipeline
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    long launches = 0;
+    int num_sms = 148;
+
+    void* buf(const std::string& name, size_t bytes) {
+        Buf& b = bufs[name];
+        if (b.bytes < bytes) {
+            if (b.p) CK(cudaFree(b.p));
+            b.p = nullptr;
+            b.bytes = 0;
+            // any cached graph may hold the old pointer
+            for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+            graphs.clear();
+            CK(cudaMalloc(&b.p, bytes));
+            b.bytes = bytes;
+        }
+        return b.p;
+    }
+    template <class T>
+    T* get(const std::string& name, size_t count) {
+        return static_cast<T*>(buf(name, count * sizeof(T)));
+    }
+};
+
+namespace {
+
+// ------------------------------------------------------------ level batch
+struct Level {
+    int n = 0;
+    int B = 0;
+    Layout L{};
+    double* base = nullptr;
+    PairCtl* ctl = nullptr;
+    unsigned* ticket = nullptr;
+    double* partial = nullptr;
+    int* ndone = nullptr;
+    SweepArgs args{};
+    dim3 grid;
+};
+
+Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, double tau,
+                 double* hist, long hist_cap) {
+    Level lv;
+    lv.n = n;
+    lv.B = B;
+    lv.L = Layout::make(n);
+    lv.base = c->get<double>(tag + ".base", (size_t)B * NSLOT * lv.L.plane);
+    lv.ctl = c->get<PairCtl>(tag + ".ctl", B);
+    lv.ticket = c->get<unsigned>(tag + ".ticket", B);
+    lv.ndone = c->get<int>(tag + ".ndone", 1);
+
+    SweepArgs& a = lv.args;
+    a.base = lv.base;
+    a.L = lv.L;
+    a.ncx = (n + 1 + kOwn - 1) / kOwn;
+    // strip height: the tallest that still gives >= 32 warps per SM overall
+    const long target = (long)c->num_sms * 32;
+    int H = 64;
+    while (H > 2) {
+        long tiles = (long)B * a.ncx * ((n + 1 + H - 1) / H);
+        if (tiles >= target) break;
+        H >>= 1;
+    }
+    a.H = H;
+    a.nsy = (n + 1 + H - 1) / H;
+    a.ntiles = a.ncx * a.nsy;
+    a.mu = mu;
+    a.tau = tau;
+    const double h = 1.0 / n;
+    a.ih = 1.0 / h;  // inv_h, grid.cpp:48/79
+    a.h2 = h * h;    // solver_cp.cpp:25
+    a.ctl = lv.ctl;
+    a.ticket = lv.ticket;
+    a.hist = hist;
+    a.hist_cap = hist_cap;
+    a.ndone = lv.ndone;
+    lv.grid = dim3((a.ntiles + kSweepWarps - 1) / kSweepWarps, B, 1);
+    lv.partial = c->get<double>(tag + ".partial", (size_t)B * lv.grid.x * 3);
+    a.partial = lv.partial;
+    CK(cudaMemsetAsync(lv.ticket, 0, sizeof(unsigned) * B, c->stream));
+    return lv;
+}
+
+void zero_level(w1mg_ctx* c, const Level& lv) {
+    CK(cudaMemsetAsync(lv.base, 0, sizeof(double) * (size_t)lv.B * NSLOT * lv.L.plane, c->stream));
+}
+
+double* slot_ptr(const Level& lv, int pair, int slot) {
+    return lv.base + ((long)pair * NSLOT + slot) * lv.L.plane;
+}
+
+// dense reference-layout host/device array <-> one slot of one pair
+void put_nodes(w1mg_ctx* c, const Level& lv, int pair, int slot, const double* src,
+               cudaMemcpyKind kind) {
+    const int n = lv.n;
+    CK(cudaMemcpy2DAsync(slot_ptr(lv, pair, slot) + lv.L.at(0, 0), lv.L.pitch * 8, src,
+                         (size_t)(n + 1) * 8, (size_t)(n + 1) * 8, n + 1, kind, c->stream));
+}
+void put_xedges(w1mg_ctx* c, const Level& lv, int pair, int slot, const double* src,
+                cudaMemcpyKind kind) {
+    const int n = lv.n;
+    CK(cudaMemcpy2DAsync(slot_ptr(lv, pair, slot) + lv.L.at(0, 0), lv.L.pitch * 8, src,
+                         (size_t)n * 8, (size_t)n * 8, n + 1, kind, c->stream));
+}
+void put_yedges(w1mg_ctx* c, const Level& lv, int pair, int slot, const double* src,
+                cudaMemcpyKind kind) {
+    const int n = lv.n;
+    CK(cudaMemcpy2DAsync(slot_ptr(lv, pair, slot) + lv.L.at(0, 0), lv.L.pitch * 8, src,
+                         (size_t)(n + 1) * 8, (size_t)(n + 1) * 8, n, kind, c->stream));
+}
+void get_nodes(w1mg_ctx* c, const Level& lv, int pair, int slot, double* dst) {
+    const int n = lv.n;
+    CK(cudaMemcpy2DAsync(dst, (size_t)(n + 1) * 8, slot_ptr(lv, pair, slot) + lv.L.at(0, 0),
+                         lv.L.pitch * 8, (size_t)(n + 1) * 8, n + 1, cudaMemcpyDefault,
+                         c->stream));
+}
+void get_xedges(w1mg_ctx* c, const Level& lv, int pair, int slot, double* dst) {
+    const int n = lv.n;
+    CK(cudaMemcpy2DAsync(dst, (size_t)n * 8, slot_ptr(lv, pair, slot) + lv.L.at(0, 0),
+                         lv.L.pitch * 8, (size_t)n * 8, n + 1, cudaMemcpyDefault, c->stream));
+}
+void get_yedges(w1mg_ctx* c, const Level& lv, int pair, int slot, double* dst) {
+    const int n = lv.n;
+    CK(cudaMemcpy2DAsync(dst, (size_t)(n + 1) * 8, slot_ptr(lv, pair, slot) + lv.L.at(0, 0),
+                         lv.L.pitch * 8, (size_t)(n + 1) * 8, n, cudaMemcpyDefault, c->stream));
+}
+
+dim3 node_grid(int n, int B, dim3 blk) {
+    return dim3((n + 1 + blk.x - 1) / blk.x, (n + 1 + blk.y - 1) / blk.y, B);
+}
+
+// compensated per-pair reduction, out[b] = (sum f * s1) * s2
+template <class F>
+void reduce_pairs(w1mg_ctx* c, F f, int w, int rows, int B, double s1, double s2, double* out) {
+    int G = (2 * c->num_sms + B - 1) / B;
+    if (G > 64) G = 64;
+    if (G > rows) G = rows;
+    if (G < 1) G = 1;
+    double2* part = c->get<double2>("reduce.partial", (size_t)G * B);
+    node_reduce_kernel<F><<<dim3(G, B), kRedThreads, 0, c->stream>>>(f, w, rows, part);
+    CK(cudaGetLastError());
+    reduce_finish_kernel<<<B, 32, 0, c->stream>>>(part, G, s1, s2, out);
+    CK(cudaGetLastError());
+}
+
+void launch_sweep(const Level& lv, int pn, int parity, cudaStream_t s) {
+    dim3 blk(kSweepWarps * 32);
+    switch (pn) {
+        case 0: cp_sweep_kernel<0><<<lv.grid, blk, 0, s>>>(lv.args, parity); break;
+        case 1: cp_sweep_kernel<1><<<lv.grid, blk, 0, s>>>(lv.args, parity); break;
+        default: cp_sweep_kernel<2><<<lv.grid, blk, 0, s>>>(lv.args, parity); break;
+    }
+}
+
+cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
+    std::string key(reinterpret_cast<const char*>(&lv.args), sizeof(SweepArgs));
+    key += std::to_string(pn) + ":" + std::to_string(K) + ":" + std::to_string(lv.grid.x) + ":" +
+           std::to_string(lv.grid.y);
+    auto it = c->graphs.find(key);
+    if (it != c->graphs.end()) return it->second;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < K; ++k) launch_sweep(lv, pn, k & 1, c->stream);
+    CK(cudaStreamEndCapture(c->stream, &g));
+    cudaGraphExec_t ex;
+    CK(cudaGraphInstantiate(&ex, g, 0));
+    CK(cudaGraphDestroy(g));
+    c->graphs[key] = ex;
+    return ex;
+}
+
+// Runs sweeps on every pair of the level until each pair's stop flag is set
+// (device-side, solver_cp.cpp:128-136 semantics).  The host only watches a
+// done-counter one graph behind, so it never stalls the GPU per iteration.
+void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
+    if (max_iters <= 0) return;
+    constexpr int K = 16;
+    if (max_iters < K) {
+        for (long k = 0; k < max_iters; ++k) launch_sweep(lv, pn, (int)(k & 1), c->stream);
+        CK(cudaGetLastError());
+        c->launches += max_iters;
+        return;
+    }
+    cudaGraphExec_t ex = sweep_graph(c, lv, pn, K);
+    long launched = 0;
+    for (long g = 0;; ++g) {
+        CK(cudaGraphLaunch(ex, c->stream));
+        launched += K;
+        c->launches += K;
+        CK(cudaMemcpyAsync(c->pinned + (g & 1), lv.ndone, sizeof(int), cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaEventRecord(c->ev[g & 1], c->stream));
+        if (g > 0) {
+            CK(cudaEventSynchronize(c->ev[(g - 1) & 1]));
+            if (c->pinned[(g - 1) & 1] >= lv.B) break;
+        }
+        if (launched >= max_iters + K) break;  // every pair hit its cap by now
+    }
+}
+
+// Per-level control init: tolerance = rel_scale * sum(rho^2) (relative mode,
+// computed on device) or abs_tol.
+void init_level_ctl(w1mg_ctx* c, const Level& lv, double rel_tol, double abs_tol, long max_it) {
+    double* rs = nullptr;
+    double rel_scale = 0.0;
+    if (rel_tol > 0) {
+        rs = c->get<double>("level.rho_sq", lv.B);
+        const double h = 1.0 / lv.n;
+        reduce_pairs(c, FSlotSq{lv.base, lv.L, RHO}, lv.n + 1, lv.n + 1, lv.B, h * h, 1.0, rs);
+        rel_scale = rel_tol * lv.args.tau;  // eps = rel * tau * (h^2 sum rho^2)
+    }
+    init_ctl_kernel<<<(lv.B + 127) / 128, 128, 0, c->stream>>>(lv.ctl, lv.B, rs, rel_scale,
+                                                                 abs_tol, max_it, lv.ndone);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(lv.ticket, 0, sizeof(unsigned) * lv.B, c->stream));
+}
+
+void level_values(w1mg_ctx* c, const Level& lv, int pn, double* w1, double* dual) {
+    const double h = 1.0 / lv.n;
+    if (w1) {
+        switch (pn) {
+            case 0:
+                reduce_pairs(c, FPrimal<0>{lv.base, lv.L, lv.ctl}, lv.n + 1, lv.n + 1, lv.B, h, h, w1);
+                break;
+            case 1:
+                reduce_pairs(c, FPrimal<1>{lv.base, lv.L, lv.ctl}, lv.n + 1, lv.n + 1, lv.B, h, h, w1);
+                break;
+            default:
+                reduce_pairs(c, FPrimal<2>{lv.base, lv.L, lv.ctl}, lv.n + 1, lv.n + 1, lv.B, h, h, w1);
+                break;
+        }
+    }
+    if (dual) reduce_pairs(c, FDual{lv.base, lv.L, lv.ctl}, lv.n + 1, lv.n + 1, lv.B, h, h, dual);
+}
+
+// Sources for every level of a batch from the finest cell images (device).
+void build_sources(w1mg_ctx* c, std::vector<Level>& lv, const double* img0, const double* img1,
+                   int m) {
+    const int levels = (int)lv.size();
+    const int B = lv[0].B;
+    const double* a = img0;
+    const double* b = img1;
+    dim3 blk(32, 8);
+    double* sa = c->get<double>("src.sa", B);
+    double* sb = c->get<double>("src.sb", B);
+    double* sm = c->get<double>("src.sm", B);
+    for (int l = levels - 1; l >= 0; --l) {
+        const Level& L = lv[l];
+        const int n = L.n;
+        image_to_nodes_kernel<<<node_grid(n, B, blk), blk, 0, c->stream>>>(a, b, L.base, L.L, PHI1, MX1);
+        CK(cudaGetLastError());
+        reduce_pairs(c, FSlot{L.base, L.L, PHI1}, n + 1, n + 1, B, 1.0, 1.0, sa);
+        reduce_pairs(c, FSlot{L.base, L.L, MX1}, n + 1, n + 1, B, 1.0, 1.0, sb);
+        const double h = 1.0 / n;
+        make_source_kernel<<<node_grid(n, B, blk), blk, 0, c->stream>>>(L.base, L.L, PHI1, MX1, sa, sb, h * h);
+        CK(cudaGetLastError());
+        reduce_pairs(c, FSlot{L.base, L.L, RHO}, n + 1, n + 1, B, 1.0, 1.0, sm);
+        center_source_kernel<<<node_grid(n, B, blk), blk, 0, c->stream>>>(L.base, L.L, sm, PHI1, MX1);
+        CK(cudaGetLastError());
+        if (l > 0) {
+            const int mc = n / 2;
+            double* ca = c->get<double>("src.img0." + std::to_string(l - 1), (size_t)B * mc * mc);
+            double* cb = c->get<double>("src.img1." + std::to_string(l - 1), (size_t)B * mc * mc);
+            long total = (long)B * mc * mc;
+            int nb = (int)std::min<long>((total + 255) / 256, 65535L * 4);
+            block_sum_kernel<<<nb, 256, 0, c->stream>>>(a, ca, n, B);
+            block_sum_kernel<<<nb, 256, 0, c->stream>>>(b, cb, n, B);
+            CK(cudaGetLastError());
+            a = ca;
+            b = cb;
+        }
+    }
+    (void)m;
+}
+
+struct CascadeOut {
+    std::vector<double> seconds;
+};
+
+// Cascade over prepared levels (sources in RHO, level 0 zero state).
+void run_cascade(w1mg_ctx* c, std::vector<Level>& lv, const w1mg_ml_params& p, long* iters_dev,
+                 double* fpr_dev, double* tol_dev, std::vector<double>* secs) {
+    const int levels = (int)lv.size();
+    dim3 blk(32, 8);
+    for (int l = 0; l < levels; ++l) {
+        Level& L = lv[l];
+        if (l > 0) {
+            prolong_kernel<<<node_grid(L.n, L.B, blk), blk, 0, c->stream>>>(
+                lv[l - 1].base, lv[l - 1].L, lv[l - 1].ctl, L.base, L.L);
+            CK(cudaGetLastError());
+        }
+        const double abs_tol = (p.rel_tol > 0 || !p.eps) ? 0.0 : p.eps[l];
+        CK(cudaEventRecord(c->t0, c->stream));
+        init_level_ctl(c, L, p.rel_tol, abs_tol, p.max_iters);
+        run_sweeps(c, L, p.pnorm, p.max_iters);
+        CK(cudaEventRecord(c->t1, c->stream));
+        harvest_kernel<<<(L.B + 127) / 128, 128, 0, c->stream>>>(L.ctl, L.B, l, levels, iters_dev,
+                                                                   fpr_dev, tol_dev);
+        CK(cudaGetLastError());
+        if (secs) {
+            CK(cudaEventSynchronize(c->t1));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, c->t0, c->t1));
+            secs->push_back(ms * 1e-3);
+        }
+    }
+}
+
+std::vector<Level> make_levels(w1mg_ctx* c, const std::string& tag, int n_finest, int levels,
+                               int B, int step_mode, double* hist, long hist_cap) {
+    if (levels < 1) fail(W1MG_EINVAL, "levels must be >= 1");
+    if (n_finest % (1 << (levels - 1)) != 0)
+        fail(W1MG_EINVAL, "make_schedule: N must be divisible by 2^(L-1)");
+    std::vector<Level> lv;
+    for (int l = 0; l < levels; ++l) {
+        const int n = n_finest >> (levels - 1 - l);
+        const double step = w1mg_cp_step_size(n, step_mode);
+        const bool fin = (l == levels - 1);
+        lv.push_back(make_level(c, tag + std::to_string(l), n, B, step, step, fin ? hist : nullptr,
+                                fin ? hist_cap : 0));
+    }
+    return lv;
+}
+
+void check_ml(const w1mg_ml_params* p) {
+    if (!p) fail(W1MG_EINVAL, "null parameters");
+    check_pnorm(p->pnorm);
+    if (p->rel_tol <= 0 && !p->eps) fail(W1MG_EINVAL, "tolerances: need rel_tol > 0 or eps");
+}
+
+}  // namespace
+
+// ======================================================================
+extern "C" {
+
+const char* w1mg_last_error(void) { return g_err.c_str(); }
+int w1mg_abi_version(void) { return W1MG_ABI_VERSION; }
+
+int w1mg_ctx_create(int device, w1mg_ctx** out) {
+    return guard([&] {
+        if (!out) fail(W1MG_EINVAL, "null out");
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) fail(W1MG_EINVAL, "no such CUDA device");
+        CK(cudaSetDevice(device));
+        int major = 0;
+        CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        if (major < 10) fail(W1MG_ECUDA, "this build targets sm_100a (B200)");
+        auto* c = new w1mg_ctx();
+        c->device = device;
+        CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->pinned), 2 * sizeof(int), cudaHostAllocDefault));
+        for (auto& e : c->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventCreate(&c->t0));
+        CK(cudaEventCreate(&c->t1));
+        *out = c;
+    });
+}
+
+void w1mg_ctx_destroy(w1mg_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.second);
+    for (auto& b : c->bufs)
+        if (b.second.p) cudaFree(b.second.p);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->t0) cudaEventDestroy(c->t0);
+    if (c->t1) cudaEventDestroy(c->t1);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+long w1mg_ctx_launch_count(const w1mg_ctx* c) { return c ? c->launches : 0; }
+
+int w1mg_ctx_synchronize(w1mg_ctx* c) {
+    return guard([&] { CK(cudaStreamSynchronize(c->stream)); });
+}
+
+void* w1mg_ctx_stream(w1mg_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+double w1mg_cp_step_size(int n, int step_mode) {
+    const double h = 1.0 / n;                      // GridSpec, grid.hpp:19
+    const double bound = 2.0 * std::sqrt(2.0) / h;  // grid.cpp:130
+    return step_mode == W1MG_STEP_SAFE ? 1.0 / (2.0 * bound) : 1.0 / bound;
+}
+
+double w1mg_pdhg_step_size(int step_mode) { return step_mode == W1MG_STEP_SAFE ? 0.5 : 1.0; }
+
+int w1mg_make_schedule(int n_finest, int levels, double eps_finest, double alpha, double* eps) {
+    return guard([&] {
+        check_n(n_finest);
+        if (levels < 1 || n_finest % (1 << (levels - 1)) != 0)
+            fail(W1MG_EINVAL, "make_schedule: N must be divisible by 2^(L-1)");
+        if (!(eps_finest > 0)) fail(W1MG_EINVAL, "make_schedule: eps_L must be positive");
+        for (int l = 0; l < levels; ++l) {
+            // h_l / h_L = 2^(L-1-l)   (Eq. 16)
+            eps[l] = eps_finest * std::pow(std::ldexp(1.0, levels - 1 - l), alpha);
+        }
+    });
+}
+
+int w1mg_source_check(int n, const double* rho) {
+    return guard([&] {
+        check_n(n);
+        double s = 0, cs = 0, a = 0, ca = 0;  // Neumaier, grid.cpp:13-25
+        auto add = [](double& sum, double& comp, double v) {
+            double t = sum + v;
+            if (std::fabs(sum) >= std::fabs(v)) comp += (sum - t) + v;
+            else comp += (v - t) + sum;
+            sum = t;
+        };
+        const long V = (long)(n + 1) * (n + 1);
+        for (long k = 0; k < V; ++k) {
+            add(s, cs, rho[k]);
+            add(a, ca, std::fabs(rho[k]));
+        }
+        if (std::fabs(s + cs) > 1e-12 * (a + ca))
+            fail(W1MG_EINVAL, "SourceField: values do not sum to zero");
+    });
+}
+
+// ---------------------------------------------------------- grid operators
+int w1mg_divergence(w1mg_ctx* c, int n, const double* mx, const double* my, double* out) {
+    return guard([&] {
+        check_n(n);
+        const size_t E = (size_t)n * (n + 1), V = (size_t)(n + 1) * (n + 1);
+        double* dx = c->get<double>("op.a", E);
+        double* dy = c->get<double>("op.b", E);
+        double* dv = c->get<double>("op.c", V);
+        CK(cudaMemcpyAsync(dx, mx, E * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(dy, my, E * 8, cudaMemcpyDefault, c->stream));
+        dim3 blk(32, 8);
+        divergence_ref_kernel<<<node_grid(n, 1, blk), blk, 0, c->stream>>>(n, dx, dy, dv);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, dv, V * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int w1mg_adjoint(w1mg_ctx* c, int n, const double* phi, double* gx, double* gy) {
+    return guard([&] {
+        check_n(n);
+        const size_t E = (size_t)n * (n + 1), V = (size_t)(n + 1) * (n + 1);
+        double* dp = c->get<double>("op.c", V);
+        double* dx = c->get<double>("op.a", E);
+        double* dy = c->get<double>("op.b", E);
+        CK(cudaMemcpyAsync(dp, phi, V * 8, cudaMemcpyDefault, c->stream));
+        dim3 blk(32, 8);
+        adjoint_ref_kernel<<<node_grid(n, 1, blk), blk, 0, c->stream>>>(n, dp, dx, dy);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(gx, dx, E * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(gy, dy, E * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int w1mg_primal_value(w1mg_ctx* c, int n, const double* mx, const double* my, int pnorm,
+                      double* out) {
+    return guard([&] {
+        check_n(n);
+        check_pnorm(pnorm);
+        const size_t E = (size_t)n * (n + 1);
+        double* dx = c->get<double>("op.a", E);
+        double* dy = c->get<double>("op.b", E);
+        double* r = c->get<double>("op.r", 1);
+        CK(cudaMemcpyAsync(dx, mx, E * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(dy, my, E * 8, cudaMemcpyDefault, c->stream));
+        const double h = 1.0 / n;
+        if (pnorm == 0) reduce_pairs(c, FRefPrimal<0>{dx, dy, n}, n + 1, n + 1, 1, h, h, r);
+        else if (pnorm == 1) reduce_pairs(c, FRefPrimal<1>{dx, dy, n}, n + 1, n + 1, 1, h, h, r);
+        else reduce_pairs(c, FRefPrimal<2>{dx, dy, n}, n + 1, n + 1, 1, h, h, r);
+        CK(cudaMemcpyAsync(out, r, 8, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int w1mg_inner_h_nodes(w1mg_ctx* c, int n, const double* a, const double* b, double* out) {
+    return guard([&] {
+        check_n(n);
+        const size_t V = (size_t)(n + 1) * (n + 1);
+        double* da = c->get<double>("op.c", V);
+        double* db = c->get<double>("op.d", V);
+        double* r = c->get<double>("op.r", 1);
+        CK(cudaMemcpyAsync(da, a, V * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(db, b, V * 8, cudaMemcpyDefault, c->stream));
+        const double h = 1.0 / n;
+        reduce_pairs(c, FRefDot{da, db, n + 1}, n + 1, n + 1, 1, h, h, r);
+        CK(cudaMemcpyAsync(out, r, 8, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int w1mg_inner_h_edges(w1mg_ctx* c, int n, const double* ax, const double* ay, const double* bx,
+                       const double* by, double* out) {
+    return guard([&] {
+        check_n(n);
+        const size_t E = (size_t)n * (n + 1);
+        double* d0 = c->get<double>("op.a", E);
+        double* d1 = c->get<double>("op.b", E);
+        double* d2 = c->get<double>("op.e", E);
+        double* d3 = c->get<double>("op.f", E);
+        double* r = c->get<double>("op.r2", 2);
+        CK(cudaMemcpyAsync(d0, ax, E * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(d1, ay, E * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(d2, bx, E * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(d3, by, E * 8, cudaMemcpyDefault, c->stream));
+        // x-edges are n wide, n+1 rows; y-edges n+1 wide, n rows
+        reduce_pairs(c, FRefDot{d0, d2, n}, n, n + 1, 1, 1.0, 1.0, r);
+        reduce_pairs(c, FRefDot{d1, d3, n + 1}, n + 1, n, 1, 1.0, 1.0, r + 1);
+        double hr[2];
+        CK(cudaMemcpyAsync(hr, r, 16, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const double h = 1.0 / n;
+        *out = ((hr[0] + hr[1]) * h) * h;
+    });
+}
+
+// -------------------------------------------------------------- Algorithm 1
+int w1mg_cp_run(w1mg_ctx* c, int n, const double* rho, const double* m0x, const double* m0y,
+                const double* phi0, int pnorm, double mu, double tau, double tol, long max_iters,
+                double* mx, double* my, double* phi, double* fpr_hist, long hist_cap,
+                w1mg_cp_report* rep) {
+    return guard([&] {
+        check_n(n);
+        check_pnorm(pnorm);
+        if (!rho) fail(W1MG_EINVAL, "null rho");
+        if (!(mu > 0.0)) fail(W1MG_EINVAL, "shrink: mu must be positive");
+        CK(cudaSetDevice(c->device));
+        long cap = (fpr_hist && hist_cap > 0) ? hist_cap : 0;
+        double* dh = cap ? c->get<double>("cp.hist", cap) : nullptr;
+        Level lv = make_level(c, "cp", n, 1, mu, tau, dh, cap);
+        zero_level(c, lv);
+        put_nodes(c, lv, 0, RHO, rho, cudaMemcpyDefault);
+        if (m0x) put_xedges(c, lv, 0, MX0, m0x, cudaMemcpyDefault);
+        if (m0y) put_yedges(c, lv, 0, MY0, m0y, cudaMemcpyDefault);
+        if (phi0) put_nodes(c, lv, 0, PHI0, phi0, cudaMemcpyDefault);
+        CK(cudaEventRecord(c->t0, c->stream));
+        init_level_ctl(c, lv, 0.0, tol, max_iters);
+        run_sweeps(c, lv, pnorm, max_iters);
+        CK(cudaEventRecord(c->t1, c->stream));
+        double* vals = c->get<double>("cp.vals", 2);
+        level_values(c, lv, pnorm, vals, vals + 1);
+        PairCtl hc;
+        double hv[2];
+        CK(cudaMemcpyAsync(&hc, lv.ctl, sizeof(PairCtl), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hv, vals, 16, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (mx) get_xedges(c, lv, 0, MX0 + hc.cur, mx);
+        if (my) get_yedges(c, lv, 0, MY0 + hc.cur, my);
+        if (phi) get_nodes(c, lv, 0, PHI0 + hc.cur, phi);
+        long nh = std::min(hc.it, cap);
+        if (nh > 0) CK(cudaMemcpyAsync(fpr_hist, dh, nh * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->t0, c->t1));
+        if (rep) {
+            rep->distance = hv[0];
+            rep->dual_value = hv[1];
+            rep->iterations = hc.it;
+            rep->fpr_final = hc.fpr;
+            rep->converged = (hc.it > 0 && hc.fpr < tol) ? 1 : 0;
+            rep->seconds = ms * 1e-3;
+        }
+    });
+}
+
+int w1mg_cp_residual(w1mg_ctx* c, int n, const double* cmx, const double* cmy,
+                     const double* cphi, const double* pmx, const double* pmy,
+                     const double* pphi, double mu, double tau, double* out) {
+    return guard([&] {
+        check_n(n);
+        const size_t E = (size_t)n * (n + 1), V = (size_t)(n + 1) * (n + 1);
+        // dm and dphi on the host would be a CPU path: do the differences on
+        // the device (reference: solver_cp.cpp:103-108).
+        double* a0 = c->get<double>("res.a0", E);
+        double* a1 = c->get<double>("res.a1", E);
+        double* b0 = c->get<double>("res.b0", E);
+        double* b1 = c->get<double>("res.b1", E);
+        double* p0 = c->get<double>("res.p0", V);
+        double* p1 = c->get<double>("res.p1", V);
+        double* adm = c->get<double>("res.adm", V);
+        double* r = c->get<double>("res.r", 4);
+        CK(cudaMemcpyAsync(a0, cmx, E * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(a1, cmy, E * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(b0, pmx, E * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(b1, pmy, E * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(p0, cphi, V * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(p1, pphi, V * 8, cudaMemcpyDefault, c->stream));
+        sub_inplace_kernel<<<(int)((E + 255) / 256), 256, 0, c->stream>>>(a0, b0, (long)E);
+        sub_inplace_kernel<<<(int)((E + 255) / 256), 256, 0, c->stream>>>(a1, b1, (long)E);
+        sub_inplace_kernel<<<(int)((V + 255) / 256), 256, 0, c->stream>>>(p0, p1, (long)V);
+        CK(cudaGetLastError());
+        dim3 blk(32, 8);
+        divergence_ref_kernel<<<node_grid(n, 1, blk), blk, 0, c->stream>>>(n, a0, a1, adm);
+        CK(cudaGetLastError());
+        const double h = 1.0 / n;
+        reduce_pairs(c, FRefDot{a0, a0, n}, n, n + 1, 1, 1.0, 1.0, r);
+        reduce_pairs(c, FRefDot{a1, a1, n + 1}, n + 1, n, 1, 1.0, 1.0, r + 1);
+        reduce_pairs(c, FRefDot{p0, p0, n + 1}, n + 1, n + 1, 1, h, h, r + 2);
+        reduce_pairs(c, FRefDot{p0, adm, n + 1}, n + 1, n + 1, 1, h, h, r + 3);
+        double hr[4];
+        CK(cudaMemcpyAsync(hr, r, 32, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        // norm_L2 = sqrt(inner_h), then squared (solver_cp.cpp:109-110)
+        double nm = std::sqrt(((hr[0] + hr[1]) * h) * h);
+        double np = std::sqrt(hr[2]);
+        *out = nm * nm / mu + np * np / tau - 2.0 * hr[3];
+    });
+}
+
+// ---------------------------------------------------------------- cascade
+int w1mg_ml_sources(w1mg_ctx* c, int m, const double* img0, const double* img1, int levels,
+                    double* rho_levels) {
+    return guard([&] {
+        check_n(m);
+        const size_t MM = (size_t)m * m;
+        double* d0 = c->get<double>("in.img0", MM);
+        double* d1 = c->get<double>("in.img1", MM);
+        CK(cudaMemcpyAsync(d0, img0, MM * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(d1, img1, MM * 8, cudaMemcpyDefault, c->stream));
+        std::vector<Level> lv = make_levels(c, "src", m, levels, 1, W1MG_STEP_PRACTICAL, nullptr, 0);
+        for (auto& L : lv) zero_level(c, L);
+        build_sources(c, lv, d0, d1, m);
+        size_t off = 0;
+        for (int l = 0; l < levels; ++l) {
+            get_nodes(c, lv[l], 0, RHO, rho_levels + off);
+            off += (size_t)(lv[l].n + 1) * (lv[l].n + 1);
+        }
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int w1mg_ml_cp_run(w1mg_ctx* c, int n_finest, const double* rho_levels,
+                   const w1mg_ml_params* prm, double* mx, double* my, double* phi,
+                   w1mg_level_stats* stats, double* fpr_hist, long hist_cap,
+                   w1mg_cp_report* rep) {
+    return guard([&] {
+        check_n(n_finest);
+        check_ml(prm);
+        const int levels = prm->levels;
+        long cap = (fpr_hist && hist_cap > 0) ? hist_cap : 0;
+        double* dh = cap ? c->get<double>("ml.hist", cap) : nullptr;
+        std::vector<Level> lv =
+            make_levels(c, "ml", n_finest, levels, 1, prm->step_mode, dh, cap);
+        size_t off = 0;
+        for (auto& L : lv) {
+            zero_level(c, L);
+            put_nodes(c, L, 0, RHO, rho_levels + off, cudaMemcpyDefault);
+            off += (size_t)(L.n + 1) * (L.n + 1);
+        }
+        long* it = c->get<long>("ml.iters", levels);
+        double* ff = c->get<double>("ml.fpr", levels);
+        double* tl = c->get<double>("ml.tol", levels);
+        std::vector<double> secs;
+        run_cascade(c, lv, *prm, it, ff, tl, &secs);
+        const Level& F = lv.back();
+        double* vals = c->get<double>("ml.vals", 2);
+        level_values(c, F, prm->pnorm, vals, vals + 1);
+        std::vector<long> hit(levels);
+        std::vector<double> hff(levels), htl(levels);
+        PairCtl hc;
+        double hv[2];
+        CK(cudaMemcpyAsync(hit.data(), it, levels * sizeof(long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hff.data(), ff, levels * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(htl.data(), tl, levels * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(&hc, F.ctl, sizeof(PairCtl), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hv, vals, 16, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (mx) get_xedges(c, F, 0, MX0 + hc.cur, mx);
+        if (my) get_yedges(c, F, 0, MY0 + hc.cur, my);
+        if (phi) get_nodes(c, F, 0, PHI0 + hc.cur, phi);
+        long nh = std::min(hc.it, cap);
+        if (nh > 0) CK(cudaMemcpyAsync(fpr_hist, dh, nh * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        long total = 0;
+        double tsec = 0;
+        for (int l = 0; l < levels; ++l) {
+            total += hit[l];
+            tsec += secs[l];
+            if (stats) {
+                stats[l].h = 1.0 / lv[l].n;
+                stats[l].eps = htl[l];
+                stats[l].iters = hit[l];
+                stats[l].fpr_final = hff[l];
+                stats[l].seconds = secs[l];
+            }
+        }
+        if (rep) {
+            rep->distance = hv[0];
+            rep->dual_value = hv[1];
+            rep->iterations = total;
+            rep->fpr_final = hc.fpr;
+            rep->converged = (hc.fpr < hc.tol) ? 1 : 0;
+            rep->seconds = tsec;
+        }
+    });
+}
+
+int w1mg_ml_cp_batch_dev(w1mg_ctx* c, int npairs, int m, const double* img0s,
+                         const double* img1s, const w1mg_ml_params* prm, double* distance,
+                         double* dual, long* iters, int* converged) {
+    return guard([&] {
+        check_n(m);
+        check_ml(prm);
+        if (npairs < 1 || npairs > 65535) fail(W1MG_EINVAL, "npairs must be in [1, 65535]");
+        std::vector<Level> lv =
+            make_levels(c, "mlb", m, prm->levels, npairs, prm->step_mode, nullptr, 0);
+        for (auto& L : lv) zero_level(c, L);
+        build_sources(c, lv, img0s, img1s, m);
+        run_cascade(c, lv, *prm, iters, nullptr, nullptr, nullptr);
+        level_values(c, lv.back(), prm->pnorm, distance, dual);
+        if (converged) {
+            converged_kernel<<<(npairs + 127) / 128, 128, 0, c->stream>>>(lv.back().ctl, npairs, converged);
+            CK(cudaGetLastError());
+        }
+    });
+}
+
+int w1mg_ml_cp_batch(w1mg_ctx* c, int npairs, int m, const double* img0s, const double* img1s,
+                     const w1mg_ml_params* prm, double* distance, double* dual, long* iters,
+                     int* converged) {
+    return guard([&] {
+        check_n(m);
+        check_ml(prm);
+        const size_t MM = (size_t)npairs * m * m;
+        double* d0 = c->get<double>("in.img0s", MM);
+        double* d1 = c->get<double>("in.img1s", MM);
+        CK(cudaMemcpyAsync(d0, img0s, MM * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(d1, img1s, MM * 8, cudaMemcpyDefault, c->stream));
+        double* od = c->get<double>("out.dist", npairs);
+        double* ou = c->get<double>("out.dual", npairs);
+        long* oi = c->get<long>("out.iters", (size_t)npairs * prm->levels);
+        int* oc = c->get<int>("out.conv", npairs);
+        int rc = w1mg_ml_cp_batch_dev(c, npairs, m, d0, d1, prm, od, ou, oi, oc);
+        if (rc) throw Fail{rc, g_err};
+        if (distance) CK(cudaMemcpyAsync(distance, od, npairs * 8, cudaMemcpyDefault, c->stream));
+        if (dual) CK(cudaMemcpyAsync(dual, ou, npairs * 8, cudaMemcpyDefault, c->stream));
+        if (iters)
+            CK(cudaMemcpyAsync(iters, oi, (size_t)npairs * prm->levels * sizeof(long),
+                               cudaMemcpyDefault, c->stream));
+        if (converged) CK(cudaMemcpyAsync(converged, oc, npairs * 4, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,63 @@
+"""GPU parity for the cascade (Algorithm 3): device restriction (sources),
+Eq. 14/15 prolongation, per-level relative tolerances and batched pairs,
+against the C oracle's cascade on the same inputs."""
+import numpy as np
+import pytest
+
+from paper_1810_00118_b200 import instances
+from paper_1810_00118_b200 import w1mg
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_sources_match_host(oracle):
+    img0, img1 = instances.config2_images(m=128)
+    dev = w1mg.ml_sources(img0, img1, 4)
+    host = instances.ml_sources(img0, img1, 4)
+    orc = oracle.ml_sources(img0, img1, 4)
+    for d, h, o in zip(dev, host, orc):
+        scale = np.abs(h).max()
+        assert np.abs(d - h).max() <= 1e-13 * scale
+        assert np.abs(d - o).max() <= 1e-13 * scale
+        assert abs(d.sum()) <= 1e-12 * np.abs(d).sum()  # SourceField gate passes
+
+
+def test_cascade_fixed_iterations_bit_exact(oracle):
+    """Absolute tolerance < 0 disables stopping: every level runs max_iters
+    sweeps, so prolongation + sweeps must reproduce the oracle bit for bit."""
+    img0, img1 = instances.config2_images(m=64)
+    rhos = instances.ml_sources(img0, img1, 3)
+    eps = [-1.0, -1.0, -1.0]
+    rep = w1mg.ml_run(rhos, p=w1mg.PNorm.p2, eps=eps, max_iters=150)
+    ref = oracle.ml_cp_run(rhos, p=1, eps=eps, max_iters=150)
+    assert [l.iters for l in rep.levels] == [150, 150, 150]
+    assert np.array_equal(rep.flux.x_edges, ref.mx)
+    assert np.array_equal(rep.flux.y_edges, ref.my)
+    assert np.array_equal(rep.potential.values, ref.phi)
+    assert abs(rep.distance - ref.distance) <= 1e-12 * ref.distance
+
+
+def test_config2_cascade_converged(oracle):
+    """BASELINE.json configs[1]: 32->64->128->256, relative tolerance 1e-5 per
+    level; W1 within 1e-4 of the oracle cascade."""
+    img0, img1 = instances.config2_images(m=256)
+    rhos = instances.ml_sources(img0, img1, 4)
+    rep = w1mg.ml_run(rhos, p=w1mg.PNorm.p2, rel_tol=1e-5)
+    ref = oracle.ml_cp_run(rhos, p=1, rel_tol=1e-5)
+    assert rep.converged
+    assert abs(rep.distance - ref.distance) <= 1e-4 * ref.distance
+    for a, b in zip([l.iters for l in rep.levels], ref.level_iters):
+        assert abs(a - b) <= 1
+    for a, b in zip([l.eps for l in rep.levels], ref.level_eps):
+        assert a == pytest.approx(b, rel=1e-12)
+
+
+def test_batch_matches_single_pair(oracle):
+    img0s, img1s = instances.config4_pairs(0, 3, m=64)
+    dist, dual, iters, conv = w1mg.ml_run_batch(img0s, img1s, 3, p=w1mg.PNorm.p2, rel_tol=1e-5)
+    assert conv.all()
+    for b in range(3):
+        rhos = instances.ml_sources(img0s[b], img1s[b], 3)
+        ref = oracle.ml_cp_run(rhos, p=1, rel_tol=1e-5)
+        assert abs(dist[b] - ref.distance) <= 1e-4 * ref.distance
+        assert all(abs(int(a) - c) <= 1 for a, c in zip(iters[b], ref.level_iters))
