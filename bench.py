@@ -1,0 +1,479 @@
+#!/usr/bin/env python
+"""Benchmark: batched cascadic Li et al. PD on 512^2 density pairs (config 4).
+
+BASELINE.json metric: "PD cell-updates/s and time-to-converged-W1 at 512^2;
+pairs/s batched".  Workload (BASELINE.json configs[3]): pairs generated as in
+configs[2] (seeded U[0,1] noise on 512x512, Gaussian blur sigma = 8 px with
+reflect boundary, exp(4x) + 1e-6, unit mass; pair i uses seeds 2i, 2i+1),
+each solved by a 5-level CP cascade 32 -> 512 (p = 2, practical steps,
+per-level tolerance 1e-5 * R_cold,l).  A step = one batch of
+--pairs pairs (default 1024 = the whole config) solved to converged W1.
+
+value  = cell-updates/s over the whole job: sum over pairs and levels of
+         (n_l+1)^2 * sweeps_l, divided by the device time of the K timed steps
+         (max over ranks).  Inputs are resident in HBM before timing and the
+         per-step working set (GBs) exceeds the 126 MB L2.
+e2e    = the same metric through the public C-ABI call w1mg_ml_cp_batch with
+         pinned HOST images (H2D of both image stacks and D2H of every pair's
+         W1/dual/iterations inside the timed region).
+Extra: pairs_per_s, time_to_w1_512_s (one pair, device-resident), roofline of
+the fused sweep (dominant kernel), cpu_baseline (oracle port, 1 core).
+
+Multi-GPU (torchrun): the 1024 pairs are split across ranks (strong scaling,
+no collective on the data path; one barrier and a max-reduce of the timings).
+--impl reference runs the reference C++ solver (oracle/_ref, compiled from
+/root/reference) on the host cores instead, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PD cell-updates/s and time-to-converged-W1 at 512^2; pairs/s batched"
+UNIT = "cell-updates/s"
+M = 512
+LEVELS = 5
+REL_TOL = 1e-5
+
+
+def level_sizes(m=M, levels=LEVELS):
+    return [m >> (levels - 1 - l) for l in range(levels)]
+
+
+def cell_updates(iters):
+    """iters: (pairs, levels) sweeps -> sum (n_l+1)^2 * sweeps."""
+    v = np.array([(n + 1) ** 2 for n in level_sizes()], dtype=np.float64)
+    return float((np.asarray(iters, dtype=np.float64) * v[None, :]).sum())
+
+
+def alg_bytes_per_sweep(n):
+    """Compulsory HBM bytes of one fused CP sweep: read phi, rho,
+    m_x, m_y; write phi, m_x, m_y -> 8 (3V + 4E)."""
+    V = (n + 1) ** 2
+    E = n * (n + 1)
+    return 8 * (3 * V + 4 * E)
+
+
+# ------------------------------------------------------------------ inputs
+def blur_matrix(m, sigma=8.0):
+    from paper_1810_00118_b200.instances import _blur_matrix
+
+    return _blur_matrix(m, sigma)
+
+
+def make_images_gpu(first, count, device, m=M):
+    """configs[2] images for pairs first..first+count-1; the noise comes from
+    numpy.random.default_rng(seed) exactly as instances.blurred_noise_images,
+    the separable blur runs as fp64 GEMMs on the GPU (bench input synthesis
+    only, not timed)."""
+    import torch
+
+    Bm = torch.from_numpy(blur_matrix(m)).to(device)
+    out0 = torch.empty((count, m, m), dtype=torch.float64, device=device)
+    out1 = torch.empty((count, m, m), dtype=torch.float64, device=device)
+    chunk = 64
+    for s in range(0, count, chunk):
+        e = min(count, s + chunk)
+        for out, par in ((out0, 0), (out1, 1)):
+            noise = np.stack([np.random.default_rng(2 * (first + i) + par).random((m, m))
+                              for i in range(s, e)])
+            x = torch.from_numpy(noise).to(device)
+            x = torch.matmul(torch.matmul(Bm, x), Bm.T)
+            x = torch.exp(4.0 * x) + 1e-6
+            x = x / x.sum(dim=(1, 2), keepdim=True)
+            out[s:e] = x
+    torch.cuda.synchronize(device)
+    return out0, out1
+
+
+# ------------------------------------------------------------------ clocks
+REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons, loaded = [], 0.0, set(), []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                s, m_, r, u = float(parts[0]), float(parts[1]), int(parts[2], 16), float(parts[3])
+            except ValueError:
+                continue
+            mx = max(mx, m_)
+            sm.append(s)
+            if u > 0:
+                loaded.append(s)
+            for bit, name in REASONS.items():
+                if r & bit and name != "gpu_idle":
+                    reasons.add(name)
+        use = loaded or sm
+        return {"sm_mhz": statistics.median(use) if use else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ dist
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_cascade_oracle(pair, use_reference=False):
+    """One pair through the CPU cascade: the C oracle (port) or the reference
+    build (oracle/_ref cp_run per level with Eq. 14/15 warm starts restated in
+    the oracle).  Returns (W1, sweeps per level, seconds)."""
+    from oracle import Oracle, Reference
+    from paper_1810_00118_b200 import instances
+
+    a, b = instances.config4_pair(pair)
+    O = Oracle()
+    rhos = O.ml_sources(a, b, LEVELS)
+    t = time.perf_counter()
+    if not use_reference:
+        r = O.ml_cp_run(rhos, p=1, rel_tol=REL_TOL)
+        return r.distance, r.level_iters, time.perf_counter() - t
+    R = Reference()
+    its = []
+    m0 = phi0 = None
+    r = None
+    for l, rho in enumerate(rhos):
+        n = rho.shape[0] - 1
+        step = R.cp_step_size(n)
+        tol = REL_TOL * step * ((1.0 / n) ** 2 * O.compensated_sum((rho * rho).ravel()))
+        r = R.cp_run(rho, p=1, tol=tol, m0=m0, phi0=phi0, hist_cap=1)
+        its.append(r.iterations)
+        if l + 1 < len(rhos):
+            m0 = O.prolong_flux(r.mx, r.my)
+            phi0 = O.prolong_scalar(r.phi)
+    return r.distance, its, time.perf_counter() - t
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU solver on all host cores,
+    independent pairs in parallel threads (ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import have_reference
+
+    cores = os.cpu_count() or 1
+    use_ref = have_reference()
+    per_step = cores
+    rates = []
+    first = 0
+
+    def one(i):
+        return cpu_cascade_oracle(i, use_reference=use_ref)
+
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        for s in range(args.warmup + args.steps):
+            t = time.perf_counter()
+            res = list(ex.map(one, range(first, first + per_step)))
+            dt = time.perf_counter() - t
+            first += per_step
+            if s >= args.warmup:
+                cu = cell_updates([r[1] for r in res])
+                rates.append((cu, dt, per_step))
+    tot_cu = sum(r[0] for r in rates)
+    tot_t = sum(r[1] for r in rates)
+    tot_p = sum(r[2] for r in rates)
+    v = tot_cu / tot_t
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_t / max(len(rates), 1), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, per_step),
+        "pairs_per_s": tot_p / tot_t,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores,
+                         "kind": "reference" if use_ref else "port",
+                         "sample": f"{per_step} config-4 pairs per step (one per core), each a "
+                                   f"5-level CP cascade 32->512 to rel tol {REL_TOL}"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, pairs):
+    return {"workload": "config4: batched 512^2 density pairs, cascadic Li et al. PD "
+                        "32->64->128->256->512, p=2, rel tol 1e-5 per level",
+            "pairs_per_step": pairs, "grid": M, "levels": LEVELS,
+            "l2": "inputs exceed L2 (per-step state >> 126 MB); no flush needed",
+            "parallelism": f"pairs sharded over {args.gpus} GPU(s), no collective"}
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pairs", type=int, default=1024, help="pairs per step (whole job)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup()
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference_arm(args)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    from paper_1810_00118_b200 import _lib
+    from paper_1810_00118_b200._lib import MLParams, check
+    import ctypes as C
+
+    per = [args.pairs // world + (1 if r < args.pairs % world else 0) for r in range(world)]
+    first = sum(per[:rank])
+    B = per[rank]
+    img0, img1 = make_images_gpu(first, B, dev)
+
+    ctx = _lib.Context(local)
+    L = ctx.L
+    prm = MLParams()
+    prm.levels, prm.pnorm, prm.step_mode = LEVELS, 1, 1
+    prm.rel_tol, prm.eps, prm.max_iters = REL_TOL, None, 5_000_000
+    dist_d = torch.zeros(B, dtype=torch.float64, device=dev)
+    dual_d = torch.zeros(B, dtype=torch.float64, device=dev)
+    iters_d = torch.zeros((B, LEVELS), dtype=torch.int64, device=dev)
+    conv_d = torch.zeros(B, dtype=torch.int32, device=dev)
+    cstream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+
+    def step_dev():
+        check(L.w1mg_ml_cp_batch_dev(ctx.h, B, M, C.c_void_p(img0.data_ptr()),
+                                     C.c_void_p(img1.data_ptr()), C.byref(prm),
+                                     C.c_void_p(dist_d.data_ptr()), C.c_void_p(dual_d.data_ptr()),
+                                     C.c_void_p(iters_d.data_ptr()), C.c_void_p(conv_d.data_ptr())))
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        ctx.synchronize()
+        if pg:
+            pg.barrier()
+
+    def max_over_ranks(x):
+        if not pg:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if not pg:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        pg.all_reduce(t)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step_dev()
+    barrier()
+
+    # ---- timed region: device-resident inputs
+    launches0 = ctx.launches
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    cu = 0.0
+    finest_s = 0.0
+    finest_sweeps = 0.0
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(cstream)
+        for _ in range(args.steps):
+            step_dev()
+            ctx.synchronize()
+            secs = ctx.level_seconds(LEVELS)
+            it = iters_d.cpu().numpy()
+            cu += cell_updates(it)
+            finest_s += secs[-1]
+            finest_sweeps += float(it[:, -1].sum())
+        ev1.record(cstream)
+        barrier()
+    t_local = ev0.elapsed_time(ev1) * 1e-3
+    launches = ctx.launches - launches0
+    T = max_over_ranks(t_local)
+    cu_all = sum_over_ranks(cu)
+    value = cu_all / T
+    pairs_per_s = args.pairs * args.steps / T
+
+    # roofline of the fused sweep at the finest level, measured in the timed
+    # region: algorithmic bytes of every pair-sweep / device time of the
+    # finest level's sweep loop (includes early-exit launches of converged pairs)
+    hbm, peak_kind = peaks()
+    achieved = finest_sweeps * alg_bytes_per_sweep(M) / finest_s / 1e9
+
+    # ---- e2e through the public host API (pinned host buffers)
+    e2e = None
+    if not args.no_e2e:
+        h0 = torch.empty((B, M, M), dtype=torch.float64, pin_memory=True)
+        h1 = torch.empty((B, M, M), dtype=torch.float64, pin_memory=True)
+        h0.copy_(img0)
+        h1.copy_(img1)
+        od = torch.zeros(B, dtype=torch.float64, pin_memory=True)
+        ou = torch.zeros(B, dtype=torch.float64, pin_memory=True)
+        oi = torch.zeros((B, LEVELS), dtype=torch.int64, pin_memory=True)
+        oc = torch.zeros(B, dtype=torch.int32, pin_memory=True)
+        dp = C.POINTER(C.c_double)
+
+        def step_host():
+            check(L.w1mg_ml_cp_batch(ctx.h, B, M, C.cast(h0.data_ptr(), dp),
+                                     C.cast(h1.data_ptr(), dp), C.byref(prm),
+                                     C.cast(od.data_ptr(), dp), C.cast(ou.data_ptr(), dp),
+                                     C.cast(oi.data_ptr(), C.POINTER(C.c_long)),
+                                     C.cast(oc.data_ptr(), C.POINTER(C.c_int))))
+
+        step_host()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        ecu = 0.0
+        e0.record(cstream)
+        for _ in range(args.steps):
+            step_host()
+            ecu += cell_updates(oi.numpy())
+        e1.record(cstream)
+        barrier()
+        te = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
+        e2e = {"value": sum_over_ranks(ecu) / te, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * args.pairs * M * M * 8,
+               "d2h_bytes_per_step": args.pairs * (8 + 8 + 8 * LEVELS + 4),
+               "pairs_per_s": args.pairs * args.steps / te}
+        del h0, h1
+
+    # ---- single-pair time-to-converged-W1 at 512^2 (device-resident input)
+    t_single = None
+    if rank == 0:
+        one = [None]
+
+        def single():
+            check(L.w1mg_ml_cp_batch_dev(ctx.h, 1, M, C.c_void_p(img0.data_ptr()),
+                                         C.c_void_p(img1.data_ptr()), C.byref(prm),
+                                         C.c_void_p(dist_d.data_ptr()),
+                                         C.c_void_p(dual_d.data_ptr()),
+                                         C.c_void_p(iters_d.data_ptr()),
+                                         C.c_void_p(conv_d.data_ptr())))
+            ctx.synchronize()
+
+        single()
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            single()
+            ts.append(time.perf_counter() - t0)
+        t_single = min(ts)
+        one[0] = float(dist_d[0].item())
+
+    # ---- CPU baseline + per-pair parity sample (rank 0, N = 1 only)
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        w1_cpu, its_cpu, secs_cpu = cpu_cascade_oracle(0)
+        cpu = {"value": cell_updates([its_cpu]) / secs_cpu, "unit": UNIT, "cores": 1,
+               "kind": "port",
+               "sample": "config-4 pair 0 (seeds 0,1): one 5-level CP cascade 32->512 through "
+                         "the C oracle (bit-identical restatement of the reference), 1 thread",
+               "pairs_per_s": 1.0 / secs_cpu}
+        # the bench images come from GPU GEMM blur: re-solve pair 0 from the
+        # numpy images for an exact-input comparison
+        from paper_1810_00118_b200 import instances, w1mg
+
+        a, b = instances.config4_pair(0)
+        g = w1mg.ml_run_batch(a[None], b[None], LEVELS, rel_tol=REL_TOL)
+        parity = {"pair": 0, "w1_gpu": float(g[0][0]), "w1_cpu": w1_cpu,
+                  "rel_err": abs(float(g[0][0]) - w1_cpu) / w1_cpu,
+                  "sweeps_gpu": [int(x) for x in g[2][0]], "sweeps_cpu": list(its_cpu)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args, args.pairs),
+            "pairs_per_s": pairs_per_s, "time_to_w1_512_s": t_single,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None,
+                         "kernel": "w1mg_dev::cp_sweep_kernel<1> (fused PD sweep, 512^2 level)",
+                         "bytes_per_sweep": alg_bytes_per_sweep(M), "peak_kind": peak_kind},
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+            "cpu_baseline": cpu, "parity_sample": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -94,6 +94,10 @@ int w1mg_abi_version(void);
 /* Number of fused-iteration kernel launches issued by this context so far
  * (for bench.py's gpu_launches claim). */
 long w1mg_ctx_launch_count(const w1mg_ctx* ctx);
+/* Device seconds of each level of the last cascade run on this context
+ * (CUDA events; waits for that cascade).  Returns the number written, or a
+ * negative status. */
+int w1mg_ctx_level_seconds(w1mg_ctx* ctx, double* out, int cap);
 /* Block until all work queued on the context stream is done. */
 int w1mg_ctx_synchronize(w1mg_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t), for callers that time on it. */

@@ -76,6 +76,7 @@ def lib():
         L.w1mg_ctx_launch_count.argtypes = [C.c_void_p]
         L.w1mg_ctx_launch_count.restype = C.c_long
         L.w1mg_ctx_synchronize.argtypes = [C.c_void_p]
+        L.w1mg_ctx_level_seconds.argtypes = [C.c_void_p, _dp, C.c_int]
         L.w1mg_ctx_stream.argtypes = [C.c_void_p]
         L.w1mg_ctx_stream.restype = C.c_void_p
         L.w1mg_cp_step_size.argtypes = [C.c_int, C.c_int]
@@ -154,6 +155,13 @@ class Context:
     @property
     def stream(self) -> int:
         return int(self.L.w1mg_ctx_stream(self.h) or 0)
+
+    def level_seconds(self, levels: int):
+        out = np.zeros(levels)
+        n = self.L.w1mg_ctx_level_seconds(self.h, ptr(out), levels)
+        if n < 0:
+            check(-n)
+        return out[:n].tolist()
 
     def synchronize(self):
         check(self.L.w1mg_ctx_synchronize(self.h))

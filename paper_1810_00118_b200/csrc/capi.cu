@@ -82,6 +82,8 @@ struct w1mg_ctx {
     int* pinned = nullptr;  // 2 ints for the done-count pipeline
     cudaEvent_t ev[2] = {nullptr, nullptr};
     cudaEvent_t t0 = nullptr, t1 = nullptr;
+    std::vector<cudaEvent_t> lev_ev;  // start/end per level of the last cascade
+    int lev_count = 0;
     long launches = 0;
     int num_sms = 148;
 
@@ -221,8 +223,10 @@ void reduce_pairs(w1mg_ctx* c, F f, int w, int rows, int B, double s1, double s2
     if (G < 1) G = 1;
     double2* part = c->get<double2>("reduce.partial", (size_t)G * B);
     node_reduce_kernel<F><<<dim3(G, B), kRedThreads, 0, c->stream>>>(f, w, rows, part);
+    ++c->launches;
     CK(cudaGetLastError());
     reduce_finish_kernel<<<B, 32, 0, c->stream>>>(part, G, s1, s2, out);
+    ++c->launches;
     CK(cudaGetLastError());
 }
 
@@ -294,6 +298,7 @@ void init_level_ctl(w1mg_ctx* c, const Level& lv, double rel_tol, double abs_tol
     }
     init_ctl_kernel<<<(lv.B + 127) / 128, 128, 0, c->stream>>>(lv.ctl, lv.B, rs, rel_scale,
                                                                  abs_tol, max_it, lv.ndone);
+    ++c->launches;
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(lv.ticket, 0, sizeof(unsigned) * lv.B, c->stream));
 }
@@ -331,14 +336,17 @@ void build_sources(w1mg_ctx* c, std::vector<Level>& lv, const double* img0, cons
         const Level& L = lv[l];
         const int n = L.n;
         image_to_nodes_kernel<<<node_grid(n, B, blk), blk, 0, c->stream>>>(a, b, L.base, L.L, PHI1, MX1);
+        ++c->launches;
         CK(cudaGetLastError());
         reduce_pairs(c, FSlot{L.base, L.L, PHI1}, n + 1, n + 1, B, 1.0, 1.0, sa);
         reduce_pairs(c, FSlot{L.base, L.L, MX1}, n + 1, n + 1, B, 1.0, 1.0, sb);
         const double h = 1.0 / n;
         make_source_kernel<<<node_grid(n, B, blk), blk, 0, c->stream>>>(L.base, L.L, PHI1, MX1, sa, sb, h * h);
+        ++c->launches;
         CK(cudaGetLastError());
         reduce_pairs(c, FSlot{L.base, L.L, RHO}, n + 1, n + 1, B, 1.0, 1.0, sm);
         center_source_kernel<<<node_grid(n, B, blk), blk, 0, c->stream>>>(L.base, L.L, sm, PHI1, MX1);
+        ++c->launches;
         CK(cudaGetLastError());
         if (l > 0) {
             const int mc = n / 2;
@@ -347,7 +355,9 @@ void build_sources(w1mg_ctx* c, std::vector<Level>& lv, const double* img0, cons
             long total = (long)B * mc * mc;
             int nb = (int)std::min<long>((total + 255) / 256, 65535L * 4);
             block_sum_kernel<<<nb, 256, 0, c->stream>>>(a, ca, n, B);
+            ++c->launches;
             block_sum_kernel<<<nb, 256, 0, c->stream>>>(b, cb, n, B);
+            ++c->launches;
             CK(cudaGetLastError());
             a = ca;
             b = cb;
@@ -356,37 +366,48 @@ void build_sources(w1mg_ctx* c, std::vector<Level>& lv, const double* img0, cons
     (void)m;
 }
 
-struct CascadeOut {
-    std::vector<double> seconds;
-};
+// device time of each level of the last cascade (waits for it to finish)
+void level_seconds(w1mg_ctx* c, std::vector<double>& out) {
+    out.clear();
+    if (c->lev_count == 0) return;
+    CK(cudaEventSynchronize(c->lev_ev[2 * c->lev_count - 1]));
+    for (int l = 0; l < c->lev_count; ++l) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->lev_ev[2 * l], c->lev_ev[2 * l + 1]));
+        out.push_back(ms * 1e-3);
+    }
+}
 
 // Cascade over prepared levels (sources in RHO, level 0 zero state).
 void run_cascade(w1mg_ctx* c, std::vector<Level>& lv, const w1mg_ml_params& p, long* iters_dev,
                  double* fpr_dev, double* tol_dev, std::vector<double>* secs) {
     const int levels = (int)lv.size();
     dim3 blk(32, 8);
+    while ((int)c->lev_ev.size() < 2 * levels) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->lev_ev.push_back(e);
+    }
+    c->lev_count = levels;
     for (int l = 0; l < levels; ++l) {
         Level& L = lv[l];
         if (l > 0) {
             prolong_kernel<<<node_grid(L.n, L.B, blk), blk, 0, c->stream>>>(
                 lv[l - 1].base, lv[l - 1].L, lv[l - 1].ctl, L.base, L.L);
+                ++c->launches;
             CK(cudaGetLastError());
         }
         const double abs_tol = (p.rel_tol > 0 || !p.eps) ? 0.0 : p.eps[l];
-        CK(cudaEventRecord(c->t0, c->stream));
+        CK(cudaEventRecord(c->lev_ev[2 * l], c->stream));
         init_level_ctl(c, L, p.rel_tol, abs_tol, p.max_iters);
         run_sweeps(c, L, p.pnorm, p.max_iters);
-        CK(cudaEventRecord(c->t1, c->stream));
+        CK(cudaEventRecord(c->lev_ev[2 * l + 1], c->stream));
         harvest_kernel<<<(L.B + 127) / 128, 128, 0, c->stream>>>(L.ctl, L.B, l, levels, iters_dev,
                                                                    fpr_dev, tol_dev);
+        ++c->launches;
         CK(cudaGetLastError());
-        if (secs) {
-            CK(cudaEventSynchronize(c->t1));
-            float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, c->t0, c->t1));
-            secs->push_back(ms * 1e-3);
-        }
     }
+    if (secs) level_seconds(c, *secs);
 }
 
 std::vector<Level> make_levels(w1mg_ctx* c, const std::string& tag, int n_finest, int levels,
@@ -451,6 +472,7 @@ void w1mg_ctx_destroy(w1mg_ctx* c) {
     if (c->pinned) cudaFreeHost(c->pinned);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : c->lev_ev) cudaEventDestroy(e);
     if (c->t0) cudaEventDestroy(c->t0);
     if (c->t1) cudaEventDestroy(c->t1);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -458,6 +480,16 @@ void w1mg_ctx_destroy(w1mg_ctx* c) {
 }
 
 long w1mg_ctx_launch_count(const w1mg_ctx* c) { return c ? c->launches : 0; }
+
+int w1mg_ctx_level_seconds(w1mg_ctx* c, double* out, int cap) {
+    int n = 0;
+    int rc = guard([&] {
+        std::vector<double> s;
+        level_seconds(c, s);
+        for (; n < cap && n < (int)s.size(); ++n) out[n] = s[n];
+    });
+    return rc ? -rc : n;
+}
 
 int w1mg_ctx_synchronize(w1mg_ctx* c) {
     return guard([&] { CK(cudaStreamSynchronize(c->stream)); });
@@ -518,6 +550,7 @@ int w1mg_divergence(w1mg_ctx* c, int n, const double* mx, const double* my, doub
         CK(cudaMemcpyAsync(dy, my, E * 8, cudaMemcpyDefault, c->stream));
         dim3 blk(32, 8);
         divergence_ref_kernel<<<node_grid(n, 1, blk), blk, 0, c->stream>>>(n, dx, dy, dv);
+        ++c->launches;
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(out, dv, V * 8, cudaMemcpyDefault, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -534,6 +567,7 @@ int w1mg_adjoint(w1mg_ctx* c, int n, const double* phi, double* gx, double* gy) 
         CK(cudaMemcpyAsync(dp, phi, V * 8, cudaMemcpyDefault, c->stream));
         dim3 blk(32, 8);
         adjoint_ref_kernel<<<node_grid(n, 1, blk), blk, 0, c->stream>>>(n, dp, dx, dy);
+        ++c->launches;
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(gx, dx, E * 8, cudaMemcpyDefault, c->stream));
         CK(cudaMemcpyAsync(gy, dy, E * 8, cudaMemcpyDefault, c->stream));
@@ -674,11 +708,15 @@ int w1mg_cp_residual(w1mg_ctx* c, int n, const double* cmx, const double* cmy,
         CK(cudaMemcpyAsync(p0, cphi, V * 8, cudaMemcpyDefault, c->stream));
         CK(cudaMemcpyAsync(p1, pphi, V * 8, cudaMemcpyDefault, c->stream));
         sub_inplace_kernel<<<(int)((E + 255) / 256), 256, 0, c->stream>>>(a0, b0, (long)E);
+        ++c->launches;
         sub_inplace_kernel<<<(int)((E + 255) / 256), 256, 0, c->stream>>>(a1, b1, (long)E);
+        ++c->launches;
         sub_inplace_kernel<<<(int)((V + 255) / 256), 256, 0, c->stream>>>(p0, p1, (long)V);
+        ++c->launches;
         CK(cudaGetLastError());
         dim3 blk(32, 8);
         divergence_ref_kernel<<<node_grid(n, 1, blk), blk, 0, c->stream>>>(n, a0, a1, adm);
+        ++c->launches;
         CK(cudaGetLastError());
         const double h = 1.0 / n;
         reduce_pairs(c, FRefDot{a0, a0, n}, n, n + 1, 1, 1.0, 1.0, r);
@@ -798,6 +836,7 @@ int w1mg_ml_cp_batch_dev(w1mg_ctx* c, int npairs, int m, const double* img0s,
         level_values(c, lv.back(), prm->pnorm, distance, dual);
         if (converged) {
             converged_kernel<<<(npairs + 127) / 128, 128, 0, c->stream>>>(lv.back().ctl, npairs, converged);
+            ++c->launches;
             CK(cudaGetLastError());
         }
     });
