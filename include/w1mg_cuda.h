@@ -174,6 +174,17 @@ int w1mg_ml_cp_batch_dev(w1mg_ctx* ctx, int npairs, int m, const double* img0s_d
                          double* distance_dev, double* dual_dev, long* iters_dev,
                          int* converged_dev);
 
+/* --------------------------------------------------------------- probes */
+/* Select the load engine of the fused sweep for subsequent launches in this
+ * process: 0 = register-pipelined LDG, 1 = TMA bulk-copy ring (default).
+ * Also settable with the environment variable W1MG_SWEEP=ldg|tma. */
+int w1mg_set_sweep_engine(int engine);
+/* Times the fused sweep kernel alone: `iters` sweeps over B pairs of an
+ * n-cell level (synthetic source, stop rule off) after `warm` untimed ones;
+ * writes the mean milliseconds per sweep launch (CUDA events). */
+int w1mg_sweep_probe(w1mg_ctx* ctx, int n, int B, int pnorm, long warm, long iters,
+                     double* ms_per_sweep);
+
 #ifdef __cplusplus
 }
 #endif

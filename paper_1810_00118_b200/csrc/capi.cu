@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -230,8 +231,18 @@ void reduce_pairs(w1mg_ctx* c, F f, int w, int rows, int B, double s1, double s2
     CK(cudaGetLastError());
 }
 
+int g_sweep_variant = kTma;  // engine for the fused sweep (W1MG_SWEEP=ldg|tma)
+
 void launch_sweep(const Level& lv, int pn, int parity, cudaStream_t s) {
     dim3 blk(kSweepWarps * 32);
+    if (g_sweep_variant == kTma) {
+        switch (pn) {
+            case 0: cp_sweep_tma_kernel<0><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
+            case 1: cp_sweep_tma_kernel<1><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
+            default: cp_sweep_tma_kernel<2><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
+        }
+        return;
+    }
     switch (pn) {
         case 0: cp_sweep_kernel<0><<<lv.grid, blk, 0, s>>>(lv.args, parity); break;
         case 1: cp_sweep_kernel<1><<<lv.grid, blk, 0, s>>>(lv.args, parity); break;
@@ -242,7 +253,7 @@ void launch_sweep(const Level& lv, int pn, int parity, cudaStream_t s) {
 cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
     std::string key(reinterpret_cast<const char*>(&lv.args), sizeof(SweepArgs));
     key += std::to_string(pn) + ":" + std::to_string(K) + ":" + std::to_string(lv.grid.x) + ":" +
-           std::to_string(lv.grid.y);
+           std::to_string(lv.grid.y) + ":v" + std::to_string(g_sweep_variant);
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) return it->second;
     cudaGraph_t g;
@@ -450,6 +461,8 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         int major = 0;
         CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
         if (major < 10) fail(W1MG_ECUDA, "this build targets sm_100a (B200)");
+        if (const char* v = std::getenv("W1MG_SWEEP"))
+            g_sweep_variant = (std::string(v) == "ldg") ? kLdg : kTma;
         auto* c = new w1mg_ctx();
         c->device = device;
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -866,6 +879,41 @@ int w1mg_ml_cp_batch(w1mg_ctx* c, int npairs, int m, const double* img0s, const 
                                cudaMemcpyDefault, c->stream));
         if (converged) CK(cudaMemcpyAsync(converged, oc, npairs * 4, cudaMemcpyDefault, c->stream));
         CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// Kernel probe: `iters` fused sweeps on B pairs of an n-cell level with the
+// stop rule disabled, after `warm` untimed sweeps; returns ms per sweep.
+int w1mg_set_sweep_engine(int engine) {
+    if (engine != kLdg && engine != kTma) return W1MG_EINVAL;
+    g_sweep_variant = engine;
+    return W1MG_OK;
+}
+
+int w1mg_sweep_probe(w1mg_ctx* c, int n, int B, int pnorm, long warm, long iters,
+                     double* ms_per_sweep) {
+    return guard([&] {
+        check_n(n);
+        check_pnorm(pnorm);
+        const double step = w1mg_cp_step_size(n, W1MG_STEP_PRACTICAL);
+        Level lv = make_level(c, "probe", n, B, step, step, nullptr, 0);
+        zero_level(c, lv);
+        dim3 blk(32, 8);
+        probe_fill_kernel<<<node_grid(n, B, blk), blk, 0, c->stream>>>(lv.base, lv.L);
+        ++c->launches;
+        CK(cudaGetLastError());
+        init_level_ctl(c, lv, 0.0, -1.0, warm + iters + 64);
+        long k = 0;
+        for (; k < warm; ++k) launch_sweep(lv, pnorm, (int)(k & 1), c->stream);
+        CK(cudaEventRecord(c->t0, c->stream));
+        for (long t = 0; t < iters; ++t, ++k) launch_sweep(lv, pnorm, (int)(k & 1), c->stream);
+        CK(cudaEventRecord(c->t1, c->stream));
+        CK(cudaGetLastError());
+        c->launches += warm + iters;
+        CK(cudaEventSynchronize(c->t1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->t0, c->t1));
+        *ms_per_sweep = ms / (double)iters;
     });
 }
 

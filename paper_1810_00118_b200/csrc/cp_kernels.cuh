@@ -14,10 +14,15 @@
 // up the rows keeping the previous row's y-flux in registers.  Lane 0 is the
 // left halo column (its m^{k+1} feeds the owned lane 1 through a shuffle),
 // lanes 1..31 own nodes.  The row below the strip is recomputed once at the
-// strip start.  phi(i+1, j) arrives by shuffle from the right neighbour lane
-// (lane 31 loads it).  No shared memory and no block barrier on the data
-// path; the residual is a warp-shuffle -> block -> last-block tree with a
-// fixed order, so it is deterministic run to run.
+// strip start.  No block barrier on the data path; the residual is a
+// warp-shuffle -> block -> last-block tree with a fixed order, so it is
+// deterministic run to run.
+//
+// Two load engines feed the march:
+//   * kLdg: register double-buffering of plain LDGs one row ahead;
+//   * kTma: per-warp ring of kStages row chunks in shared memory filled by
+//     cp.async.bulk (TMA bulk copies, one elected lane, mbarrier complete_tx),
+//     so kStages rows of look-ahead cost no registers.
 //
 // The last block of each pair (atomic ticket) finalises R^k, appends it to
 // the residual history, and sets the pair's stop flag when R^k < tol or the
@@ -59,6 +64,13 @@ struct SweepArgs {
 
 constexpr int kSweepWarps = 8;  // warps per block
 constexpr int kOwn = 31;        // owned columns per warp
+constexpr int kLdg = 0;
+constexpr int kTma = 1;
+constexpr int kStages = 4;      // TMA ring depth (rows of look-ahead)
+constexpr int kChunk = 36;      // doubles per row chunk: 33 needed, 16-B aligned start
+constexpr int kStreams = 4;     // phi(j+1), m_x(j), m_y(j), rho(j)
+constexpr int kStageBytes = kStreams * kChunk * 8;
+constexpr int kTmaSmem = kSweepWarps * (kStages * kStageBytes + kStages * 8);
 
 // One node of the m-update: returns the new flux and its increment, zero for
 // absent components (solver_cp.cpp:39-54; absent components enter shrink as 0).
@@ -75,103 +87,99 @@ __device__ __forceinline__ void node_flux(bool hx, bool hy, double pc, double pr
     uy = hy ? uy : 0.0;
 }
 
+// Everything a warp needs about its strip.
+struct Strip {
+    int i, j0, j1;
+    bool in, hx, own;
+    const double* phr;
+    const double* mxr;
+    const double* myr;
+    const double* rho;
+    double* phw;
+    double* mxw;
+    double* myw;
+};
+
+__device__ __forceinline__ Strip make_strip(const SweepArgs& a, int pair, int parity, int tile,
+                                            int lane) {
+    Strip s;
+    const Layout& L = a.L;
+    const int cx = tile % a.ncx;
+    const int sy = tile / a.ncx;
+    s.i = cx * kOwn - 1 + lane;
+    s.j0 = sy * a.H;
+    s.j1 = min(s.j0 + a.H, L.n + 1);
+    double* pb = a.base + (long)pair * NSLOT * L.plane;
+    s.phr = pb + (PHI0 + parity) * L.plane;
+    s.mxr = pb + (MX0 + parity) * L.plane;
+    s.myr = pb + (MY0 + parity) * L.plane;
+    s.rho = pb + RHO * L.plane;
+    s.phw = pb + (PHI0 + 1 - parity) * L.plane;
+    s.mxw = pb + (MX0 + 1 - parity) * L.plane;
+    s.myw = pb + (MY0 + 1 - parity) * L.plane;
+    s.in = (s.i >= 0) && (s.i <= L.n);
+    s.hx = (s.i >= 0) && (s.i < L.n);
+    s.own = (lane > 0) && s.in;
+    return s;
+}
+
+// y-flux (and its increment) of the row below the strip, recomputed once.
 template <int PN>
-__global__ void __launch_bounds__(kSweepWarps * 32)
-cp_sweep_kernel(const SweepArgs a, const int parity) {
-    const int pair = blockIdx.y;
-    PairCtl* ctl = a.ctl + pair;
-    if (*(volatile int*)&ctl->done) return;
+__device__ __forceinline__ void below_row(const SweepArgs& a, const Strip& s, int lane,
+                                          double& uyb, double& dyb) {
+    uyb = 0.0;
+    dyb = 0.0;
+    if (s.j0 == 0) return;
+    const Layout& L = a.L;
+    const long o = L.at(s.i, s.j0 - 1);
+    double pc = s.in ? __ldg(s.phr + o) : 0.0;
+    double pu = s.in ? __ldg(s.phr + o + L.pitch) : 0.0;
+    double pr = __shfl_down_sync(0xffffffffu, pc, 1);
+    if (lane == 31) pr = s.hx ? __ldg(s.phr + o + 1) : 0.0;
+    double mxo = s.hx ? __ldg(s.mxr + o) : 0.0;
+    double myo = s.in ? __ldg(s.myr + o) : 0.0;
+    double ux, uy, dx, dy;
+    node_flux<PN>(s.hx, s.in, pc, pr, pu, mxo, myo, a.mu, a.ih, ux, uy, dx, dy);
+    uyb = uy;
+    dyb = dy;
+}
 
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int tile = blockIdx.x * kSweepWarps + warp;
-    const Layout L = a.L;
-    const int n = L.n;
-    const int P = L.pitch;
-    const double mu = a.mu, tau = a.tau, ih = a.ih;
-
-    double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
-
-    if (tile < a.ntiles) {
-        const int cx = tile % a.ncx;
-        const int sy = tile / a.ncx;
-        const int i = cx * kOwn - 1 + lane;
-        const int j0 = sy * a.H;
-        const int j1 = min(j0 + a.H, n + 1);
-
-        double* pb = a.base + (long)pair * NSLOT * L.plane;
-        const double* __restrict__ phr = pb + (PHI0 + parity) * L.plane;
-        const double* __restrict__ mxr = pb + (MX0 + parity) * L.plane;
-        const double* __restrict__ myr = pb + (MY0 + parity) * L.plane;
-        const double* __restrict__ rho = pb + RHO * L.plane;
-        double* __restrict__ phw = pb + (PHI0 + 1 - parity) * L.plane;
-        double* __restrict__ mxw = pb + (MX0 + 1 - parity) * L.plane;
-        double* __restrict__ myw = pb + (MY0 + 1 - parity) * L.plane;
-
-        const bool in = (i >= 0) && (i <= n);
-        const bool hx = (i >= 0) && (i < n);
-        const bool own = (lane > 0) && in;
-        const long c0 = L.at(i, 0);  // column offset; row j adds j*P
-
-        // y-flux (and its increment) of the row below the strip.
-        double uyb = 0.0, dyb = 0.0;
-        if (j0 > 0) {
-            const long o = c0 + (long)(j0 - 1) * P;
-            double pc = in ? __ldg(phr + o) : 0.0;
-            double pu = in ? __ldg(phr + o + P) : 0.0;
-            double pr = __shfl_down_sync(0xffffffffu, pc, 1);
-            if (lane == 31) pr = hx ? __ldg(phr + o + 1) : 0.0;
-            double mxo = hx ? __ldg(mxr + o) : 0.0;
-            double myo = in ? __ldg(myr + o) : 0.0;
-            double ux, uy, dx, dy;
-            node_flux<PN>(hx, in, pc, pr, pu, mxo, myo, mu, ih, ux, uy, dx, dy);
-            uyb = uy;
-            dyb = dy;
-        }
-
-        long o = c0 + (long)j0 * P;
-        double pc = in ? __ldg(phr + o) : 0.0;
-        double pr = __shfl_down_sync(0xffffffffu, pc, 1);
-        if (lane == 31) pr = hx ? __ldg(phr + o + 1) : 0.0;
-
-        for (int j = j0; j < j1; ++j, o += P) {
-            const bool hy = in && (j < n);
-            // loads for this row (m^k, rho) and the next potential row
-            double pu = hy ? __ldg(phr + o + P) : 0.0;
-            double pur = (lane == 31 && hx && j < n) ? __ldg(phr + o + P + 1) : 0.0;
-            double mxo = hx ? __ldg(mxr + o) : 0.0;
-            double myo = hy ? __ldg(myr + o) : 0.0;
-            double r = in ? __ldg(rho + o) : 0.0;
-
-            double ux, uy, dx, dy;
-            node_flux<PN>(hx, hy, pc, pr, pu, mxo, myo, mu, ih, ux, uy, dx, dy);
-            double uxl = __shfl_up_sync(0xffffffffu, ux, 1);
-            double dxl = __shfl_up_sync(0xffffffffu, dx, 1);
-
-            // divergence_into x pass then y pass (grid.cpp:52-65)
-            double divm = (ux - uxl) * ih + (uy - uyb) * ih;
-            double divd = (dx - dxl) * ih + (dy - dyb) * ih;
-            double d = tau * (divm + divd - r);
-            if (own) {
-                phw[o] = pc + d;
-                if (hx) mxw[o] = ux;
-                if (hy) myw[o] = uy;
-                s_dm2 += dx * dx + dy * dy;
-                s_dp2 += d * d;
-                s_cr += d * divd;
-            }
-            uyb = uy;
-            dyb = dy;
-            // advance the potential window one row up
-            double nr = __shfl_down_sync(0xffffffffu, pu, 1);
-            pr = (lane == 31) ? pur : nr;
-            pc = pu;
-        }
+// One row of the march: m-update at (i, j), left-neighbour exchange,
+// divergence of m^{k+1} and dm (grid.cpp:52-65 order), phi-update.
+template <int PN>
+__device__ __forceinline__ void row_update(const SweepArgs& a, const Strip& s, int j, long o,
+                                           double pc, double pr, double pu, double mxo,
+                                           double myo, double r, double& uyb, double& dyb,
+                                           double& s_dm2, double& s_dp2, double& s_cr) {
+    const bool hy = s.in && (j < a.L.n);
+    const double ih = a.ih;
+    double ux, uy, dx, dy;
+    node_flux<PN>(s.hx, hy, pc, pr, pu, mxo, myo, a.mu, ih, ux, uy, dx, dy);
+    double uxl = __shfl_up_sync(0xffffffffu, ux, 1);
+    double dxl = __shfl_up_sync(0xffffffffu, dx, 1);
+    double divm = (ux - uxl) * ih + (uy - uyb) * ih;
+    double divd = (dx - dxl) * ih + (dy - dyb) * ih;
+    double d = a.tau * (divm + divd - r);
+    if (s.own) {
+        s.phw[o] = pc + d;
+        if (s.hx) s.mxw[o] = ux;
+        if (hy) s.myw[o] = uy;
+        s_dm2 += dx * dx + dy * dy;
+        s_dp2 += d * d;
+        s_cr += d * divd;
     }
+    uyb = uy;
+    dyb = dy;
+}
 
-    // ---- deterministic residual reduction
+// Block + last-block reduction of the three residual sums; the last block of
+// a pair finalises R^k and the stop flag (solver_cp.cpp:70, :128-136).
+__device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int parity,
+                                             double s_dm2, double s_dp2, double s_cr) {
     __shared__ double red[kSweepWarps][3];
     __shared__ bool is_last;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     s_dm2 = warp_sum(s_dm2);
     s_dp2 = warp_sum(s_dp2);
     s_cr = warp_sum(s_cr);
@@ -202,7 +210,6 @@ cp_sweep_kernel(const SweepArgs a, const int parity) {
     if (!is_last) return;
     __threadfence();
 
-    // last block of this pair: fixed-order sum of the block partials
     double t0 = 0.0, t1 = 0.0, t2 = 0.0;
     for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
         const volatile double* pv = part + b * 3;
@@ -227,7 +234,8 @@ cp_sweep_kernel(const SweepArgs a, const int parity) {
             sdp2 += red[w][1];
             scr += red[w][2];
         }
-        double fpr = a.h2 * (sdm2 / mu + sdp2 / a.tau - 2.0 * scr);
+        PairCtl* ctl = a.ctl + pair;
+        double fpr = a.h2 * (sdm2 / a.mu + sdp2 / a.tau - 2.0 * scr);
         long k = ctl->it;
         if (a.hist && k < a.hist_cap) a.hist[(long)pair * a.hist_cap + k] = fpr;
         ctl->it = k + 1;
@@ -242,6 +250,167 @@ cp_sweep_kernel(const SweepArgs a, const int parity) {
         a.ticket[pair] = 0u;
         __threadfence();
     }
+}
+
+// ------------------------------------------------------------ kLdg engine
+template <int PN>
+__global__ void __launch_bounds__(kSweepWarps * 32)
+cp_sweep_kernel(const SweepArgs a, const int parity) {
+    const int pair = blockIdx.y;
+    if (*(volatile int*)&a.ctl[pair].done) return;
+    const int lane = threadIdx.x & 31;
+    const int tile = blockIdx.x * kSweepWarps + (threadIdx.x >> 5);
+    double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
+
+    if (tile < a.ntiles) {
+        const Strip s = make_strip(a, pair, parity, tile, lane);
+        const Layout L = a.L;
+        const int n = L.n;
+        const int P = L.pitch;
+        double uyb, dyb;
+        below_row<PN>(a, s, lane, uyb, dyb);
+
+        long o = L.at(s.i, s.j0);
+        double pc = s.in ? __ldg(s.phr + o) : 0.0;
+        double pr = __shfl_down_sync(0xffffffffu, pc, 1);
+        if (lane == 31) pr = s.hx ? __ldg(s.phr + o + 1) : 0.0;
+
+        const bool l31 = (lane == 31) && s.hx;
+        double n_pu, n_pur, n_mx, n_my, n_r;
+        {
+            const bool hy = s.in && (s.j0 < n);
+            n_pu = hy ? __ldg(s.phr + o + P) : 0.0;
+            n_pur = (l31 && s.j0 < n) ? __ldg(s.phr + o + P + 1) : 0.0;
+            n_mx = s.hx ? __ldg(s.mxr + o) : 0.0;
+            n_my = hy ? __ldg(s.myr + o) : 0.0;
+            n_r = s.in ? __ldg(s.rho + o) : 0.0;
+        }
+        for (int j = s.j0; j < s.j1; ++j, o += P) {
+            const double pu = n_pu, pur = n_pur, mxo = n_mx, myo = n_my, r = n_r;
+            if (j + 1 < s.j1) {  // loads of row j+1 overlap row j's math
+                const long q = o + P;
+                const bool hy1 = s.in && (j + 1 < n);
+                n_pu = hy1 ? __ldg(s.phr + q + P) : 0.0;
+                n_pur = (l31 && j + 1 < n) ? __ldg(s.phr + q + P + 1) : 0.0;
+                n_mx = s.hx ? __ldg(s.mxr + q) : 0.0;
+                n_my = hy1 ? __ldg(s.myr + q) : 0.0;
+                n_r = s.in ? __ldg(s.rho + q) : 0.0;
+            }
+            row_update<PN>(a, s, j, o, pc, pr, pu, mxo, myo, r, uyb, dyb, s_dm2, s_dp2, s_cr);
+            double nr = __shfl_down_sync(0xffffffffu, pu, 1);
+            pr = (lane == 31) ? pur : nr;
+            pc = pu;
+        }
+    }
+    finish_sweep(a, pair, parity, s_dm2, s_dp2, s_cr);
+}
+
+// ------------------------------------------------------------ kTma engine
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "W1MG_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra W1MG_WAIT;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int PN>
+__global__ void __launch_bounds__(kSweepWarps * 32, 3)
+cp_sweep_tma_kernel(const SweepArgs a, const int parity) {
+    const int pair = blockIdx.y;
+    if (*(volatile int*)&a.ctl[pair].done) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int tile = blockIdx.x * kSweepWarps + warp;
+    // per-warp ring: kStages x [kStreams][kChunk] doubles, then kStages mbarriers
+    double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * kStages * kStreams * kChunk;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kSweepWarps * kStages * kStageBytes) +
+                     warp * kStages;
+    double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
+
+    if (tile < a.ntiles) {
+        const Strip s = make_strip(a, pair, parity, tile, lane);
+        const Layout L = a.L;
+        const int P = L.pitch;
+        // chunk start: column i of lane 0 rounded down to even (16-B aligned;
+        // rows are 256-B aligned and the front pad keeps column -2 in bounds)
+        const int ilo = s.i - lane;             // column of lane 0
+        const int a0 = ilo & ~1;
+        const int sh = ilo - a0;                // 0 or 1
+        const long c0 = L.at(a0, 0);
+
+        if (lane == 0) {
+#pragma unroll
+            for (int t = 0; t < kStages; ++t) mbar_init(&bars[t], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        auto issue = [&](int st, int row) {
+            double* dst = ring + st * kStreams * kChunk;
+            const long orow = c0 + (long)row * P;
+            mbar_expect_tx(&bars[st], kStageBytes);
+            bulk_g2s(dst + 0 * kChunk, s.phr + orow + P, kChunk * 8, &bars[st]);
+            bulk_g2s(dst + 1 * kChunk, s.mxr + orow, kChunk * 8, &bars[st]);
+            bulk_g2s(dst + 2 * kChunk, s.myr + orow, kChunk * 8, &bars[st]);
+            bulk_g2s(dst + 3 * kChunk, s.rho + orow, kChunk * 8, &bars[st]);
+        };
+        const int rows = s.j1 - s.j0;
+        if (lane == 0) {
+            for (int t = 0; t < kStages && t < rows; ++t) issue(t, s.j0 + t);
+        }
+
+        double uyb, dyb;
+        below_row<PN>(a, s, lane, uyb, dyb);
+        long o = L.at(s.i, s.j0);
+        double pc = s.in ? __ldg(s.phr + o) : 0.0;
+        double pr = __shfl_down_sync(0xffffffffu, pc, 1);
+        if (lane == 31) pr = s.hx ? __ldg(s.phr + o + 1) : 0.0;
+
+        for (int t = 0; t < rows; ++t, o += P) {
+            const int j = s.j0 + t;
+            const int st = t % kStages;
+            mbar_wait(&bars[st], (uint32_t)((t / kStages) & 1));
+            const double* c = ring + st * kStreams * kChunk + sh + lane;
+            const bool hy = s.in && (j < L.n);
+            const double pu = hy ? c[0] : 0.0;
+            const double pur = (s.hx && j < L.n) ? c[1] : 0.0;
+            const double mxo = s.hx ? c[kChunk] : 0.0;
+            const double myo = hy ? c[2 * kChunk] : 0.0;
+            const double r = s.in ? c[3 * kChunk] : 0.0;
+            __syncwarp();
+            if (lane == 0 && t + kStages < rows) {
+                // all lanes have read the stage: hand it back to the async proxy
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(st, j + kStages);
+            }
+            row_update<PN>(a, s, j, o, pc, pr, pu, mxo, myo, r, uyb, dyb, s_dm2, s_dp2, s_cr);
+            pr = pur;
+            pc = pu;
+        }
+    }
+    finish_sweep(a, pair, parity, s_dm2, s_dp2, s_cr);
 }
 
 }  // namespace w1mg_dev

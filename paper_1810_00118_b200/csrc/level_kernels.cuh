@@ -318,3 +318,18 @@ struct FRefPrimal {
 };
 
 }  // namespace w1mg_dev
+
+namespace w1mg_dev {
+// Deterministic synthetic source for kernel probes (not a solver input path):
+// a smooth zero-mean-ish pattern per pair.
+__global__ void probe_fill_kernel(double* base, Layout L) {
+    const int n = L.n;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y * blockDim.y + threadIdx.y;
+    const int b = blockIdx.z;
+    if (i > n || j > n) return;
+    double x = (double)i / n, y = (double)j / n;
+    double v = sin(6.283185307179586 * (x + 0.37 * b)) * cos(3.141592653589793 * (2.0 * y + 0.11 * b));
+    base[((long)b * NSLOT + RHO) * L.plane + L.at(i, j)] = v * n * n * 1e-3;
+}
+}  // namespace w1mg_dev
