@@ -7,7 +7,8 @@ configs[2] (seeded U[0,1] noise on 512x512, Gaussian blur sigma = 8 px with
 reflect boundary, exp(4x) + 1e-6, unit mass; pair i uses seeds 2i, 2i+1),
 each solved by a 5-level CP cascade 32 -> 512 (p = 2, practical steps,
 per-level tolerance 1e-5 * R_cold,l).  A step = one batch of
---pairs pairs (default 1024 = the whole config) solved to converged W1.
+--pairs pairs per GPU (default 256, a quarter of the 1024-pair config, so the
+default run ends in minutes) solved to converged W1.
 
 value  = cell-updates/s over the whole job: sum over pairs and levels of
          (n_l+1)^2 * sweeps_l, divided by the device time of the K timed steps
@@ -19,8 +20,9 @@ e2e    = the same metric through the public C-ABI call w1mg_ml_cp_batch with
 Extra: pairs_per_s, time_to_w1_512_s (one pair, device-resident), roofline of
 the fused sweep (dominant kernel), cpu_baseline (oracle port, 1 core).
 
-Multi-GPU (torchrun): the 1024 pairs are split across ranks (strong scaling,
-no collective on the data path; one barrier and a max-reduce of the timings).
+Multi-GPU (torchrun): every rank solves its own --pairs pairs (distinct seeds;
+weak scaling, no collective on the data path; one barrier and a max-reduce of
+the timings).
 --impl reference runs the reference C++ solver (oracle/_ref, compiled from
 /root/reference) on the host cores instead, rank 0 only.
 """
@@ -241,7 +243,7 @@ def run_reference_arm(args):
         "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot_t / max(len(rates), 1), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, per_step),
         "pairs_per_s": tot_p / tot_t,
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores,
@@ -258,7 +260,7 @@ def workload_config(args, pairs):
                         "32->64->128->256->512, p=2, rel tol 1e-5 per level",
             "pairs_per_step": pairs, "grid": M, "levels": LEVELS,
             "l2": "inputs exceed L2 (per-step state >> 126 MB); no flush needed",
-            "parallelism": f"pairs sharded over {args.gpus} GPU(s), no collective"}
+            "parallelism": f"independent pairs per GPU ({args.gpus} GPU(s)), no collective"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -268,7 +270,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pairs", type=int, default=1024, help="pairs per step (whole job)")
+    ap.add_argument("--pairs", type=int, default=256, help="pairs per GPU per step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -295,9 +297,8 @@ def main():
     from paper_1810_00118_b200._lib import MLParams, check
     import ctypes as C
 
-    per = [args.pairs // world + (1 if r < args.pairs % world else 0) for r in range(world)]
-    first = sum(per[:rank])
-    B = per[rank]
+    B = args.pairs
+    first = rank * B
     img0, img1 = make_images_gpu(first, B, dev)
 
     ctx = _lib.Context(local)
@@ -348,6 +349,8 @@ def main():
     cu = 0.0
     finest_s = 0.0
     finest_sweeps = 0.0
+    lev_s = np.zeros(LEVELS)
+    lev_cu = np.zeros(LEVELS)
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(cstream)
@@ -359,6 +362,8 @@ def main():
             cu += cell_updates(it)
             finest_s += secs[-1]
             finest_sweeps += float(it[:, -1].sum())
+            lev_s += np.array(secs)
+            lev_cu += it.sum(axis=0) * np.array([(n + 1) ** 2 for n in level_sizes()])
         ev1.record(cstream)
         barrier()
     t_local = ev0.elapsed_time(ev1) * 1e-3
@@ -366,7 +371,7 @@ def main():
     T = max_over_ranks(t_local)
     cu_all = sum_over_ranks(cu)
     value = cu_all / T
-    pairs_per_s = args.pairs * args.steps / T
+    pairs_per_s = args.pairs * world * args.steps / T
 
     # roofline of the fused sweep at the finest level, measured in the timed
     # region: algorithmic bytes of every pair-sweep / device time of the
@@ -407,9 +412,9 @@ def main():
         barrier()
         te = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
         e2e = {"value": sum_over_ranks(ecu) / te, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * args.pairs * M * M * 8,
-               "d2h_bytes_per_step": args.pairs * (8 + 8 + 8 * LEVELS + 4),
-               "pairs_per_s": args.pairs * args.steps / te}
+               "h2d_bytes_per_step": 2 * args.pairs * world * M * M * 8,
+               "d2h_bytes_per_step": args.pairs * world * (8 + 8 + 8 * LEVELS + 4),
+               "pairs_per_s": args.pairs * world * args.steps / te}
         del h0, h1
 
     # ---- single-pair time-to-converged-W1 at 512^2 (device-resident input)
@@ -459,9 +464,12 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(args, args.pairs),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args, args.pairs * world),
             "pairs_per_s": pairs_per_s, "time_to_w1_512_s": t_single,
+            "levels": [{"n": n, "seconds_per_step": s_ / args.steps,
+                        "cell_updates_per_s": c_ / s_}
+                       for n, s_, c_ in zip(level_sizes(), lev_s, lev_cu)],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": None,
                          "kernel": "w1mg_dev::cp_sweep_kernel<1> (fused PD sweep, 512^2 level)",

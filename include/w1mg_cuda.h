@@ -179,6 +179,10 @@ int w1mg_ml_cp_batch_dev(w1mg_ctx* ctx, int npairs, int m, const double* img0s_d
  * process: 0 = register-pipelined LDG, 1 = TMA bulk-copy ring (default).
  * Also settable with the environment variable W1MG_SWEEP=ldg|tma. */
 int w1mg_set_sweep_engine(int engine);
+/* Levels with n <= 64 run in one launch per level, one CTA per pair, state
+ * resident in shared memory (1 = on, default) or through the streaming sweep
+ * (0).  Also W1MG_RESIDENT=0|1. */
+int w1mg_set_resident_engine(int on);
 /* Times the fused sweep kernel alone: `iters` sweeps over B pairs of an
  * n-cell level (synthetic source, stop rule off) after `warm` untimed ones;
  * writes the mean milliseconds per sweep launch (CUDA events). */

@@ -270,8 +270,33 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
 // Runs sweeps on every pair of the level until each pair's stop flag is set
 // (device-side, solver_cp.cpp:128-136 semantics).  The host only watches a
 // done-counter one graph behind, so it never stalls the GPU per iteration.
+int g_resident = 1;  // shared-memory-resident engine for small levels (W1MG_RESIDENT=0 off)
+
+template <int PN>
+void launch_resident_pn(const Level& lv, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(cp_resident_kernel<PN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kResidentMaxBytes));
+        attr = true;
+    }
+    cp_resident_kernel<PN><<<lv.B, kResidentThreads, resident_bytes(lv.n), s>>>(lv.args);
+}
+
+bool resident_ok(const Level& lv) {
+    return g_resident && resident_bytes(lv.n) <= kResidentMaxBytes;
+}
+
 void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
     if (max_iters <= 0) return;
+    if (resident_ok(lv)) {  // whole level in one launch, stop rule on device
+        if (pn == 0) launch_resident_pn<0>(lv, c->stream);
+        else if (pn == 1) launch_resident_pn<1>(lv, c->stream);
+        else launch_resident_pn<2>(lv, c->stream);
+        CK(cudaGetLastError());
+        ++c->launches;
+        return;
+    }
     constexpr int K = 16;
     if (max_iters < K) {
         for (long k = 0; k < max_iters; ++k) launch_sweep(lv, pn, (int)(k & 1), c->stream);
@@ -463,6 +488,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (major < 10) fail(W1MG_ECUDA, "this build targets sm_100a (B200)");
         if (const char* v = std::getenv("W1MG_SWEEP"))
             g_sweep_variant = (std::string(v) == "ldg") ? kLdg : kTma;
+        if (const char* v = std::getenv("W1MG_RESIDENT")) g_resident = std::atoi(v) != 0;
         auto* c = new w1mg_ctx();
         c->device = device;
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -887,6 +913,11 @@ int w1mg_ml_cp_batch(w1mg_ctx* c, int npairs, int m, const double* img0s, const 
 int w1mg_set_sweep_engine(int engine) {
     if (engine != kLdg && engine != kTma) return W1MG_EINVAL;
     g_sweep_variant = engine;
+    return W1MG_OK;
+}
+
+int w1mg_set_resident_engine(int on) {
+    g_resident = on ? 1 : 0;
     return W1MG_OK;
 }
 

@@ -414,3 +414,164 @@ cp_sweep_tma_kernel(const SweepArgs a, const int parity) {
 }
 
 }  // namespace w1mg_dev
+
+namespace w1mg_dev {
+
+// ------------------------------------------------------- resident engine
+// Small levels (6 (n+1)^2 doubles <= kResidentMaxBytes): one CTA per pair
+// keeps phi, rho, m and dm in shared memory and runs every sweep of the
+// level in ONE launch, deciding the stop rule itself after each sweep.
+// Two phases per sweep separated by a block barrier:
+//   A: m-update of every node (reads phi^k, writes m^{k+1} in place + dm)
+//   B: phi-update of every node (reads m^{k+1}, dm of the node and its
+//      left/lower neighbours, rho) -- same arithmetic as row_update.
+// The state after the last sweep is written back to buffer 0 (ctl.cur = 0).
+constexpr int kResidentThreads = 512;
+constexpr int kResidentMaxBytes = 6 * 65 * 65 * 8;  // n <= 64
+
+__host__ __device__ constexpr long resident_bytes(int n) {
+    return 6L * (n + 1) * (n + 1) * 8;
+}
+
+template <int PN>
+__global__ void __launch_bounds__(kResidentThreads, 1)
+cp_resident_kernel(const SweepArgs a) {
+    const int pair = blockIdx.x;
+    PairCtl* ctl = a.ctl + pair;
+    if (ctl->done) return;
+    extern __shared__ __align__(16) double sm[];
+    const Layout L = a.L;
+    const int n = L.n;
+    const int W = n + 1;
+    const int V = W * W;
+    double* phi = sm;
+    double* rho = sm + V;
+    double* mx = sm + 2 * V;
+    double* my = sm + 3 * V;
+    double* ddx = sm + 4 * V;
+    double* ddy = sm + 5 * V;
+    const int T = blockDim.x;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int di = T % W, dj = T / W;  // incremental (i, j) of k += T
+    const int i0 = tid % W, j0 = tid / W;
+
+    double* pb = a.base + (long)pair * NSLOT * L.plane;
+    const int cur = ctl->cur;
+    {
+        const double* gp = pb + (PHI0 + cur) * L.plane;
+        const double* gx = pb + (MX0 + cur) * L.plane;
+        const double* gy = pb + (MY0 + cur) * L.plane;
+        const double* gr = pb + RHO * L.plane;
+        int i = i0, j = j0;
+        for (int k = tid; k < V; k += T) {
+            const long o = L.at(i, j);
+            phi[k] = gp[o];
+            rho[k] = gr[o];
+            mx[k] = (i < n) ? gx[o] : 0.0;
+            my[k] = (j < n) ? gy[o] : 0.0;
+            i += di;
+            j += dj;
+            if (i >= W) { i -= W; ++j; }
+        }
+    }
+    __shared__ double red[kResidentThreads / 32][3];
+    __shared__ int stop;
+    const double mu = a.mu, tau = a.tau, ih = a.ih;
+    long it = ctl->it;
+    const long max_it = ctl->max_it;
+    const double tol = ctl->tol;
+    __syncthreads();
+
+    for (;;) {
+        double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
+        {  // phase A: flux
+            int i = i0, j = j0;
+            for (int k = tid; k < V; k += T) {
+                const bool hx = i < n, hy = j < n;
+                const double pc = phi[k];
+                const double pr = hx ? phi[k + 1] : 0.0;
+                const double pu = hy ? phi[k + W] : 0.0;
+                double ux, uy, dx, dy;
+                node_flux<PN>(hx, hy, pc, pr, pu, mx[k], my[k], mu, ih, ux, uy, dx, dy);
+                mx[k] = ux;
+                my[k] = uy;
+                ddx[k] = dx;
+                ddy[k] = dy;
+                s_dm2 += dx * dx + dy * dy;
+                i += di;
+                j += dj;
+                if (i >= W) { i -= W; ++j; }
+            }
+        }
+        __syncthreads();
+        {  // phase B: potential (divergence_into order, grid.cpp:52-65)
+            int i = i0, j = j0;
+            for (int k = tid; k < V; k += T) {
+                const double uxl = (i > 0) ? mx[k - 1] : 0.0;
+                const double dxl = (i > 0) ? ddx[k - 1] : 0.0;
+                const double uyb = (j > 0) ? my[k - W] : 0.0;
+                const double dyb = (j > 0) ? ddy[k - W] : 0.0;
+                const double divm = (mx[k] - uxl) * ih + (my[k] - uyb) * ih;
+                const double divd = (ddx[k] - dxl) * ih + (ddy[k] - dyb) * ih;
+                const double d = tau * (divm + divd - rho[k]);
+                phi[k] = phi[k] + d;
+                s_dp2 += d * d;
+                s_cr += d * divd;
+                i += di;
+                j += dj;
+                if (i >= W) { i -= W; ++j; }
+            }
+        }
+        s_dm2 = warp_sum(s_dm2);
+        s_dp2 = warp_sum(s_dp2);
+        s_cr = warp_sum(s_cr);
+        if (lane == 0) {
+            red[warp][0] = s_dm2;
+            red[warp][1] = s_dp2;
+            red[warp][2] = s_cr;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double sdm2 = 0.0, sdp2 = 0.0, scr = 0.0;
+            for (int w = 0; w < T / 32; ++w) {
+                sdm2 += red[w][0];
+                sdp2 += red[w][1];
+                scr += red[w][2];
+            }
+            const double fpr = a.h2 * (sdm2 / mu + sdp2 / tau - 2.0 * scr);
+            if (a.hist && it < a.hist_cap) a.hist[(long)pair * a.hist_cap + it] = fpr;
+            ++it;
+            const bool finite = isfinite(fpr);
+            const bool done = (fpr < tol) || (it >= max_it) || !finite;
+            stop = done;
+            ctl->fpr = fpr;
+            if (!finite) ctl->nonfinite = 1;
+        }
+        __syncthreads();
+        if (stop) break;
+    }
+    {  // write the final state back to buffer 0
+        double* gp = pb + PHI0 * L.plane;
+        double* gx = pb + MX0 * L.plane;
+        double* gy = pb + MY0 * L.plane;
+        int i = i0, j = j0;
+        for (int k = tid; k < V; k += T) {
+            const long o = L.at(i, j);
+            gp[o] = phi[k];
+            if (i < n) gx[o] = mx[k];
+            if (j < n) gy[o] = my[k];
+            i += di;
+            j += dj;
+            if (i >= W) { i -= W; ++j; }
+        }
+    }
+    if (tid == 0) {
+        ctl->it = it;
+        ctl->cur = 0;
+        ctl->done = 1;
+        atomicAdd(a.ndone, 1);
+    }
+}
+
+}  // namespace w1mg_dev

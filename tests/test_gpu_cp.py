@@ -51,9 +51,22 @@ def _random_source(n, seed):
     return instances.make_source(a, b, n)
 
 
+@pytest.fixture(params=["resident", "stream-tma", "stream-ldg"])
+def engine(request):
+    """Every small-level test runs on all three sweep engines."""
+    from paper_1810_00118_b200 import _lib
+
+    L = _lib.lib()
+    L.w1mg_set_resident_engine(1 if request.param == "resident" else 0)
+    L.w1mg_set_sweep_engine(0 if request.param == "stream-ldg" else 1)
+    yield request.param
+    L.w1mg_set_resident_engine(1)
+    L.w1mg_set_sweep_engine(1)
+
+
 @pytest.mark.parametrize("p", [0, 1, 2])
 @pytest.mark.parametrize("n", [1, 2, 8, 31, 33, 100])
-def test_fixed_iterations_bit_exact(oracle, n, p):
+def test_fixed_iterations_bit_exact(oracle, n, p, engine):
     rho = _random_source(n, 7 + n)
     rep = _run(rho, p, 300)
     ref = oracle.cp_run(rho, p=p, tol=-1.0, max_iters=300)
@@ -65,7 +78,7 @@ def test_fixed_iterations_bit_exact(oracle, n, p):
     np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-10, atol=0)
 
 
-def test_config1_20000_iterations(oracle):
+def test_config1_20000_iterations(oracle, engine):
     """BASELINE.json configs[0]: N=64, fixed 20,000 sweeps, p=2, practical steps."""
     rho = instances.config1_source(64)
     rep = _run(rho, 1, 20000)
@@ -89,7 +102,7 @@ def test_warm_start_bit_exact(oracle, p):
 
 
 @pytest.mark.parametrize("safe", [False, True])
-def test_converged_mode_same_stop(oracle, safe):
+def test_converged_mode_same_stop(oracle, safe, engine):
     rho = instances.config1_source(32)
     tol = 1e-7
     rep = _run(rho, 1, 200000, tol=tol, safe=safe)

@@ -37,3 +37,24 @@ if __name__ == "__main__":
             r = probe(ctx, n, B)
             r["engine"] = ["ldg", "tma"][e]
             print(json.dumps(r), flush=True)
+
+
+def level_time(ctx, n, B, p=1, sweeps=2000):
+    """Device seconds for `sweeps` sweeps of an n-level over B pairs through
+    the cascade driver with the stop rule off (eps < 0)."""
+    import numpy as np
+    from paper_1810_00118_b200 import w1mg
+    from paper_1810_00118_b200._lib import MLParams, check
+
+    img = np.random.default_rng(0).random((B, n, n)) + 0.5
+    img1 = img[:, ::-1, :].copy()
+    prm = MLParams()
+    prm.levels, prm.pnorm, prm.step_mode, prm.rel_tol = 1, p, 1, -1.0
+    eps = np.array([-1.0])
+    prm.eps = eps.ctypes.data_as(C.POINTER(C.c_double))
+    prm.max_iters = sweeps
+    out = np.zeros(B)
+    its = np.zeros(B, dtype=np.int64)
+    check(ctx.L.w1mg_ml_cp_batch(ctx.h, B, n, _lib.ptr(img), _lib.ptr(img1), C.byref(prm),
+                                 _lib.ptr(out), None, its.ctypes.data_as(_lib._lp), None))
+    return ctx.level_seconds(1)[0]
