@@ -2,9 +2,10 @@
  * w1mg_cuda.h -- the C-ABI drop-in boundary of the B200-native W1 solver.
  *
  * The reference (/root/reference/proj) is a C++20 library whose entry points
- * are the w1mg:: free functions in proj/include/w1mg/*.hpp.  This header is
- * the thin, FFI-friendly layer underneath our source-compatible
- * re-implementation of those headers (include/w1mg/*.hpp, implemented in
+ * are the w1mg:: free functions in proj/include/w1mg/ (grid, prox, solver_cp,
+ * poisson, solver_pdhg).  This header is the thin, FFI-friendly layer
+ * underneath our source-compatible re-implementation of those headers
+ * (include/w1mg/, implemented in
  * paper_1810_00118_b200/csrc/host/w1mg_api.cpp): plain pointers, plain
  * sizes, status codes, no C++ or torch types.  Python (ctypes), Go (cgo),
  * Java (JNI/Panama) or Rust bind it directly; see INTEGRATION.md.
@@ -146,6 +147,14 @@ int w1mg_cp_residual(w1mg_ctx* ctx, int n, const double* cmx, const double* cmy,
                      const double* pphi, double mu, double tau, double* out);
 
 /* ------------------------------------------- sources and cascade (Alg. 3) */
+/* Eq. 14: nested-bilinear prolongation of a potential from
+ * nc cells to 2 nc cells. */
+int w1mg_interpolate_scalar(w1mg_ctx* ctx, int nc, const double* coarse, double* fine);
+/* Eq. 15: flux prolongation, nearest coarse edge along the
+ * edge direction (ties to the lower coordinate), transverse average. */
+int w1mg_interpolate_flux(w1mg_ctx* ctx, int nc, const double* cx, const double* cy,
+                          double* fx, double* fy);
+
 /* Per-level sources from two m x m cell images (finest level n = m): 2x2
  * block-sum restriction, cell->node averaging, unit-mass normalisation,
  * rho = (a - b)/h^2 minus its compensated mean.  Output is
@@ -173,6 +182,40 @@ int w1mg_ml_cp_batch_dev(w1mg_ctx* ctx, int npairs, int m, const double* img0s_d
                          const double* img1s_dev, const w1mg_ml_params* prm,
                          double* distance_dev, double* dual_dev, long* iters_dev,
                          int* converged_dev);
+
+/* ------------------------------------- Poisson + Algorithm 2 (G-prox PDHG) */
+/* NeumannPoissonSolver::solve_into (check_compat = 1, poisson.cpp:61-70: throws
+ * "NeumannPoissonSolver: right-hand side must sum to zero") or
+ * solve_projected_into (0, poisson.cpp:72-99): zero-mean phi with
+ * A A* phi = b via DCT-II -> spectral divide -> DCT-III on the GPU. */
+int w1mg_poisson_solve(w1mg_ctx* ctx, int n, const double* b, double* phi, int check_compat);
+/* project_affine (poisson.cpp:101-132): m - A* (A A*)^{-1} (A m - rho). */
+int w1mg_project_affine(w1mg_ctx* ctx, int n, const double* mx, const double* my,
+                        const double* rho, double* out_x, double* out_y);
+/* recover_potential (solver_pdhg.hpp:42-46): zero-mean phi, A A* phi = A varphi. */
+int w1mg_recover_potential(w1mg_ctx* ctx, int n, const double* dual_x, const double* dual_y,
+                           double* phi);
+/* pdhg_run (solver_pdhg.hpp:36-40) from (m0, varphi0, varphi_bar0) (NULL = zero;
+ * varphi_bar0 NULL = varphi0) until the Eq. 12 residual < tol or
+ * max_iters.  mu = tau = w1mg_pdhg_step_size().  Outputs (any may be NULL):
+ * m, varphi, varphi_bar, the recovered potential phi; rep->dual_value is
+ * <phi, rho>_h (~ +W1). */
+int w1mg_pdhg_run(w1mg_ctx* ctx, int n, const double* rho, const double* m0x, const double* m0y,
+                  const double* d0x, const double* d0y, const double* b0x, const double* b0y,
+                  int pnorm, double mu, double tau, double tol, long max_iters, double* mx,
+                  double* my, double* dx, double* dy, double* bx, double* by, double* phi,
+                  double* fpr_hist, long hist_cap, w1mg_cp_report* rep);
+/* pdhg_residual (solver_pdhg.hpp:32-34, Eq. 12 with the + cross term). */
+int w1mg_pdhg_residual(w1mg_ctx* ctx, int n, const double* cmx, const double* cmy,
+                       const double* cdx, const double* cdy, const double* pmx, const double* pmy,
+                       const double* pdx, const double* pdy, double mu, double tau, double* out);
+/* Cascadic Algorithm 4 for one pair (per-level sources coarse -> fine).  With
+ * rel_tol > 0 each level's tolerance is rel_tol * G_cold,l (first Eq. 12
+ * residual from the zero state). */
+int w1mg_ml_pdhg_run(w1mg_ctx* ctx, int n_finest, const double* rho_levels,
+                     const w1mg_ml_params* prm, double* mx, double* my, double* dx, double* dy,
+                     double* phi, w1mg_level_stats* stats, double* fpr_hist, long hist_cap,
+                     w1mg_cp_report* rep);
 
 /* --------------------------------------------------------------- probes */
 /* Select the load engine of the fused sweep for subsequent launches in this

@@ -103,6 +103,22 @@ def lib():
         L.w1mg_ml_cp_batch_dev.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                            C.POINTER(MLParams), C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_void_p]
+        L.w1mg_interpolate_scalar.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
+        L.w1mg_interpolate_flux.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp]
+        L.w1mg_poisson_solve.argtypes = [C.c_void_p, C.c_int, _dp, _dp, C.c_int]
+        L.w1mg_project_affine.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp, _dp]
+        L.w1mg_recover_potential.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp]
+        L.w1mg_pdhg_run.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                    C.c_int, C.c_double, C.c_double, C.c_double, C.c_long, _dp,
+                                    _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_long,
+                                    C.POINTER(CPReport)]
+        L.w1mg_pdhg_residual.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                         _dp, C.c_double, C.c_double, _dp]
+        L.w1mg_ml_pdhg_run.argtypes = [C.c_void_p, C.c_int, _dp, C.POINTER(MLParams), _dp, _dp,
+                                       _dp, _dp, _dp, C.POINTER(LevelStatsC), _dp, C.c_long,
+                                       C.POINTER(CPReport)]
+        L.w1mg_set_sweep_engine.argtypes = [C.c_int]
+        L.w1mg_set_resident_engine.argtypes = [C.c_int]
         _lib = L
         return L
 

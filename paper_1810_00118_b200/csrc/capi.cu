@@ -7,6 +7,7 @@
 //   cp_residual      proj/src/solver_cp.cpp:102-111
 //   grid operators   proj/src/grid.cpp:45-142
 //   ml_run (spec)
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -22,6 +23,7 @@
 
 #include "../../include/w1mg_cuda.h"
 #include "level_kernels.cuh"
+#include "ref_kernels.cuh"
 
 using namespace w1mg_dev;
 
@@ -87,16 +89,19 @@ struct w1mg_ctx {
     int lev_count = 0;
     long launches = 0;
     int num_sms = 148;
+    void* blas = nullptr;  // cublasHandle_t for the Poisson DCT GEMMs (lazy)
 
     void* buf(const std::string& name, size_t bytes) {
         Buf& b = bufs[name];
         if (b.bytes < bytes) {
-            if (b.p) CK(cudaFree(b.p));
+            if (b.p) {
+                CK(cudaFree(b.p));
+                // any cached graph may hold the old pointer
+                for (auto& g : graphs) cudaGraphExecDestroy(g.second);
+                graphs.clear();
+            }
             b.p = nullptr;
             b.bytes = 0;
-            // any cached graph may hold the old pointer
-            for (auto& g : graphs) cudaGraphExecDestroy(g.second);
-            graphs.clear();
             CK(cudaMalloc(&b.p, bytes));
             b.bytes = bytes;
         }
@@ -512,6 +517,7 @@ void w1mg_ctx_destroy(w1mg_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->lev_ev) cudaEventDestroy(e);
+    if (c->blas) cublasDestroy(static_cast<cublasHandle_t>(c->blas));
     if (c->t0) cudaEventDestroy(c->t0);
     if (c->t1) cudaEventDestroy(c->t1);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -908,6 +914,45 @@ int w1mg_ml_cp_batch(w1mg_ctx* c, int npairs, int m, const double* img0s, const 
     });
 }
 
+// Eq. 14 / Eq. 15 on single reference-layout fields (value API).
+int w1mg_interpolate_scalar(w1mg_ctx* c, int nc, const double* coarse, double* fine) {
+    return guard([&] {
+        check_n(nc);
+        const size_t Vc = (size_t)(nc + 1) * (nc + 1), Vf = (size_t)(2 * nc + 1) * (2 * nc + 1);
+        double* dc = c->get<double>("ip.c", Vc);
+        double* df = c->get<double>("ip.f", Vf);
+        CK(cudaMemcpyAsync(dc, coarse, Vc * 8, cudaMemcpyDefault, c->stream));
+        dim3 blk(32, 8);
+        interp_scalar_ref_kernel<<<node_grid(2 * nc, 1, blk), blk, 0, c->stream>>>(nc, dc, df);
+        ++c->launches;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(fine, df, Vf * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int w1mg_interpolate_flux(w1mg_ctx* c, int nc, const double* cx, const double* cy, double* fx,
+                          double* fy) {
+    return guard([&] {
+        check_n(nc);
+        const int nf = 2 * nc;
+        const size_t Ec = (size_t)nc * (nc + 1), Ef = (size_t)nf * (nf + 1);
+        double* dcx = c->get<double>("ip.cx", Ec);
+        double* dcy = c->get<double>("ip.cy", Ec);
+        double* dfx = c->get<double>("ip.fx", Ef);
+        double* dfy = c->get<double>("ip.fy", Ef);
+        CK(cudaMemcpyAsync(dcx, cx, Ec * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(dcy, cy, Ec * 8, cudaMemcpyDefault, c->stream));
+        dim3 blk(32, 8);
+        interp_flux_ref_kernel<<<node_grid(nf, 1, blk), blk, 0, c->stream>>>(nc, dcx, dcy, dfx, dfy);
+        ++c->launches;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(fx, dfx, Ef * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(fy, dfy, Ef * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
 // Kernel probe: `iters` fused sweeps on B pairs of an n-cell level with the
 // stop rule disabled, after `warm` untimed sweeps; returns ms per sweep.
 int w1mg_set_sweep_engine(int engine) {
@@ -949,3 +994,5 @@ int w1mg_sweep_probe(w1mg_ctx* c, int n, int B, int pnorm, long warm, long iters
 }
 
 }  // extern "C"
+
+#include "pdhg_engine.cuh"

@@ -174,7 +174,8 @@ __device__ __forceinline__ void row_update(const SweepArgs& a, const Strip& s, i
 
 // Block + last-block reduction of the three residual sums; the last block of
 // a pair finalises R^k and the stop flag (solver_cp.cpp:70, :128-136).
-__device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int parity,
+template <bool kPlusCross = false>
+__device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int parity, int bid, int nblk,
                                              double s_dm2, double s_dp2, double s_cr) {
     __shared__ double red[kSweepWarps][3];
     __shared__ bool is_last;
@@ -189,7 +190,6 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
         red[warp][2] = s_cr;
     }
     __syncthreads();
-    const int nblk = gridDim.x;
     double* part = a.partial + (long)pair * nblk * 3;
     if (threadIdx.x == 0) {
         double t0 = 0.0, t1 = 0.0, t2 = 0.0;
@@ -199,9 +199,9 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
             t1 += red[w][1];
             t2 += red[w][2];
         }
-        part[blockIdx.x * 3 + 0] = t0;
-        part[blockIdx.x * 3 + 1] = t1;
-        part[blockIdx.x * 3 + 2] = t2;
+        part[bid * 3 + 0] = t0;
+        part[bid * 3 + 1] = t1;
+        part[bid * 3 + 2] = t2;
         __threadfence();
         unsigned t = atomicAdd(a.ticket + pair, 1u);
         is_last = (t == (unsigned)nblk - 1);
@@ -235,7 +235,9 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
             scr += red[w][2];
         }
         PairCtl* ctl = a.ctl + pair;
-        double fpr = a.h2 * (sdm2 / a.mu + sdp2 / a.tau - 2.0 * scr);
+        // Eq. 9 (CP, minus cross term) or Eq. 12 (PDHG, plus cross term)
+        double fpr = kPlusCross ? a.h2 * (sdm2 / a.mu + sdp2 / a.tau + 2.0 * scr)
+                                : a.h2 * (sdm2 / a.mu + sdp2 / a.tau - 2.0 * scr);
         long k = ctl->it;
         if (a.hist && k < a.hist_cap) a.hist[(long)pair * a.hist_cap + k] = fpr;
         ctl->it = k + 1;
@@ -302,7 +304,7 @@ cp_sweep_kernel(const SweepArgs a, const int parity) {
             pc = pu;
         }
     }
-    finish_sweep(a, pair, parity, s_dm2, s_dp2, s_cr);
+    finish_sweep(a, pair, parity, blockIdx.x, gridDim.x, s_dm2, s_dp2, s_cr);
 }
 
 // ------------------------------------------------------------ kTma engine
@@ -410,7 +412,7 @@ cp_sweep_tma_kernel(const SweepArgs a, const int parity) {
             pc = pu;
         }
     }
-    finish_sweep(a, pair, parity, s_dm2, s_dp2, s_cr);
+    finish_sweep(a, pair, parity, blockIdx.x, gridDim.x, s_dm2, s_dp2, s_cr);
 }
 
 }  // namespace w1mg_dev

@@ -449,3 +449,167 @@ def ml_run_batch(img0s: np.ndarray, img1s: np.ndarray, levels: int, p: PNorm = P
                                       conv.ctypes.data_as(_lib._ip)))
     del keep
     return dist, dual, iters, conv.astype(bool)
+
+
+def interpolate_scalar(coarse: ScalarField, fine: GridSpec) -> ScalarField:
+    """Eq. 14 on the GPU."""
+    if fine.n != 2 * coarse.grid.n:
+        raise ValueError("interpolate: grids do not nest")
+    out = ScalarField(fine)
+    check(_lib.lib().w1mg_interpolate_scalar(_ctx(), coarse.grid.n, ptr(coarse.values),
+                                             ptr(out.values)))
+    return out
+
+
+def interpolate_flux(coarse: FluxField, fine: GridSpec) -> FluxField:
+    """Eq. 15 on the GPU."""
+    if fine.n != 2 * coarse.grid.n:
+        raise ValueError("interpolate: grids do not nest")
+    out = FluxField(fine)
+    check(_lib.lib().w1mg_interpolate_flux(_ctx(), coarse.grid.n, ptr(coarse.x_edges),
+                                           ptr(coarse.y_edges), ptr(out.x_edges),
+                                           ptr(out.y_edges)))
+    return out
+
+
+# --------------------------------------------------------------- poisson
+class NeumannPoissonSolver:
+    """poisson.hpp:14-38: DCT-II / spectral divide / DCT-III on the GPU."""
+
+    def __init__(self, grid: GridSpec):
+        self._grid = grid
+
+    def grid(self) -> GridSpec:
+        return self._grid
+
+    def _solve(self, b: ScalarField, out: ScalarField, compat: bool):
+        if b.grid != self._grid or out.grid != self._grid:
+            raise ValueError("NeumannPoissonSolver: grid mismatch")
+        check(_lib.lib().w1mg_poisson_solve(_ctx(), self._grid.n, ptr(b.values), ptr(out.values),
+                                            1 if compat else 0))
+
+    def solve(self, b: ScalarField) -> ScalarField:
+        out = ScalarField(self._grid)
+        self._solve(b, out, True)
+        return out
+
+    def solve_into(self, b: ScalarField, out: ScalarField) -> None:
+        self._solve(b, out, True)
+
+    def solve_projected_into(self, b: ScalarField, out: ScalarField) -> None:
+        self._solve(b, out, False)
+
+
+def project_affine(solver: NeumannPoissonSolver, m: FluxField, rho: SourceField) -> FluxField:
+    if m.grid != solver.grid() or rho.grid() != solver.grid():
+        raise ValueError("project_affine: grid mismatch")
+    out = FluxField(m.grid)
+    check(_lib.lib().w1mg_project_affine(_ctx(), m.grid.n, ptr(m.x_edges), ptr(m.y_edges),
+                                         ptr(rho.rho.values), ptr(out.x_edges),
+                                         ptr(out.y_edges)))
+    return out
+
+
+# ----------------------------------------------------------- solver_pdhg
+@dataclass
+class PDHGState:
+    m: FluxField
+    dual_flux: FluxField
+    dual_flux_bar: FluxField
+    mu: float = 0.0
+    tau: float = 0.0
+    k: int = 0
+
+
+def pdhg_step_size(mode: StepMode) -> float:
+    return _lib.lib().w1mg_pdhg_step_size(int(mode))
+
+
+def pdhg_init(grid: GridSpec, mode: StepMode, m0: FluxField, dual0: FluxField) -> PDHGState:
+    if m0.grid != grid or dual0.grid != grid:
+        raise ValueError("pdhg_init: grid mismatch")
+    s = pdhg_step_size(mode)
+    return PDHGState(m0.copy(), dual0.copy(), dual0.copy(), s, s, 0)
+
+
+def _pdhg_call(n, rho, m0, d0, b0, p, mu, tau, tol, max_iters, hist_cap):
+    g = GridSpec(n)
+    m, d, b = FluxField(g), FluxField(g), FluxField(g)
+    phi = ScalarField(g)
+    cap = int(hist_cap)
+    hist = np.zeros(max(cap, 1))
+    rep = CPReport()
+    f = lambda fl, a: None if fl is None else ptr(getattr(fl, a))  # noqa: E731
+    check(_lib.lib().w1mg_pdhg_run(
+        _ctx(), n, ptr(rho), f(m0, "x_edges"), f(m0, "y_edges"), f(d0, "x_edges"),
+        f(d0, "y_edges"), f(b0, "x_edges"), f(b0, "y_edges"), int(p), mu, tau, tol,
+        int(max_iters), ptr(m.x_edges), ptr(m.y_edges), ptr(d.x_edges), ptr(d.y_edges),
+        ptr(b.x_edges), ptr(b.y_edges), ptr(phi.values), ptr(hist) if cap > 0 else None, cap,
+        C.byref(rep)))
+    return m, d, b, phi, hist[: min(rep.iterations, cap)].copy(), rep
+
+
+def pdhg_step(state: PDHGState, rho: SourceField, p: PNorm, solver=None) -> PDHGState:
+    g = state.m.grid
+    if rho.grid() != g:
+        raise ValueError("pdhg_step: grid mismatch")
+    m, d, b, _, _, _ = _pdhg_call(g.n, rho.rho.values, state.m, state.dual_flux,
+                                  state.dual_flux_bar, p, state.mu, state.tau, -math.inf, 1, 0)
+    return PDHGState(m, d, b, state.mu, state.tau, state.k + 1)
+
+
+def pdhg_residual(curr: PDHGState, prev: PDHGState) -> float:
+    g = curr.m.grid
+    r = C.c_double()
+    check(_lib.lib().w1mg_pdhg_residual(
+        _ctx(), g.n, ptr(curr.m.x_edges), ptr(curr.m.y_edges), ptr(curr.dual_flux.x_edges),
+        ptr(curr.dual_flux.y_edges), ptr(prev.m.x_edges), ptr(prev.m.y_edges),
+        ptr(prev.dual_flux.x_edges), ptr(prev.dual_flux.y_edges), curr.mu, curr.tau,
+        C.byref(r)))
+    return r.value
+
+
+def pdhg_run(rho: SourceField, params: SolverParams, m0: Optional[FluxField] = None,
+             dual0: Optional[FluxField] = None, hist_cap: Optional[int] = None) -> SolveReport:
+    """Algorithm 2 until G^k < tolerance or max_iters (solver_pdhg.hpp:36-40);
+    the potential is recovered from the final dual flux (Appendix B)."""
+    g = rho.grid()
+    if (m0 is not None and m0.grid != g) or (dual0 is not None and dual0.grid != g):
+        raise ValueError("pdhg_run: grid mismatch")
+    s = pdhg_step_size(params.step_mode)
+    cap = min(params.max_iters, 1 << 20) if hist_cap is None else hist_cap
+    m, d, _, phi, hist, rep = _pdhg_call(g.n, rho.rho.values, m0, dual0, None, params.p, s, s,
+                                         params.tolerance, params.max_iters, cap)
+    return SolveReport(rep.distance, rep.dual_value, bool(rep.converged), rep.iterations, m, phi,
+                       d, [LevelStats(g.h, params.tolerance, rep.iterations, rep.fpr_final,
+                                      rep.seconds)], hist, rep.seconds)
+
+
+def recover_potential(dual_flux: FluxField, solver=None) -> ScalarField:
+    out = ScalarField(dual_flux.grid)
+    check(_lib.lib().w1mg_recover_potential(_ctx(), dual_flux.grid.n, ptr(dual_flux.x_edges),
+                                            ptr(dual_flux.y_edges), ptr(out.values)))
+    return out
+
+
+def ml_pdhg_run(rho_levels: list, p: PNorm = PNorm.p2, rel_tol: float = 1e-5, eps=None,
+                max_iters: int = 5_000_000, step_mode: StepMode = StepMode.practical,
+                hist_cap: int = 1 << 16) -> SolveReport:
+    """Cascadic Algorithm 4 over per-level sources; level
+    tolerance rel_tol * G_cold,l unless absolute ``eps`` is given."""
+    levels = len(rho_levels)
+    nf = rho_levels[-1].shape[0] - 1
+    flat = np.ascontiguousarray(np.concatenate([np.ravel(r) for r in rho_levels]))
+    prm, keep = _ml_params(levels, p, step_mode, rel_tol, eps, max_iters)
+    g = GridSpec(nf)
+    m, d, phi = FluxField(g), FluxField(g), ScalarField(g)
+    st = (LevelStatsC * levels)()
+    hist = np.zeros(max(hist_cap, 1))
+    rep = CPReport()
+    check(_lib.lib().w1mg_ml_pdhg_run(_ctx(), nf, ptr(flat), C.byref(prm), ptr(m.x_edges),
+                                      ptr(m.y_edges), ptr(d.x_edges), ptr(d.y_edges),
+                                      ptr(phi.values), st, ptr(hist), hist_cap, C.byref(rep)))
+    del keep
+    lv = [LevelStats(s.h, s.eps, s.iters, s.fpr_final, s.seconds) for s in st]
+    return SolveReport(rep.distance, rep.dual_value, bool(rep.converged), rep.iterations, m, phi,
+                       d, lv, hist[: min(lv[-1].iters, hist_cap)].copy(), rep.seconds)
