@@ -24,6 +24,7 @@
 #include "../../include/w1mg_cuda.h"
 #include "level_kernels.cuh"
 #include "ref_kernels.cuh"
+#include "cp2_kernels.cuh"
 
 using namespace w1mg_dev;
 
@@ -125,8 +126,10 @@ struct Level {
     unsigned* ticket = nullptr;
     double* partial = nullptr;
     int* ndone = nullptr;
-    SweepArgs args{};
+    SweepArgs args{};   // single-sweep engines
     dim3 grid;
+    SweepArgs args2{};  // two-sweep engine
+    dim3 grid2;
 };
 
 Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, double tau,
@@ -166,8 +169,24 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     a.hist_cap = hist_cap;
     a.ndone = lv.ndone;
     lv.grid = dim3((a.ntiles + kSweepWarps - 1) / kSweepWarps, B, 1);
-    lv.partial = c->get<double>(tag + ".partial", (size_t)B * lv.grid.x * 3);
+    // two-sweep geometry: 29 owned columns per warp
+    SweepArgs& a2 = lv.args2;
+    a2 = a;
+    a2.ncx = (n + 1 + kOwn2 - 1) / kOwn2;
+    int H2 = 64;
+    while (H2 > 4) {
+        long tiles = (long)B * a2.ncx * ((n + 1 + H2 - 1) / H2);
+        if (tiles >= target) break;
+        H2 >>= 1;
+    }
+    a2.H = H2;
+    a2.nsy = (n + 1 + H2 - 1) / H2;
+    a2.ntiles = a2.ncx * a2.nsy;
+    lv.grid2 = dim3((a2.ntiles + kSweepWarps - 1) / kSweepWarps, B, 1);
+    lv.partial = c->get<double>(
+        tag + ".partial", (size_t)B * std::max<size_t>(lv.grid.x * 3, lv.grid2.x * 6));
     a.partial = lv.partial;
+    a2.partial = lv.partial;
     CK(cudaMemsetAsync(lv.ticket, 0, sizeof(unsigned) * B, c->stream));
     return lv;
 }
@@ -236,11 +255,24 @@ void reduce_pairs(w1mg_ctx* c, F f, int w, int rows, int B, double s1, double s2
     CK(cudaGetLastError());
 }
 
-int g_sweep_variant = kTma;  // engine for the fused sweep (W1MG_SWEEP=ldg|tma)
+// engine for the fused sweep (W1MG_SWEEP=ldg|tma|tma2); kTma2 streams two
+// sweeps per HBM pass, falling back to the single-sweep TMA kernel for the
+// short loops and the stop fix-up
+constexpr int kTma2 = 2;
+int g_sweep_variant = kTma2;
+
+void launch_sweep2(const Level& lv, int pn, int parity, cudaStream_t s) {
+    dim3 blk(kSweepWarps * 32);
+    switch (pn) {
+        case 0: cp_sweep2_tma_kernel<0><<<lv.grid2, blk, kTmaSmem, s>>>(lv.args2, parity); break;
+        case 1: cp_sweep2_tma_kernel<1><<<lv.grid2, blk, kTmaSmem, s>>>(lv.args2, parity); break;
+        default: cp_sweep2_tma_kernel<2><<<lv.grid2, blk, kTmaSmem, s>>>(lv.args2, parity); break;
+    }
+}
 
 void launch_sweep(const Level& lv, int pn, int parity, cudaStream_t s) {
     dim3 blk(kSweepWarps * 32);
-    if (g_sweep_variant == kTma) {
+    if (g_sweep_variant == kTma || g_sweep_variant == kTma2) {
         switch (pn) {
             case 0: cp_sweep_tma_kernel<0><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
             case 1: cp_sweep_tma_kernel<1><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
@@ -263,7 +295,10 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
     if (it != c->graphs.end()) return it->second;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    for (int k = 0; k < K; ++k) launch_sweep(lv, pn, k & 1, c->stream);
+    for (int k = 0; k < K; ++k) {
+        if (g_sweep_variant == kTma2) launch_sweep2(lv, pn, k & 1, c->stream);
+        else launch_sweep(lv, pn, k & 1, c->stream);
+    }
     CK(cudaStreamEndCapture(c->stream, &g));
     cudaGraphExec_t ex;
     CK(cudaGraphInstantiate(&ex, g, 0));
@@ -310,10 +345,11 @@ void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
         return;
     }
     cudaGraphExec_t ex = sweep_graph(c, lv, pn, K);
+    const long per_launch = (g_sweep_variant == kTma2) ? 2 : 1;
     long launched = 0;
     for (long g = 0;; ++g) {
         CK(cudaGraphLaunch(ex, c->stream));
-        launched += K;
+        launched += K * per_launch;
         c->launches += K;
         CK(cudaMemcpyAsync(c->pinned + (g & 1), lv.ndone, sizeof(int), cudaMemcpyDeviceToHost,
                            c->stream));
@@ -322,7 +358,13 @@ void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
             CK(cudaEventSynchronize(c->ev[(g - 1) & 1]));
             if (c->pinned[(g - 1) & 1] >= lv.B) break;
         }
-        if (launched >= max_iters + K) break;  // every pair hit its cap by now
+        if (launched >= max_iters + K * per_launch) break;  // every pair hit its cap by now
+    }
+    if (g_sweep_variant == kTma2) {
+        // replay the first sweep of pairs whose two-sweep launch stopped early
+        launch_sweep(lv, pn, -1, c->stream);
+        CK(cudaGetLastError());
+        ++c->launches;
     }
 }
 
@@ -492,7 +534,9 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
         if (major < 10) fail(W1MG_ECUDA, "this build targets sm_100a (B200)");
         if (const char* v = std::getenv("W1MG_SWEEP"))
-            g_sweep_variant = (std::string(v) == "ldg") ? kLdg : kTma;
+            g_sweep_variant = (std::string(v) == "ldg") ? kLdg
+                              : (std::string(v) == "tma") ? kTma
+                                                          : kTma2;
         if (const char* v = std::getenv("W1MG_RESIDENT")) g_resident = std::atoi(v) != 0;
         auto* c = new w1mg_ctx();
         c->device = device;
@@ -956,7 +1000,7 @@ int w1mg_interpolate_flux(w1mg_ctx* c, int nc, const double* cx, const double* c
 // Kernel probe: `iters` fused sweeps on B pairs of an n-cell level with the
 // stop rule disabled, after `warm` untimed sweeps; returns ms per sweep.
 int w1mg_set_sweep_engine(int engine) {
-    if (engine != kLdg && engine != kTma) return W1MG_EINVAL;
+    if (engine != kLdg && engine != kTma && engine != kTma2) return W1MG_EINVAL;
     g_sweep_variant = engine;
     return W1MG_OK;
 }
@@ -978,14 +1022,22 @@ int w1mg_sweep_probe(w1mg_ctx* c, int n, int B, int pnorm, long warm, long iters
         probe_fill_kernel<<<node_grid(n, B, blk), blk, 0, c->stream>>>(lv.base, lv.L);
         ++c->launches;
         CK(cudaGetLastError());
-        init_level_ctl(c, lv, 0.0, -1.0, warm + iters + 64);
+        init_level_ctl(c, lv, 0.0, -1.0, 2 * (warm + iters) + 64);
+        // kTma2: each launch is two sweeps; iters counts sweeps
+        const int per = (g_sweep_variant == kTma2) ? 2 : 1;
+        auto one = [&](long k) {
+            if (per == 2) launch_sweep2(lv, pnorm, (int)(k & 1), c->stream);
+            else launch_sweep(lv, pnorm, (int)(k & 1), c->stream);
+        };
         long k = 0;
-        for (; k < warm; ++k) launch_sweep(lv, pnorm, (int)(k & 1), c->stream);
+        for (; k < warm / per; ++k) one(k);
         CK(cudaEventRecord(c->t0, c->stream));
-        for (long t = 0; t < iters; ++t, ++k) launch_sweep(lv, pnorm, (int)(k & 1), c->stream);
+        const long nl = iters / per;
+        for (long t = 0; t < nl; ++t, ++k) one(k);
         CK(cudaEventRecord(c->t1, c->stream));
         CK(cudaGetLastError());
-        c->launches += warm + iters;
+        c->launches += k;
+        iters = nl * per;
         CK(cudaEventSynchronize(c->t1));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, c->t0, c->t1));

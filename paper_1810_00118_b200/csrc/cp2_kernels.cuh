@@ -1,0 +1,270 @@
+// cp2_kernels.cuh -- temporally blocked fused sweep: TWO Li et al. PD sweeps
+// (solver_cp.cpp:22-71 applied twice) per pass over HBM.
+//
+// The warp row-march of cp_sweep_tma_kernel is run for sweep A (k -> k+1)
+// and, one row behind it in the same warp, for sweep B (k+1 -> k+2):
+//   * A at row r needs phi^k rows r, r+1 and m^k row r (TMA ring, as before);
+//   * B at row r-1 needs phi^{k+1} rows r-1, r (A's outputs of the previous
+//     and the current step, kept in registers / shuffled from lane+1), m^{k+1}
+//     row r-1 (A's previous-step output) and rho row r-1.
+// The dependency cone widens by one column per sweep on each side, so a warp
+// owns 29 columns (lanes 2..30): lane 0 feeds A's left flux, lanes 0..1 feed
+// B, lane 31 provides phi^{k+1}(i+1) to lane 30.  At the strip bottom A
+// starts two rows early (m only, then m + phi) so B has its lower neighbours.
+// Only phi^{k+2}, m^{k+2} are written: 56 B of compulsory HBM traffic per
+// node per TWO sweeps.  Arithmetic per node is exactly the single-sweep
+// kernel's, so fields stay bit-identical to the reference.
+//
+// Stopping: both residuals R^k and R^{k+1} are reduced.  If the reference
+// would have stopped after A (R^k < tol or the iteration cap), the pair is
+// marked done + redo with its latest buffer = the untouched input state, and
+// one fix-up single-sweep launch (sweep_gate parity < 0) replays sweep A from
+// it, reproducing the reference's first-k stop exactly.
+#pragma once
+
+#include "cp_kernels.cuh"
+
+namespace w1mg_dev {
+
+constexpr int kOwn2 = 29;  // owned columns per warp in the two-sweep march
+
+// Reduction of both sweeps' residual sums (6 per block) and the two-sweep
+// stop rule; partial holds [pairs][blocks][6].
+__device__ __forceinline__ void finish_sweep2(const SweepArgs& a, int pair, int parity,
+                                              double a0, double a1, double a2, double b0,
+                                              double b1, double b2) {
+    __shared__ double red[kSweepWarps][6];
+    __shared__ bool is_last;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    double v[6] = {a0, a1, a2, b0, b1, b2};
+#pragma unroll
+    for (int q = 0; q < 6; ++q) v[q] = warp_sum(v[q]);
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) red[warp][q] = v[q];
+    __syncthreads();
+    const int nblk = gridDim.x;
+    double* part = a.partial + (long)pair * nblk * 6;
+    if (threadIdx.x == 0) {
+        double t[6] = {0, 0, 0, 0, 0, 0};
+        for (int w = 0; w < kSweepWarps; ++w)
+#pragma unroll
+            for (int q = 0; q < 6; ++q) t[q] += red[w][q];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) part[blockIdx.x * 6 + q] = t[q];
+        __threadfence();
+        unsigned tk = atomicAdd(a.ticket + pair, 1u);
+        is_last = (tk == (unsigned)nblk - 1);
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    double t[6] = {0, 0, 0, 0, 0, 0};
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+        const volatile double* pv = part + b * 6;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) t[q] += pv[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) t[q] = warp_sum(t[q]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) red[warp][q] = t[q];
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double s[6] = {0, 0, 0, 0, 0, 0};
+    for (int w = 0; w < kSweepWarps; ++w)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) s[q] += red[w][q];
+    PairCtl* ctl = a.ctl + pair;
+    const double fA = a.h2 * (s[0] / a.mu + s[1] / a.tau - 2.0 * s[2]);
+    const double fB = a.h2 * (s[3] / a.mu + s[4] / a.tau - 2.0 * s[5]);
+    const long k = ctl->it;
+    if (fA < ctl->tol || k + 1 >= ctl->max_it || !isfinite(fA)) {
+        // the reference stops after sweep A, whose state was not stored:
+        // keep the input buffer as "latest" and replay A in the fix-up launch
+        ctl->cur = parity;
+        ctl->redo = 1;
+        ctl->done = 1;
+        atomicAdd(a.ndone, 1);
+    } else {
+        if (a.hist && k < a.hist_cap) a.hist[(long)pair * a.hist_cap + k] = fA;
+        if (a.hist && k + 1 < a.hist_cap) a.hist[(long)pair * a.hist_cap + k + 1] = fB;
+        ctl->it = k + 2;
+        ctl->fpr = fB;
+        ctl->cur = 1 - parity;
+        const bool finite = isfinite(fB);
+        if (!finite) ctl->nonfinite = 1;
+        if (fB < ctl->tol || k + 2 >= ctl->max_it || !finite) {
+            ctl->done = 1;
+            atomicAdd(a.ndone, 1);
+        }
+    }
+    a.ticket[pair] = 0u;
+    __threadfence();
+}
+
+template <int PN>
+__global__ void __launch_bounds__(kSweepWarps * 32, 2)
+cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
+    const int pair = blockIdx.y;
+    if (*(volatile int*)&a.ctl[pair].done) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int tile = blockIdx.x * kSweepWarps + warp;
+    double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * kStages * kStreams * kChunk;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kSweepWarps * kStages * kStageBytes) +
+                     warp * kStages;
+    // residual partial sums of sweep A (k) and sweep B (k+1)
+    double a_dm2 = 0.0, a_dp2 = 0.0, a_cr = 0.0;
+    double b_dm2 = 0.0, b_dp2 = 0.0, b_cr = 0.0;
+
+    if (tile < a.ntiles) {
+        const Layout L = a.L;
+        const int n = L.n;
+        const int P = L.pitch;
+        const int cx = tile % a.ncx;
+        const int sy = tile / a.ncx;
+        const int i = cx * kOwn2 - 2 + lane;
+        const int j0 = sy * a.H;
+        const int j1 = min(j0 + a.H, n + 1);
+        double* pb = a.base + (long)pair * NSLOT * L.plane;
+        const double* __restrict__ phr = pb + (PHI0 + parity) * L.plane;
+        const double* __restrict__ mxr = pb + (MX0 + parity) * L.plane;
+        const double* __restrict__ myr = pb + (MY0 + parity) * L.plane;
+        const double* __restrict__ rho = pb + RHO * L.plane;
+        double* __restrict__ phw = pb + (PHI0 + 1 - parity) * L.plane;
+        double* __restrict__ mxw = pb + (MX0 + 1 - parity) * L.plane;
+        double* __restrict__ myw = pb + (MY0 + 1 - parity) * L.plane;
+        const bool in = (i >= 0) && (i <= n);
+        const bool hx = (i >= 0) && (i < n);
+        const bool own = (lane >= 2) && (lane <= 30) && in;
+        const double mu = a.mu, tau = a.tau, ih = a.ih;
+
+        const int ilo = i - lane;
+        const int a0 = ilo & ~1;
+        const int sh = ilo - a0;
+        const long c0 = L.at(a0, 0);
+        if (lane == 0) {
+#pragma unroll
+            for (int t = 0; t < kStages; ++t) mbar_init(&bars[t], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        auto issue = [&](int st, int row) {
+            double* dst = ring + st * kStreams * kChunk;
+            const long orow = c0 + (long)row * P;
+            mbar_expect_tx(&bars[st], kStageBytes);
+            bulk_g2s(dst + 0 * kChunk, phr + orow + P, kChunk * 8, &bars[st]);
+            bulk_g2s(dst + 1 * kChunk, mxr + orow, kChunk * 8, &bars[st]);
+            bulk_g2s(dst + 2 * kChunk, myr + orow, kChunk * 8, &bars[st]);
+            bulk_g2s(dst + 3 * kChunk, rho + orow, kChunk * 8, &bars[st]);
+        };
+        // A rows rA0 .. rA1 (inclusive); B rows rA0-1 .. j1-1
+        const int rA0 = max(j0 - 1, 0);
+        const int rA1 = min(j1, n);
+        const int nA = rA1 - rA0 + 1;
+        if (lane == 0) {
+            for (int t = 0; t < kStages && t < nA; ++t) issue(t, rA0 + t);
+        }
+
+        // A's y-flux below row rA0 (m-only warm-up, direct loads)
+        double uyA = 0.0, dyA = 0.0;
+        if (rA0 > 0) {
+            const long o = L.at(i, rA0 - 1);
+            double pc = in ? __ldg(phr + o) : 0.0;
+            double pu = in ? __ldg(phr + o + P) : 0.0;
+            double pr = hx ? __ldg(phr + o + 1) : 0.0;
+            double mxo = hx ? __ldg(mxr + o) : 0.0;
+            double myo = in ? __ldg(myr + o) : 0.0;
+            double ux, uy, dx, dy;
+            node_flux<PN>(hx, in, pc, pr, pu, mxo, myo, mu, ih, ux, uy, dx, dy);
+            uyA = uy;
+            dyA = dy;
+        }
+        long o = L.at(i, rA0);
+        double pc = in ? __ldg(phr + o) : 0.0;  // phi^k(i, r)
+        double pr = hx ? __ldg(phr + o + 1) : 0.0;  // phi^k(i+1, r)
+
+        // B state: A's outputs of the previous row, rho of the previous row
+        double fA_prev = 0.0, mxA_prev = 0.0, myA_prev = 0.0;
+        double r_prev = 0.0;
+        double uyB = 0.0, dyB = 0.0;  // B's y-flux below the row it processes
+
+        for (int t = 0; t <= j1 - rA0; ++t, o += P) {
+            const int rA = rA0 + t;  // A row of this step (rA == n+1: virtual)
+            const int rB = rA - 1;   // B row of this step
+            double fA = 0.0, uxA = 0.0, uyAn = 0.0, dxA = 0.0, dyAn = 0.0, r = 0.0;
+            double pu = 0.0, pur = 0.0;
+            if (rA <= rA1) {
+                const int st = t % kStages;
+                mbar_wait(&bars[st], (uint32_t)((t / kStages) & 1));
+                const double* c = ring + st * kStreams * kChunk + sh + lane;
+                const bool hy = in && (rA < n);
+                pu = hy ? c[0] : 0.0;
+                pur = (hx && rA < n) ? c[1] : 0.0;
+                const double mxo = hx ? c[kChunk] : 0.0;
+                const double myo = hy ? c[2 * kChunk] : 0.0;
+                r = in ? c[3 * kChunk] : 0.0;
+                __syncwarp();
+                if (lane == 0 && t + kStages < nA) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    issue(st, rA + kStages);
+                }
+                // ---- sweep A at row rA
+                node_flux<PN>(hx, hy, pc, pr, pu, mxo, myo, mu, ih, uxA, uyAn, dxA, dyAn);
+                const double uxl = __shfl_up_sync(0xffffffffu, uxA, 1);
+                const double dxl = __shfl_up_sync(0xffffffffu, dxA, 1);
+                const double divm = (uxA - uxl) * ih + (uyAn - uyA) * ih;
+                const double divd = (dxA - dxl) * ih + (dyAn - dyA) * ih;
+                const double d = tau * (divm + divd - r);
+                fA = pc + d;
+                if (own && rA >= j0 && rA < j1) {
+                    a_dm2 += dxA * dxA + dyAn * dyAn;
+                    a_dp2 += d * d;
+                    a_cr += d * divd;
+                }
+                uyA = uyAn;
+                dyA = dyAn;
+            }
+            // ---- sweep B at row rB (inputs: A's rows rB and rB+1)
+            if (rB >= rA0) {
+                const bool hyB = in && (rB < n);
+                const double pcB = fA_prev;
+                const double prB = __shfl_down_sync(0xffffffffu, fA_prev, 1);
+                const double puB = hyB ? fA : 0.0;
+                double ux, uy, dx, dy;
+                node_flux<PN>(hx, hyB, pcB, hx ? prB : 0.0, puB, mxA_prev, myA_prev, mu, ih, ux, uy,
+                              dx, dy);
+                const double uxl = __shfl_up_sync(0xffffffffu, ux, 1);
+                const double dxl = __shfl_up_sync(0xffffffffu, dx, 1);
+                const double divm = (ux - uxl) * ih + (uy - uyB) * ih;
+                const double divd = (dx - dxl) * ih + (dy - dyB) * ih;
+                const double d = tau * (divm + divd - r_prev);
+                if (own && rB >= j0) {  // rB < j1 always
+                    const long ob = o - P;
+                    phw[ob] = pcB + d;
+                    if (hx) mxw[ob] = ux;
+                    if (hyB) myw[ob] = uy;
+                    b_dm2 += dx * dx + dy * dy;
+                    b_dp2 += d * d;
+                    b_cr += d * divd;
+                }
+                uyB = uy;
+                dyB = dy;
+            }
+            fA_prev = fA;
+            mxA_prev = uxA;
+            myA_prev = uyAn;
+            r_prev = r;
+            pc = pu;
+            pr = pur;
+        }
+    }
+    finish_sweep2(a, pair, parity, a_dm2, a_dp2, a_cr, b_dm2, b_dp2, b_cr);
+}
+
+}  // namespace w1mg_dev

@@ -43,8 +43,20 @@ struct PairCtl {
     int done;       // stop flag
     int cur;        // buffer parity holding the latest state
     int nonfinite;  // residual was NaN/Inf
-    int pad;
+    int redo;       // a two-sweep launch stopped after its first sweep: replay it
 };
+
+// Launch gate shared by the single-sweep kernels.  parity >= 0: a normal
+// sweep of every running pair.  parity < 0: the fix-up sweep, run only for
+// pairs flagged `redo`, from their own latest buffer.
+__device__ __forceinline__ bool sweep_gate(const PairCtl* ctl, int parity, int& par) {
+    if (parity >= 0) {
+        par = parity;
+        return !*(const volatile int*)&ctl->done;
+    }
+    par = ctl->cur;
+    return ctl->redo != 0;
+}
 
 struct SweepArgs {
     double* base;       // pair b, slot s at base + (b*NSLOT + s)*L.plane
@@ -245,7 +257,11 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
         ctl->cur = 1 - parity;
         bool finite = isfinite(fpr);
         if (!finite) ctl->nonfinite = 1;
-        if (fpr < ctl->tol || k + 1 >= ctl->max_it || !finite) {
+        if (ctl->redo) {
+            // fix-up sweep after a two-sweep launch stopped on its first
+            // sweep: the pair is already counted as done
+            ctl->redo = 0;
+        } else if (fpr < ctl->tol || k + 1 >= ctl->max_it || !finite) {
             ctl->done = 1;
             atomicAdd(a.ndone, 1);
         }
@@ -257,9 +273,10 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
 // ------------------------------------------------------------ kLdg engine
 template <int PN>
 __global__ void __launch_bounds__(kSweepWarps * 32)
-cp_sweep_kernel(const SweepArgs a, const int parity) {
+cp_sweep_kernel(const SweepArgs a, const int parity_arg) {
     const int pair = blockIdx.y;
-    if (*(volatile int*)&a.ctl[pair].done) return;
+    int parity;
+    if (!sweep_gate(a.ctl + pair, parity_arg, parity)) return;
     const int lane = threadIdx.x & 31;
     const int tile = blockIdx.x * kSweepWarps + (threadIdx.x >> 5);
     double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
@@ -339,9 +356,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 template <int PN>
 __global__ void __launch_bounds__(kSweepWarps * 32, 3)
-cp_sweep_tma_kernel(const SweepArgs a, const int parity) {
+cp_sweep_tma_kernel(const SweepArgs a, const int parity_arg) {
     const int pair = blockIdx.y;
-    if (*(volatile int*)&a.ctl[pair].done) return;
+    int parity;
+    if (!sweep_gate(a.ctl + pair, parity_arg, parity)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;

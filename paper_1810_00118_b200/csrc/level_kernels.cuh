@@ -227,7 +227,7 @@ __global__ void init_ctl_kernel(PairCtl* ctl, int npairs, const double* __restri
     c.done = max_it <= 0 ? 1 : 0;
     c.cur = 0;
     c.nonfinite = 0;
-    c.pad = 0;
+    c.redo = 0;
     ctl[b] = c;
 }
 

@@ -51,26 +51,32 @@ def _random_source(n, seed):
     return instances.make_source(a, b, n)
 
 
-@pytest.fixture(params=["resident", "stream-tma", "stream-ldg"])
+ENGINES = {"resident": (1, 2), "stream-tma2": (0, 2), "stream-tma": (0, 1), "stream-ldg": (0, 0)}
+
+
+@pytest.fixture(params=list(ENGINES))
 def engine(request):
-    """Every small-level test runs on all three sweep engines."""
+    """Every small-level test runs on all sweep engines: shared-memory
+    resident, two-sweep TMA (temporal blocking), one-sweep TMA, one-sweep LDG."""
     from paper_1810_00118_b200 import _lib
 
     L = _lib.lib()
-    L.w1mg_set_resident_engine(1 if request.param == "resident" else 0)
-    L.w1mg_set_sweep_engine(0 if request.param == "stream-ldg" else 1)
+    res, eng = ENGINES[request.param]
+    L.w1mg_set_resident_engine(res)
+    L.w1mg_set_sweep_engine(eng)
     yield request.param
     L.w1mg_set_resident_engine(1)
-    L.w1mg_set_sweep_engine(1)
+    L.w1mg_set_sweep_engine(2)
 
 
+@pytest.mark.parametrize("iters", [300, 301])
 @pytest.mark.parametrize("p", [0, 1, 2])
 @pytest.mark.parametrize("n", [1, 2, 8, 31, 33, 100])
-def test_fixed_iterations_bit_exact(oracle, n, p, engine):
+def test_fixed_iterations_bit_exact(oracle, n, p, engine, iters):
     rho = _random_source(n, 7 + n)
-    rep = _run(rho, p, 300)
-    ref = oracle.cp_run(rho, p=p, tol=-1.0, max_iters=300)
-    assert rep.iterations == 300
+    rep = _run(rho, p, iters)
+    ref = oracle.cp_run(rho, p=p, tol=-1.0, max_iters=iters)
+    assert rep.iterations == iters
     _assert_fields_equal(rep, ref)
     assert _rel(rep.distance, ref.distance) <= RED_TOL
     assert _rel(rep.dual_value, ref.dual_value) <= 1e-10
@@ -193,6 +199,20 @@ def test_source_field_gate():
         _src(np.ones((n + 1, n + 1)))
     with pytest.raises(ValueError, match="GridSpec: cells_per_side must be positive"):
         w1mg.GridSpec(0)
+
+
+@pytest.mark.parametrize("p", [0, 1, 2])
+def test_two_sweep_engine_odd_stop_1024(oracle, p):
+    """Two-sweep launches with an odd sweep cap: the last launch stops after
+    its first sweep and the fix-up replay must reproduce the reference state."""
+    n = 1024
+    rng = np.random.default_rng(1024 + p)
+    rho = instances.make_source(rng.random((n + 1, n + 1)), rng.random((n + 1, n + 1)), n)
+    rep = _run(rho, p, 33)
+    ref = oracle.cp_run(rho, p=p, tol=-1.0, max_iters=33)
+    assert rep.iterations == 33
+    _assert_fields_equal(rep, ref)
+    np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-10)
 
 
 def test_full_size_4096_bit_exact(oracle):
