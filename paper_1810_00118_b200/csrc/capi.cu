@@ -156,6 +156,9 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
         H >>= 1;
     }
     a.H = H;
+    a.jlo = 0;
+    a.jhi = n + 1;
+    a.red_out = nullptr;
     a.nsy = (n + 1 + H - 1) / H;
     a.ntiles = a.ncx * a.nsy;
     a.mu = mu;

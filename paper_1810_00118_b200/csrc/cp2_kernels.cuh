@@ -129,8 +129,8 @@ cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
         const int cx = tile % a.ncx;
         const int sy = tile / a.ncx;
         const int i = cx * kOwn2 - 2 + lane;
-        const int j0 = sy * a.H;
-        const int j1 = min(j0 + a.H, n + 1);
+        const int j0 = a.jlo + sy * a.H;
+        const int j1 = min(j0 + a.H, a.jhi);
         double* pb = a.base + (long)pair * NSLOT * L.plane;
         const double* __restrict__ phr = pb + (PHI0 + parity) * L.plane;
         const double* __restrict__ mxr = pb + (MX0 + parity) * L.plane;

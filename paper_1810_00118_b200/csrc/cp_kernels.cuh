@@ -64,6 +64,8 @@ struct SweepArgs {
     int ncx;            // column strips (31 owned columns each)
     int nsy;            // row strips
     int H;              // rows per strip
+    int jlo, jhi;       // owned global rows [jlo, jhi): [0, n+1) unless a row slab
+    double* red_out;    // slab mode: last block writes its pair's 3 local sums here
     int ntiles;         // ncx * nsy
     double mu, tau, ih, h2;
     PairCtl* ctl;       // [pairs]
@@ -119,8 +121,8 @@ __device__ __forceinline__ Strip make_strip(const SweepArgs& a, int pair, int pa
     const int cx = tile % a.ncx;
     const int sy = tile / a.ncx;
     s.i = cx * kOwn - 1 + lane;
-    s.j0 = sy * a.H;
-    s.j1 = min(s.j0 + a.H, L.n + 1);
+    s.j0 = a.jlo + sy * a.H;
+    s.j1 = min(s.j0 + a.H, a.jhi);
     double* pb = a.base + (long)pair * NSLOT * L.plane;
     s.phr = pb + (PHI0 + parity) * L.plane;
     s.mxr = pb + (MX0 + parity) * L.plane;

@@ -61,3 +61,34 @@ def test_batch_matches_single_pair(oracle):
         ref = oracle.ml_cp_run(rhos, p=1, rel_tol=1e-5)
         assert abs(dist[b] - ref.distance) <= 1e-4 * ref.distance
         assert all(abs(int(a) - c) <= 1 for a, c in zip(iters[b], ref.level_iters))
+
+
+def test_config5_full_size_fixed_iterations(oracle):
+    """BASELINE.json configs[4] at full size: two 20-component anisotropic
+    mixtures on 4096^2, 7 levels 64 -> 4096.  The oracle cannot converge a
+    4096^2 level in test time (~0.66 s per CPU sweep), so every level runs a
+    fixed 6 sweeps: sources, prolongation and sweeps must be bit-exact."""
+    img0, img1 = instances.config5_images()
+    rhos = oracle.ml_sources(img0, img1, 7)
+    assert rhos[0].shape == (65, 65) and rhos[-1].shape == (4097, 4097)
+    eps = [-1.0] * 7
+    rep = w1mg.ml_run(rhos, p=w1mg.PNorm.p2, eps=eps, max_iters=6)
+    ref = oracle.ml_cp_run(rhos, p=1, eps=eps, max_iters=6)
+    assert np.array_equal(rep.flux.x_edges, ref.mx)
+    assert np.array_equal(rep.flux.y_edges, ref.my)
+    assert np.array_equal(rep.potential.values, ref.phi)
+    assert abs(rep.distance - ref.distance) <= 1e-12 * ref.distance
+    # device restriction of the 4096^2 images agrees with the host rule
+    dev = w1mg.ml_sources(img0, img1, 7)
+    for d, h in zip(dev, rhos):
+        assert np.abs(d - h).max() <= 1e-12 * np.abs(h).max()
+
+
+def test_config5_reduced_converged(oracle):
+    """Config-5 densities at 512^2 (levels 64 -> 512), converged to the relative
+    rule: W1 within 1e-4 of the oracle cascade."""
+    img0, img1 = instances.config5_images(m=512)
+    rhos = instances.ml_sources(img0, img1, 4)
+    rep = w1mg.ml_run(rhos, p=w1mg.PNorm.p2, rel_tol=1e-5)
+    ref = oracle.ml_cp_run(rhos, p=1, rel_tol=1e-5)
+    assert abs(rep.distance - ref.distance) <= 1e-4 * ref.distance
