@@ -191,10 +191,13 @@ __device__ __forceinline__ void row_update(const SweepArgs& a, const Strip& s, i
 template <bool kPlusCross = false>
 __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int parity, int bid, int nblk,
                                              double s_dm2, double s_dp2, double s_cr) {
+    // blocks are 256 threads, 1-D (sweeps) or 32 x 8 (node kernels)
     __shared__ double red[kSweepWarps][3];
     __shared__ bool is_last;
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    const int tid = threadIdx.x + blockDim.x * threadIdx.y;
+    const int nthr = blockDim.x * blockDim.y;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
     s_dm2 = warp_sum(s_dm2);
     s_dp2 = warp_sum(s_dp2);
     s_cr = warp_sum(s_cr);
@@ -205,7 +208,7 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
     }
     __syncthreads();
     double* part = a.partial + (long)pair * nblk * 3;
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         double t0 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll
         for (int w = 0; w < kSweepWarps; ++w) {
@@ -225,7 +228,7 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
     __threadfence();
 
     double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-    for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+    for (int b = tid; b < nblk; b += nthr) {
         const volatile double* pv = part + b * 3;
         t0 += pv[0];
         t1 += pv[1];
@@ -241,7 +244,7 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
         red[warp][2] = t2;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         double sdm2 = 0.0, sdp2 = 0.0, scr = 0.0;
         for (int w = 0; w < kSweepWarps; ++w) {
             sdm2 += red[w][0];
