@@ -218,9 +218,10 @@ int w1mg_ml_pdhg_run(w1mg_ctx* ctx, int n_finest, const double* rho_levels,
                      w1mg_cp_report* rep);
 
 /* --------------------------------------------------------------- probes */
-/* Select the load engine of the fused sweep for subsequent launches in this
- * process: 0 = register-pipelined LDG, 1 = TMA bulk-copy ring (default).
- * Also settable with the environment variable W1MG_SWEEP=ldg|tma. */
+/* Select the engine of the fused sweep for subsequent launches in this
+ * process: 0 = register-pipelined LDG, 1 = one-sweep TMA bulk-copy ring,
+ * 2 = two-sweep (temporally blocked) TMA ring, 3 = auto (default: two-sweep
+ * for n >= 384, one-sweep below).  Also W1MG_SWEEP=ldg|tma|tma2|auto. */
 int w1mg_set_sweep_engine(int engine);
 /* Levels with n <= 64 run in one launch per level, one CTA per pair, state
  * resident in shared memory (1 = on, default) or through the streaming sweep

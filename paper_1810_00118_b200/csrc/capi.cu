@@ -262,7 +262,12 @@ void reduce_pairs(w1mg_ctx* c, F f, int w, int rows, int B, double s1, double s2
 // sweeps per HBM pass, falling back to the single-sweep TMA kernel for the
 // short loops and the stop fix-up
 constexpr int kTma2 = 2;
-int g_sweep_variant = kTma2;
+constexpr int kAuto = 3;  // two-sweep TMA for n >= 384, one-sweep TMA below (measured crossover)
+int g_sweep_variant = kAuto;
+
+bool two_sweep(const Level& lv) {
+    return g_sweep_variant == kTma2 || (g_sweep_variant == kAuto && lv.n >= 384);
+}
 
 void launch_sweep2(const Level& lv, int pn, int parity, cudaStream_t s) {
     dim3 blk(kSweepWarps * 32);
@@ -275,7 +280,7 @@ void launch_sweep2(const Level& lv, int pn, int parity, cudaStream_t s) {
 
 void launch_sweep(const Level& lv, int pn, int parity, cudaStream_t s) {
     dim3 blk(kSweepWarps * 32);
-    if (g_sweep_variant == kTma || g_sweep_variant == kTma2) {
+    if (g_sweep_variant != kLdg) {
         switch (pn) {
             case 0: cp_sweep_tma_kernel<0><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
             case 1: cp_sweep_tma_kernel<1><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
@@ -299,7 +304,7 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < K; ++k) {
-        if (g_sweep_variant == kTma2) launch_sweep2(lv, pn, k & 1, c->stream);
+        if (two_sweep(lv)) launch_sweep2(lv, pn, k & 1, c->stream);
         else launch_sweep(lv, pn, k & 1, c->stream);
     }
     CK(cudaStreamEndCapture(c->stream, &g));
@@ -348,7 +353,7 @@ void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
         return;
     }
     cudaGraphExec_t ex = sweep_graph(c, lv, pn, K);
-    const long per_launch = (g_sweep_variant == kTma2) ? 2 : 1;
+    const long per_launch = two_sweep(lv) ? 2 : 1;
     long launched = 0;
     for (long g = 0;; ++g) {
         CK(cudaGraphLaunch(ex, c->stream));
@@ -363,7 +368,7 @@ void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
         }
         if (launched >= max_iters + K * per_launch) break;  // every pair hit its cap by now
     }
-    if (g_sweep_variant == kTma2) {
+    if (two_sweep(lv)) {
         // replay the first sweep of pairs whose two-sweep launch stopped early
         launch_sweep(lv, pn, -1, c->stream);
         CK(cudaGetLastError());
@@ -539,7 +544,8 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_SWEEP"))
             g_sweep_variant = (std::string(v) == "ldg") ? kLdg
                               : (std::string(v) == "tma") ? kTma
-                                                          : kTma2;
+                              : (std::string(v) == "tma2") ? kTma2
+                                                           : kAuto;
         if (const char* v = std::getenv("W1MG_RESIDENT")) g_resident = std::atoi(v) != 0;
         auto* c = new w1mg_ctx();
         c->device = device;
@@ -1003,7 +1009,7 @@ int w1mg_interpolate_flux(w1mg_ctx* c, int nc, const double* cx, const double* c
 // Kernel probe: `iters` fused sweeps on B pairs of an n-cell level with the
 // stop rule disabled, after `warm` untimed sweeps; returns ms per sweep.
 int w1mg_set_sweep_engine(int engine) {
-    if (engine != kLdg && engine != kTma && engine != kTma2) return W1MG_EINVAL;
+    if (engine < kLdg || engine > kAuto) return W1MG_EINVAL;
     g_sweep_variant = engine;
     return W1MG_OK;
 }
@@ -1027,7 +1033,7 @@ int w1mg_sweep_probe(w1mg_ctx* c, int n, int B, int pnorm, long warm, long iters
         CK(cudaGetLastError());
         init_level_ctl(c, lv, 0.0, -1.0, 2 * (warm + iters) + 64);
         // kTma2: each launch is two sweeps; iters counts sweeps
-        const int per = (g_sweep_variant == kTma2) ? 2 : 1;
+        const int per = two_sweep(lv) ? 2 : 1;
         auto one = [&](long k) {
             if (per == 2) launch_sweep2(lv, pnorm, (int)(k & 1), c->stream);
             else launch_sweep(lv, pnorm, (int)(k & 1), c->stream);

@@ -113,7 +113,7 @@ cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
     if (*(volatile int*)&a.ctl[pair].done) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
     const int tile = blockIdx.x * kSweepWarps + warp;
     double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * kStages * kStreams * kChunk;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kSweepWarps * kStages * kStageBytes) +
@@ -144,7 +144,7 @@ cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
         const bool own = (lane >= 2) && (lane <= 30) && in;
         const double mu = a.mu, tau = a.tau, ih = a.ih;
 
-        const int ilo = i - lane;
+        const int ilo = cx * kOwn2 - 2;  // column of lane 0 (warp-uniform)
         const int a0 = ilo & ~1;
         const int sh = ilo - a0;
         const long c0 = L.at(a0, 0);

@@ -367,7 +367,9 @@ cp_sweep_tma_kernel(const SweepArgs a, const int parity_arg) {
     if (!sweep_gate(a.ctl + pair, parity_arg, parity)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    // warp index broadcast from lane 0: the compiler then keeps every TMA
+    // operand derived from it in uniform registers (no per-copy R2UR loop)
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     const int tile = blockIdx.x * kSweepWarps + warp;
     // per-warp ring: kStages x [kStreams][kChunk] doubles, then kStages mbarriers
     double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * kStages * kStreams * kChunk;
@@ -381,7 +383,7 @@ cp_sweep_tma_kernel(const SweepArgs a, const int parity_arg) {
         const int P = L.pitch;
         // chunk start: column i of lane 0 rounded down to even (16-B aligned;
         // rows are 256-B aligned and the front pad keeps column -2 in bounds)
-        const int ilo = s.i - lane;             // column of lane 0
+        const int ilo = (tile % a.ncx) * kOwn - 1;  // column of lane 0 (warp-uniform)
         const int a0 = ilo & ~1;
         const int sh = ilo - a0;                // 0 or 1
         const long c0 = L.at(a0, 0);

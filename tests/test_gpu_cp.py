@@ -66,7 +66,7 @@ def engine(request):
     L.w1mg_set_sweep_engine(eng)
     yield request.param
     L.w1mg_set_resident_engine(1)
-    L.w1mg_set_sweep_engine(2)
+    L.w1mg_set_sweep_engine(3)
 
 
 @pytest.mark.parametrize("iters", [300, 301])
