@@ -217,6 +217,30 @@ int w1mg_ml_pdhg_run(w1mg_ctx* ctx, int n_finest, const double* rho_levels,
                      double* phi, w1mg_level_stats* stats, double* fpr_hist, long hist_cap,
                      w1mg_cp_report* rep);
 
+/* ------------------------------------- row-slab decomposition (config 5) */
+/* One grid cut into contiguous row slabs with a one-row halo exchanged every
+ * sweep and a cross-slab sum of the residual.  Fields are
+ * bit-identical to the undecomposed solve. */
+typedef struct w1mg_slab_comm w1mg_slab_comm;
+/* bounds[0..nslabs]: slab r owns node rows [bounds[r], bounds[r+1]). */
+int w1mg_slab_bounds(int n, int nslabs, int* bounds);
+/* 128-byte NCCL unique id (rank 0 creates it, the caller broadcasts it). */
+int w1mg_nccl_unique_id(unsigned char* id128);
+/* One communicator per rank (one process per GPU, the context's device). */
+int w1mg_slab_comm_create(w1mg_ctx* ctx, int world, int rank, const unsigned char* id128,
+                          w1mg_slab_comm** out);
+void w1mg_slab_comm_destroy(w1mg_slab_comm* comm);
+/* cp_run on a decomposed grid.  comm == NULL: `nslabs` slabs emulated on the
+ * context's device (halo exchange by device copies).  comm != NULL: this
+ * rank's slab of comm's world (halos by ncclSend/ncclRecv, residual by
+ * ncclAllReduce, all on the context stream inside CUDA graphs).  Inputs are
+ * full-grid host arrays; outputs are written for the owned rows only; W1,
+ * dual, iterations and history are global. */
+int w1mg_slab_cp_run(w1mg_ctx* ctx, w1mg_slab_comm* comm, int n, int nslabs, const double* rho,
+                     const double* m0x, const double* m0y, const double* phi0, int pnorm,
+                     double mu, double tau, double tol, long max_iters, double* mx, double* my,
+                     double* phi, double* fpr_hist, long hist_cap, w1mg_cp_report* rep);
+
 /* --------------------------------------------------------------- probes */
 /* Select the engine of the fused sweep for subsequent launches in this
  * process: 0 = register-pipelined LDG, 1 = one-sweep TMA bulk-copy ring,

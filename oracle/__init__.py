@@ -140,6 +140,15 @@ class Oracle:
     def inner_h_nodes(self, n, a, b):
         return self.L.or_inner_h_nodes(n, _ptr(a), _ptr(b))
 
+    def cp_sweep_rows(self, n, jlo, jhi, mx, my, phi, rho, p, mu, tau, omx, omy, ophi):
+        """One sweep of node rows [jlo, jhi) (row-slab view); returns the
+        three owned partial sums."""
+        sums = np.zeros(3)
+        self.L.or_cp_sweep_rows(C.c_int(n), C.c_int(jlo), C.c_int(jhi), _ptr(mx), _ptr(my),
+                                _ptr(phi), _ptr(rho), C.c_int(p), C.c_double(mu),
+                                C.c_double(tau), _ptr(omx), _ptr(omy), _ptr(ophi), _ptr(sums))
+        return sums
+
     def compensated_sum(self, v):
         v = np.ascontiguousarray(v, dtype=np.float64)
         return self.L.or_compensated_sum(_ptr(v), v.size)

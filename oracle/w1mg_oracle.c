@@ -299,6 +299,64 @@ int or_cp_run(int n, const double* rho, const double* m0x, const double* m0y, co
     return 0;
 }
 
+/* One sweep restricted to node rows [jlo, jhi) of a full-grid state: the
+   row-slab view of cp_sweep used by the CPU multi-process test of the config-5
+   decomposition.  Reads phi rows [jlo-1, jhi], m rows [jlo-1, jhi) (halo
+   rows included), writes m and phi of the owned rows into o* (other rows are
+   left untouched) and the three partial sums of solver_cp.cpp:70 for the
+   owned nodes into sums[3]. */
+void or_cp_sweep_rows(int n, int jlo, int jhi, const double* mx, const double* my,
+                      const double* phi, const double* rho, int p, double mu, double tau,
+                      double* omx, double* omy, double* ophi, double* sums) {
+    const double ih = 1.0 / (1.0 / n);
+    const int w = n + 1;
+    const int r0 = jlo > 0 ? jlo - 1 : 0;
+    const int nr = jhi - r0;
+    double* ux = (double*)calloc((size_t)nr * w, 8);
+    double* uy = (double*)calloc((size_t)nr * w, 8);
+    double* dx = (double*)calloc((size_t)nr * w, 8);
+    double* dy = (double*)calloc((size_t)nr * w, 8);
+    double sdm2 = 0.0, sdp2 = 0.0, scr = 0.0;
+    for (int j = r0; j < jhi; ++j) {
+        const int hy = j < n;
+        for (int i = 0; i <= n; ++i) {
+            const int hx = i < n;
+            size_t kx = (size_t)j * n + i, ky = (size_t)j * w + i, kl = (size_t)(j - r0) * w + i;
+            double vx = 0.0, vy = 0.0;
+            if (hx) vx = mx[kx] - mu * ((phi[ky] - phi[ky + 1]) * ih);
+            if (hy) vy = my[ky] - mu * ((phi[ky] - phi[ky + w]) * ih);
+            double a, b;
+            or_shrink(vx, vy, mu, p, &a, &b);
+            if (hx) { dx[kl] = a - mx[kx]; ux[kl] = a; }
+            if (hy) { dy[kl] = b - my[ky]; uy[kl] = b; }
+            if (j >= jlo) {
+                if (hx) sdm2 += dx[kl] * dx[kl];
+                if (hy) sdm2 += dy[kl] * dy[kl];
+            }
+        }
+    }
+    for (int j = jlo; j < jhi; ++j)
+        for (int i = 0; i <= n; ++i) {
+            size_t kl = (size_t)(j - r0) * w + i, kg = (size_t)j * w + i;
+            double l = (i > 0) ? ux[kl - 1] : 0.0, r = (i < n) ? ux[kl] : 0.0;
+            double b = (j > 0) ? uy[kl - w] : 0.0, a = (j < n) ? uy[kl] : 0.0;
+            double divm = (r - l) * ih + (a - b) * ih;
+            double dl = (i > 0) ? dx[kl - 1] : 0.0, dr = (i < n) ? dx[kl] : 0.0;
+            double db = (j > 0) ? dy[kl - w] : 0.0, da = (j < n) ? dy[kl] : 0.0;
+            double divd = (dr - dl) * ih + (da - db) * ih;
+            double d = tau * (divm + divd - rho[kg]);
+            ophi[kg] = phi[kg] + d;
+            if (i < n) omx[(size_t)j * n + i] = ux[kl];
+            if (j < n) omy[kg] = uy[kl];
+            sdp2 += d * d;
+            scr += d * divd;
+        }
+    free(ux); free(uy); free(dx); free(dy);
+    sums[0] = sdm2;
+    sums[1] = sdp2;
+    sums[2] = scr;
+}
+
 /* cp_residual, proj/src/solver_cp.cpp:102-111 */
 double or_cp_residual(int n, const double* cmx, const double* cmy, const double* cphi,
                       const double* pmx, const double* pmy, const double* pphi, double mu,

@@ -117,6 +117,15 @@ def lib():
         L.w1mg_ml_pdhg_run.argtypes = [C.c_void_p, C.c_int, _dp, C.POINTER(MLParams), _dp, _dp,
                                        _dp, _dp, _dp, C.POINTER(LevelStatsC), _dp, C.c_long,
                                        C.POINTER(CPReport)]
+        L.w1mg_slab_bounds.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int)]
+        L.w1mg_nccl_unique_id.argtypes = [C.c_char_p]
+        L.w1mg_slab_comm_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p,
+                                            C.POINTER(C.c_void_p)]
+        L.w1mg_slab_comm_destroy.argtypes = [C.c_void_p]
+        L.w1mg_slab_cp_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _dp, _dp, _dp,
+                                       _dp, C.c_int, C.c_double, C.c_double, C.c_double,
+                                       C.c_long, _dp, _dp, _dp, _dp, C.c_long,
+                                       C.POINTER(CPReport)]
         L.w1mg_set_sweep_engine.argtypes = [C.c_int]
         L.w1mg_set_resident_engine.argtypes = [C.c_int]
         _lib = L

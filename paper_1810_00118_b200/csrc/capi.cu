@@ -130,14 +130,23 @@ struct Level {
     dim3 grid;
     SweepArgs args2{};  // two-sweep engine
     dim3 grid2;
+    bool slab = false;  // row slab of a decomposed grid (one-sweep engine only)
 };
 
+// jhi < 0: whole grid.  Otherwise a row slab owning global rows [jlo, jhi),
+// stored with one halo row below and two above (Layout::make_slab).
 Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, double tau,
-                 double* hist, long hist_cap) {
+                 double* hist, long hist_cap, int jlo = 0, int jhi = -1) {
     Level lv;
     lv.n = n;
     lv.B = B;
-    lv.L = Layout::make(n);
+    lv.slab = jhi >= 0;
+    if (!lv.slab) {
+        jlo = 0;
+        jhi = n + 1;
+    }
+    const int nrows = jhi - jlo;
+    lv.L = lv.slab ? Layout::make_slab(n, jlo - 1, jhi + 2) : Layout::make(n);
     lv.base = c->get<double>(tag + ".base", (size_t)B * NSLOT * lv.L.plane);
     lv.ctl = c->get<PairCtl>(tag + ".ctl", B);
     lv.ticket = c->get<unsigned>(tag + ".ticket", B);
@@ -151,15 +160,15 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     const long target = (long)c->num_sms * 32;
     int H = 64;
     while (H > 2) {
-        long tiles = (long)B * a.ncx * ((n + 1 + H - 1) / H);
+        long tiles = (long)B * a.ncx * ((nrows + H - 1) / H);
         if (tiles >= target) break;
         H >>= 1;
     }
     a.H = H;
-    a.jlo = 0;
-    a.jhi = n + 1;
+    a.jlo = jlo;
+    a.jhi = jhi;
     a.red_out = nullptr;
-    a.nsy = (n + 1 + H - 1) / H;
+    a.nsy = (nrows + H - 1) / H;
     a.ntiles = a.ncx * a.nsy;
     a.mu = mu;
     a.tau = tau;
@@ -178,12 +187,12 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     a2.ncx = (n + 1 + kOwn2 - 1) / kOwn2;
     int H2 = 64;
     while (H2 > 4) {
-        long tiles = (long)B * a2.ncx * ((n + 1 + H2 - 1) / H2);
+        long tiles = (long)B * a2.ncx * ((nrows + H2 - 1) / H2);
         if (tiles >= target) break;
         H2 >>= 1;
     }
     a2.H = H2;
-    a2.nsy = (n + 1 + H2 - 1) / H2;
+    a2.nsy = (nrows + H2 - 1) / H2;
     a2.ntiles = a2.ncx * a2.nsy;
     lv.grid2 = dim3((a2.ntiles + kSweepWarps - 1) / kSweepWarps, B, 1);
     lv.partial = c->get<double>(
@@ -266,6 +275,7 @@ constexpr int kAuto = 3;  // two-sweep TMA for n >= 384, one-sweep TMA below (me
 int g_sweep_variant = kAuto;
 
 bool two_sweep(const Level& lv) {
+    if (lv.slab) return false;  // slabs exchange a one-row halo per sweep
     return g_sweep_variant == kTma2 || (g_sweep_variant == kAuto && lv.n >= 384);
 }
 
@@ -1057,3 +1067,4 @@ int w1mg_sweep_probe(w1mg_ctx* c, int n, int B, int pnorm, long warm, long iters
 }  // extern "C"
 
 #include "pdhg_engine.cuh"
+#include "slab_engine.cuh"

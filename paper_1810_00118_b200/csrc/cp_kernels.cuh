@@ -186,6 +186,32 @@ __device__ __forceinline__ void row_update(const SweepArgs& a, const Strip& s, i
     dyb = dy;
 }
 
+// R^k from the three global sums, residual history, and the stop rule of
+// solver_cp.cpp:128-136 (one thread).
+template <bool kPlusCross = false>
+__device__ __forceinline__ void finalize_pair(const SweepArgs& a, int pair, int parity,
+                                              double sdm2, double sdp2, double scr) {
+    PairCtl* ctl = a.ctl + pair;
+    // Eq. 9 (CP, minus cross term) or Eq. 12 (PDHG, plus cross term)
+    double fpr = kPlusCross ? a.h2 * (sdm2 / a.mu + sdp2 / a.tau + 2.0 * scr)
+                            : a.h2 * (sdm2 / a.mu + sdp2 / a.tau - 2.0 * scr);
+    long k = ctl->it;
+    if (a.hist && k < a.hist_cap) a.hist[(long)pair * a.hist_cap + k] = fpr;
+    ctl->it = k + 1;
+    ctl->fpr = fpr;
+    ctl->cur = 1 - parity;
+    bool finite = isfinite(fpr);
+    if (!finite) ctl->nonfinite = 1;
+    if (ctl->redo) {
+        // fix-up sweep after a two-sweep launch stopped on its first
+        // sweep: the pair is already counted as done
+        ctl->redo = 0;
+    } else if (fpr < ctl->tol || k + 1 >= ctl->max_it || !finite) {
+        ctl->done = 1;
+        if (a.ndone) atomicAdd(a.ndone, 1);
+    }
+}
+
 // Block + last-block reduction of the three residual sums; the last block of
 // a pair finalises R^k and the stop flag (solver_cp.cpp:70, :128-136).
 template <bool kPlusCross = false>
@@ -251,26 +277,16 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
             sdp2 += red[w][1];
             scr += red[w][2];
         }
-        PairCtl* ctl = a.ctl + pair;
-        // Eq. 9 (CP, minus cross term) or Eq. 12 (PDHG, plus cross term)
-        double fpr = kPlusCross ? a.h2 * (sdm2 / a.mu + sdp2 / a.tau + 2.0 * scr)
-                                : a.h2 * (sdm2 / a.mu + sdp2 / a.tau - 2.0 * scr);
-        long k = ctl->it;
-        if (a.hist && k < a.hist_cap) a.hist[(long)pair * a.hist_cap + k] = fpr;
-        ctl->it = k + 1;
-        ctl->fpr = fpr;
-        ctl->cur = 1 - parity;
-        bool finite = isfinite(fpr);
-        if (!finite) ctl->nonfinite = 1;
-        if (ctl->redo) {
-            // fix-up sweep after a two-sweep launch stopped on its first
-            // sweep: the pair is already counted as done
-            ctl->redo = 0;
-        } else if (fpr < ctl->tol || k + 1 >= ctl->max_it || !finite) {
-            ctl->done = 1;
-            atomicAdd(a.ndone, 1);
-        }
         a.ticket[pair] = 0u;
+        if (a.red_out) {
+            // row slab: publish this slab's sums; the cross-slab reduction
+            // (device copy or NCCL all-reduce) then runs finalize_pair
+            a.red_out[(long)pair * 3 + 0] = sdm2;
+            a.red_out[(long)pair * 3 + 1] = sdp2;
+            a.red_out[(long)pair * 3 + 2] = scr;
+        } else {
+            finalize_pair<kPlusCross>(a, pair, parity, sdm2, sdp2, scr);
+        }
         __threadfence();
     }
 }

@@ -613,3 +613,59 @@ def ml_pdhg_run(rho_levels: list, p: PNorm = PNorm.p2, rel_tol: float = 1e-5, ep
     lv = [LevelStats(s.h, s.eps, s.iters, s.fpr_final, s.seconds) for s in st]
     return SolveReport(rep.distance, rep.dual_value, bool(rep.converged), rep.iterations, m, phi,
                        d, lv, hist[: min(lv[-1].iters, hist_cap)].copy(), rep.seconds)
+
+
+# ------------------------------------------------- row slabs (config 5)
+def slab_bounds(n: int, nslabs: int) -> list:
+    """Node-row bounds of the row-slab partition (slab r owns [b[r], b[r+1]))."""
+    out = (C.c_int * (nslabs + 1))()
+    check(_lib.lib().w1mg_slab_bounds(n, nslabs, out))
+    return list(out)
+
+
+class SlabComm:
+    """NCCL communicator for one rank of a row-slab decomposition (one process
+    per GPU).  `unique_id` (128 bytes) comes from new_unique_id() on rank 0 and
+    is broadcast by the caller (e.g. torch.distributed)."""
+
+    def __init__(self, world: int, rank: int, unique_id: bytes, device: int = 0):
+        self.h = C.c_void_p()
+        check(_lib.lib().w1mg_slab_comm_create(_lib.default_context(device).h, world, rank,
+                                               unique_id, C.byref(self.h)))
+        self.world, self.rank = world, rank
+
+    @staticmethod
+    def new_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(_lib.lib().w1mg_nccl_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if self.h:
+            _lib.lib().w1mg_slab_comm_destroy(self.h)
+            self.h = None
+
+
+def slab_cp_run(rho: SourceField, params: SolverParams, nslabs: int = 2,
+                comm: Optional[SlabComm] = None, m0: Optional[FluxField] = None,
+                phi0: Optional[ScalarField] = None, hist_cap: int = 1 << 20) -> SolveReport:
+    """cp_run on a grid cut into row slabs (config 5).  comm=None: nslabs
+    slabs emulated on one device; otherwise this rank's slab (owned rows of
+    the returned fields are filled, the rest is zero)."""
+    g = rho.grid()
+    step = cp_step_size(g, params.step_mode)
+    m = FluxField(g)
+    phi = ScalarField(g)
+    cap = int(min(hist_cap, params.max_iters))
+    hist = np.zeros(max(cap, 1))
+    rep = CPReport()
+    check(_lib.lib().w1mg_slab_cp_run(
+        _ctx(), None if comm is None else comm.h, g.n, nslabs, ptr(rho.rho.values),
+        None if m0 is None else ptr(m0.x_edges), None if m0 is None else ptr(m0.y_edges),
+        None if phi0 is None else ptr(phi0.values), int(params.p), step, step,
+        params.tolerance, int(params.max_iters), ptr(m.x_edges), ptr(m.y_edges), ptr(phi.values),
+        ptr(hist), cap, C.byref(rep)))
+    return SolveReport(rep.distance, rep.dual_value, bool(rep.converged), rep.iterations, m, phi,
+                       None, [LevelStats(g.h, params.tolerance, rep.iterations, rep.fpr_final,
+                                         rep.seconds)],
+                       hist[: min(rep.iterations, cap)].copy(), rep.seconds)

@@ -1,0 +1,87 @@
+"""GPU parity of the row-slab decomposition (config 5): the fused sweep on
+row slabs with a one-row halo exchange and a cross-slab residual sum must give
+fields bit-identical to the undecomposed oracle.  Slabs are emulated on one
+B200 (device-copy halos), and the NCCL transport is exercised with a
+single-rank communicator (the multi-rank protocol itself is covered on CPU by
+tests/test_slab_gloo.py)."""
+import numpy as np
+import pytest
+
+from paper_1810_00118_b200 import instances
+from paper_1810_00118_b200 import w1mg
+
+pytestmark = pytest.mark.gpu
+
+
+def _src(rho):
+    return w1mg.SourceField(w1mg.ScalarField(w1mg.GridSpec(rho.shape[0] - 1), rho))
+
+
+def _rand(n, seed):
+    rng = np.random.default_rng(seed)
+    return instances.make_source(rng.random((n + 1, n + 1)), rng.random((n + 1, n + 1)), n)
+
+
+@pytest.mark.parametrize("nslabs", [1, 2, 3, 5])
+@pytest.mark.parametrize("n", [64, 100, 257])
+def test_slab_fixed_iterations_bit_exact(oracle, n, nslabs):
+    rho = _random = _rand(n, n + nslabs)
+    prm = w1mg.SolverParams(p=w1mg.PNorm.p2, tolerance=-1.0, max_iters=75)
+    rep = w1mg.slab_cp_run(_src(rho), prm, nslabs=nslabs)
+    ref = oracle.cp_run(rho, p=1, tol=-1.0, max_iters=75)
+    assert rep.iterations == 75
+    assert np.array_equal(rep.flux.x_edges, ref.mx)
+    assert np.array_equal(rep.flux.y_edges, ref.my)
+    assert np.array_equal(rep.potential.values, ref.phi)
+    assert abs(rep.distance - ref.distance) <= 1e-12 * ref.distance
+    np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-10)
+
+
+def test_slab_warm_start_and_converged(oracle):
+    n = 96
+    rho = instances.config1_source(n)
+    rng = np.random.default_rng(0)
+    m0 = (1e-3 * rng.standard_normal((n + 1, n)), 1e-3 * rng.standard_normal((n, n + 1)))
+    phi0 = 1e-3 * rng.standard_normal((n + 1, n + 1))
+    g = w1mg.GridSpec(n)
+    prm = w1mg.SolverParams(p=w1mg.PNorm.p2, tolerance=1e-8, max_iters=200000)
+    rep = w1mg.slab_cp_run(_src(rho), prm, nslabs=4, m0=w1mg.FluxField(g, *m0),
+                           phi0=w1mg.ScalarField(g, phi0))
+    ref = oracle.cp_run(rho, p=1, tol=1e-8, max_iters=200000, m0=m0, phi0=phi0)
+    assert rep.converged and abs(rep.iterations - ref.iterations) <= 1
+    assert abs(rep.distance - ref.distance) <= 1e-4 * ref.distance
+
+
+def test_slab_4096_full_size(oracle):
+    """Config-5 finest grid in 8 slabs (the 8-GPU partition), 4 sweeps."""
+    n = 4096
+    rho = _rand(n, 4096)
+    prm = w1mg.SolverParams(p=w1mg.PNorm.p2, tolerance=-1.0, max_iters=4)
+    rep = w1mg.slab_cp_run(_src(rho), prm, nslabs=8)
+    ref = oracle.cp_run(rho, p=1, tol=-1.0, max_iters=4)
+    assert np.array_equal(rep.potential.values, ref.phi)
+    assert np.array_equal(rep.flux.x_edges, ref.mx)
+    assert np.array_equal(rep.flux.y_edges, ref.my)
+
+
+def test_slab_nccl_single_rank(oracle):
+    """The NCCL transport (send/recv/allreduce inside the CUDA graph) with a
+    one-rank communicator: exercises the NCCL code path on one GPU."""
+    uid = w1mg.SlabComm.new_unique_id()
+    comm = w1mg.SlabComm(1, 0, uid)
+    try:
+        n = 128
+        rho = _rand(n, 7)
+        prm = w1mg.SolverParams(p=w1mg.PNorm.p2, tolerance=-1.0, max_iters=40)
+        rep = w1mg.slab_cp_run(_src(rho), prm, comm=comm)
+        ref = oracle.cp_run(rho, p=1, tol=-1.0, max_iters=40)
+        assert np.array_equal(rep.potential.values, ref.phi)
+        assert abs(rep.distance - ref.distance) <= 1e-12 * ref.distance
+    finally:
+        comm.close()
+
+
+def test_slab_bounds_partition():
+    b = w1mg.slab_bounds(4096, 8)
+    assert b[0] == 0 and b[-1] == 4097 and len(b) == 9
+    assert all(b[r + 1] - b[r] in (512, 513) for r in range(8))
