@@ -170,6 +170,19 @@ def dist_setup():
     return world, rank, local
 
 
+def measured_traffic():
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/traffic.json: 256 pairs x 512^2,
+    one two-sweep launch = 2 x 7.54 GB algorithmic one-sweep bytes), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    # bytes per launch of the captured configuration (256 pairs, one two-sweep launch)
+    return d.get("dram_bytes_per_launch")
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -471,8 +484,10 @@ def main():
                         "cell_updates_per_s": c_ / s_}
                        for n, s_, c_ in zip(level_sizes(), lev_s, lev_cu)],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None,
-                         "kernel": "w1mg_dev::cp_sweep_kernel<1> (fused PD sweep, 512^2 level)",
+                         "frac": achieved / hbm, "traffic": measured_traffic(),
+                         "kernel": "w1mg_dev::cp_sweep2_tma_kernel<1> (two fused PD sweeps per "
+                                   "HBM pass, 512^2 level); achieved = algorithmic 8(3V+4E) "
+                                   "bytes per sweep / device time per sweep",
                          "bytes_per_sweep": alg_bytes_per_sweep(M), "peak_kind": peak_kind},
             "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "cpu_baseline": cpu, "parity_sample": parity,

@@ -106,31 +106,19 @@ __device__ __forceinline__ void finish_sweep2(const SweepArgs& a, int pair, int 
     __threadfence();
 }
 
-template <int PN>
-__global__ void __launch_bounds__(kSweepWarps * 32, 2)
-cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
-    const int pair = blockIdx.y;
-    if (*(volatile int*)&a.ctl[pair].done) return;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31;
-    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
-    const int tile = blockIdx.x * kSweepWarps + warp;
-    double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * kStages * kStreams * kChunk;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kSweepWarps * kStages * kStageBytes) +
-                     warp * kStages;
-    // residual partial sums of sweep A (k) and sweep B (k+1)
-    double a_dm2 = 0.0, a_dp2 = 0.0, a_cr = 0.0;
-    double b_dm2 = 0.0, b_dp2 = 0.0, b_cr = 0.0;
-
-    if (tile < a.ntiles) {
+// The two-sweep march of one warp over its tile.  kInt: the tile's 32 columns
+// and all rows it touches lie strictly inside the grid (no absent edges, no
+// boundary rows), so every mask folds to a constant.
+template <int PN, bool kInt>
+__device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity, int cx, int j0,
+                                       int j1, int lane, double* ring, uint64_t* bars,
+                                       double& a_dm2, double& a_dp2, double& a_cr, double& b_dm2,
+                                       double& b_dp2, double& b_cr) {
+    {
         const Layout L = a.L;
         const int n = L.n;
         const int P = L.pitch;
-        const int cx = tile % a.ncx;
-        const int sy = tile / a.ncx;
         const int i = cx * kOwn2 - 2 + lane;
-        const int j0 = a.jlo + sy * a.H;
-        const int j1 = min(j0 + a.H, a.jhi);
         double* pb = a.base + (long)pair * NSLOT * L.plane;
         const double* __restrict__ phr = pb + (PHI0 + parity) * L.plane;
         const double* __restrict__ mxr = pb + (MX0 + parity) * L.plane;
@@ -139,8 +127,8 @@ cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
         double* __restrict__ phw = pb + (PHI0 + 1 - parity) * L.plane;
         double* __restrict__ mxw = pb + (MX0 + 1 - parity) * L.plane;
         double* __restrict__ myw = pb + (MY0 + 1 - parity) * L.plane;
-        const bool in = (i >= 0) && (i <= n);
-        const bool hx = (i >= 0) && (i < n);
+        const bool in = kInt || ((i >= 0) && (i <= n));
+        const bool hx = kInt || ((i >= 0) && (i < n));
         const bool own = (lane >= 2) && (lane <= 30) && in;
         const double mu = a.mu, tau = a.tau, ih = a.ih;
 
@@ -199,13 +187,13 @@ cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
             const int rB = rA - 1;   // B row of this step
             double fA = 0.0, uxA = 0.0, uyAn = 0.0, dxA = 0.0, dyAn = 0.0, r = 0.0;
             double pu = 0.0, pur = 0.0;
-            if (rA <= rA1) {
+            if (kInt || rA <= rA1) {
                 const int st = t % kStages;
                 mbar_wait(&bars[st], (uint32_t)((t / kStages) & 1));
                 const double* c = ring + st * kStreams * kChunk + sh + lane;
-                const bool hy = in && (rA < n);
+                const bool hy = kInt || (in && (rA < n));
                 pu = hy ? c[0] : 0.0;
-                pur = (hx && rA < n) ? c[1] : 0.0;
+                pur = (kInt || (hx && rA < n)) ? c[1] : 0.0;
                 const double mxo = hx ? c[kChunk] : 0.0;
                 const double myo = hy ? c[2 * kChunk] : 0.0;
                 r = in ? c[3 * kChunk] : 0.0;
@@ -232,7 +220,7 @@ cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
             }
             // ---- sweep B at row rB (inputs: A's rows rB and rB+1)
             if (rB >= rA0) {
-                const bool hyB = in && (rB < n);
+                const bool hyB = kInt || (in && (rB < n));
                 const double pcB = fA_prev;
                 const double prB = __shfl_down_sync(0xffffffffu, fA_prev, 1);
                 const double puB = hyB ? fA : 0.0;
@@ -263,6 +251,39 @@ cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
             pc = pu;
             pr = pur;
         }
+    }
+}
+
+template <int PN>
+__global__ void __launch_bounds__(kSweepWarps * 32, 2)
+cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
+    const int pair = blockIdx.y;
+    if (*(volatile int*)&a.ctl[pair].done) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
+    const int tile = blockIdx.x * kSweepWarps + warp;
+    double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * kStages * kStreams * kChunk;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + kSweepWarps * kStages * kStageBytes) +
+                     warp * kStages;
+    // residual partial sums of sweep A (k) and sweep B (k+1)
+    double a_dm2 = 0.0, a_dp2 = 0.0, a_cr = 0.0;
+    double b_dm2 = 0.0, b_dp2 = 0.0, b_cr = 0.0;
+    if (tile < a.ntiles) {
+        const int cx = tile % a.ncx;
+        const int sy = tile / a.ncx;
+        const int j0 = a.jlo + sy * a.H;
+        const int j1 = min(j0 + a.H, a.jhi);
+        const int ilo = cx * kOwn2 - 2;
+        const int n = a.L.n;
+        // interior: columns ilo..ilo+31 all carry an x-edge, rows j0-2..j1 < n
+        const bool interior = (ilo >= 0) && (ilo + 31 < n) && (j0 >= 2) && (j1 < n);
+        if (interior)
+            march2<PN, true>(a, pair, parity, cx, j0, j1, lane, ring, bars, a_dm2, a_dp2, a_cr,
+                             b_dm2, b_dp2, b_cr);
+        else
+            march2<PN, false>(a, pair, parity, cx, j0, j1, lane, ring, bars, a_dm2, a_dp2, a_cr,
+                              b_dm2, b_dp2, b_cr);
     }
     finish_sweep2(a, pair, parity, a_dm2, a_dp2, a_cr, b_dm2, b_dp2, b_cr);
 }
