@@ -271,12 +271,12 @@ void reduce_pairs(w1mg_ctx* c, F f, int w, int rows, int B, double s1, double s2
 // sweeps per HBM pass, falling back to the single-sweep TMA kernel for the
 // short loops and the stop fix-up
 constexpr int kTma2 = 2;
-constexpr int kAuto = 3;  // two-sweep TMA for n >= 384, one-sweep TMA below (measured crossover)
+constexpr int kAuto = 3;  // two-sweep TMA for n >= 96 (faster from 128 up, measured), one-sweep below
 int g_sweep_variant = kAuto;
 
 bool two_sweep(const Level& lv) {
     if (lv.slab) return false;  // slabs exchange a one-row halo per sweep
-    return g_sweep_variant == kTma2 || (g_sweep_variant == kAuto && lv.n >= 384);
+    return g_sweep_variant == kTma2 || (g_sweep_variant == kAuto && lv.n >= 96);
 }
 
 void launch_sweep2(const Level& lv, int pn, int parity, cudaStream_t s) {
