@@ -126,6 +126,9 @@ def lib():
                                        _dp, C.c_int, C.c_double, C.c_double, C.c_double,
                                        C.c_long, _dp, _dp, _dp, _dp, C.c_long,
                                        C.POINTER(CPReport)]
+        L.w1mg_ml_slab_cp_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _dp,
+                                          C.POINTER(MLParams), _dp, _dp, _dp,
+                                          C.POINTER(LevelStatsC), C.POINTER(CPReport)]
         L.w1mg_set_sweep_engine.argtypes = [C.c_int]
         L.w1mg_set_resident_engine.argtypes = [C.c_int]
         _lib = L

@@ -268,9 +268,143 @@ void slab_run(w1mg_ctx* c, SlabSet& s, int pn, double tol, long max_iters) {
     CK(cudaGraphExecDestroy(ex));
 }
 
+// Device-side load of slab rows from a whole-grid level (buffer 0 of pair 0).
+void slab_load_from_level(w1mg_ctx* c, SlabSet& s, const Level& full) {
+    const int n = s.n;
+    const size_t row_bytes = (size_t)full.L.pitch * 8;
+    for (auto& lv : s.lv) {
+        zero_level(c, lv);
+        const int r0 = std::max(lv.args.jlo - 1, 0), r1 = std::min(lv.args.jhi + 1, n + 1);
+        for (int slot : {PHI0, MX0, MY0, RHO})
+            CK(cudaMemcpy2DAsync(slot_ptr(lv, 0, slot) + lv.L.at(0, r0), row_bytes,
+                                 slot_ptr(full, 0, slot) + full.L.at(0, r0), row_bytes, row_bytes,
+                                 r1 - r0, cudaMemcpyDeviceToDevice, c->stream));
+    }
+}
+
 }  // namespace
 
 extern "C" {
+
+// Cascade for one large grid (config 5): levels 0..L-2 replicated (identical
+// on every rank), the finest level row-slab partitioned.  comm == NULL:
+// `nslabs` slabs emulated on one device.  Outputs: finest owned rows.
+int w1mg_ml_slab_cp_run(w1mg_ctx* c, w1mg_slab_comm* comm, int nslabs, int n_finest,
+                        const double* rho_levels, const w1mg_ml_params* prm, double* mx,
+                        double* my, double* phi, w1mg_level_stats* stats, w1mg_cp_report* rep) {
+    return guard([&] {
+        check_n(n_finest);
+        check_ml(prm);
+        const int levels = prm->levels;
+        if (levels < 2) fail(W1MG_EINVAL, "ml_slab: need at least 2 levels");
+        std::vector<Level> lv =
+            make_levels(c, "mlsl", n_finest, levels, 1, prm->step_mode, nullptr, 0);
+        size_t off = 0;
+        for (auto& L : lv) {
+            zero_level(c, L);
+            put_nodes(c, L, 0, RHO, rho_levels + off, cudaMemcpyDefault);
+            off += (size_t)(L.n + 1) * (L.n + 1);
+        }
+        // replicated coarse cascade
+        std::vector<Level> coarse(lv.begin(), lv.end() - 1);
+        w1mg_ml_params pc = *prm;
+        pc.levels = levels - 1;
+        long* it = c->get<long>("mlsl.iters", levels);
+        double* ff = c->get<double>("mlsl.fpr", levels);
+        double* tl = c->get<double>("mlsl.tol", levels);
+        std::vector<double> secs;
+        run_cascade(c, coarse, pc, it, ff, tl, &secs);
+        // finest: prolong into the whole-grid level, then cut into slabs
+        Level& F = lv.back();
+        dim3 blk(32, 8);
+        prolong_kernel<<<node_grid(F.n, 1, blk), blk, 0, c->stream>>>(
+            coarse.back().base, coarse.back().L, coarse.back().ctl, F.base, F.L);
+        ++c->launches;
+        CK(cudaGetLastError());
+        double tol = (prm->rel_tol > 0 || !prm->eps) ? 0.0 : prm->eps[levels - 1];
+        if (prm->rel_tol > 0) {
+            double* rs = c->get<double>("mlsl.rho_sq", 1);
+            const double h = 1.0 / F.n;
+            reduce_pairs(c, FSlotSq{F.base, F.L, RHO}, F.n + 1, F.n + 1, 1, h * h, 1.0, rs);
+            double hrs = 0.0;
+            CK(cudaMemcpyAsync(&hrs, rs, 8, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            tol = (prm->rel_tol * F.args.tau) * hrs;  // as init_ctl_kernel
+        }
+        const double step = w1mg_cp_step_size(F.n, prm->step_mode);
+        SlabSet s = make_slabs(c, "mlsl.slab", F.n, nslabs, comm, step, step, nullptr, 0);
+        slab_load_from_level(c, s, F);
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, c->stream));
+        slab_run(c, s, prm->pnorm, tol, prm->max_iters);
+        CK(cudaEventRecord(e1, c->stream));
+        PairCtl hc;
+        CK(cudaMemcpyAsync(&hc, s.ctl, sizeof(PairCtl), cudaMemcpyDeviceToHost, c->stream));
+        std::vector<long> hit(levels - 1);
+        std::vector<double> hff(levels - 1), htl(levels - 1);
+        CK(cudaMemcpyAsync(hit.data(), it, (levels - 1) * sizeof(long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(hff.data(), ff, (levels - 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(htl.data(), tl, (levels - 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        // W1 over owned rows (+ sum over ranks)
+        double w1 = 0.0, du = 0.0;
+        double* vals = c->get<double>("mlsl.vals", 2 * s.lv.size());
+        const double h = 1.0 / F.n;
+        for (size_t q = 0; q < s.lv.size(); ++q) {
+            const Level& L = s.lv[q];
+            const int rows = L.args.jhi - L.args.jlo;
+            if (prm->pnorm == 0)
+                reduce_pairs(c, FSlabPrimal<0>{L.base, L.L, L.ctl, L.args.jlo}, F.n + 1, rows, 1, h, h, vals + 2 * q);
+            else if (prm->pnorm == 1)
+                reduce_pairs(c, FSlabPrimal<1>{L.base, L.L, L.ctl, L.args.jlo}, F.n + 1, rows, 1, h, h, vals + 2 * q);
+            else
+                reduce_pairs(c, FSlabPrimal<2>{L.base, L.L, L.ctl, L.args.jlo}, F.n + 1, rows, 1, h, h, vals + 2 * q);
+            reduce_pairs(c, FSlabDual{L.base, L.L, L.ctl, L.args.jlo}, F.n + 1, rows, 1, h, h, vals + 2 * q + 1);
+            if (mx) slab_get(c, L, MX0 + hc.cur, mx, F.n, L.args.jlo, L.args.jhi);
+            if (my) slab_get(c, L, MY0 + hc.cur, my, F.n + 1, L.args.jlo, std::min(L.args.jhi, F.n));
+            if (phi) slab_get(c, L, PHI0 + hc.cur, phi, F.n + 1, L.args.jlo, L.args.jhi);
+        }
+        std::vector<double> hv(2 * s.lv.size());
+        CK(cudaMemcpyAsync(hv.data(), vals, hv.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (size_t q = 0; q < s.lv.size(); ++q) {
+            w1 += hv[2 * q];
+            du += hv[2 * q + 1];
+        }
+        if (comm) {
+            double* d = c->get<double>("mlsl.vals_all", 2);
+            double loc[2] = {w1, du};
+            CK(cudaMemcpyAsync(d, loc, 16, cudaMemcpyHostToDevice, c->stream));
+            check_nccl(ncclAllReduce(d, d, 2, ncclDouble, ncclSum, comm->comm, c->stream), "allreduce W1");
+            CK(cudaMemcpyAsync(loc, d, 16, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            w1 = loc[0];
+            du = loc[1];
+        }
+        long total = hc.it;
+        double tsec = ms * 1e-3;
+        for (int l = 0; l < levels - 1; ++l) {
+            total += hit[l];
+            tsec += secs[l];
+            if (stats) stats[l] = {1.0 / lv[l].n, htl[l], hit[l], hff[l], secs[l]};
+        }
+        if (stats) stats[levels - 1] = {1.0 / F.n, tol, hc.it, hc.fpr, ms * 1e-3};
+        if (rep) {
+            rep->distance = w1;
+            rep->dual_value = du;
+            rep->iterations = total;
+            rep->fpr_final = hc.fpr;
+            rep->converged = (hc.fpr < tol) ? 1 : 0;
+            rep->seconds = tsec;
+        }
+    });
+}
 
 int w1mg_slab_bounds(int n, int nslabs, int* bounds) {
     return guard([&] {

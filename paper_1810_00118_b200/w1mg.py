@@ -616,6 +616,29 @@ def ml_pdhg_run(rho_levels: list, p: PNorm = PNorm.p2, rel_tol: float = 1e-5, ep
 
 
 # ------------------------------------------------- row slabs (config 5)
+def ml_slab_run(rho_levels: list, nslabs: int = 2, comm=None, p: PNorm = PNorm.p2,
+                rel_tol: float = 1e-5, eps=None, max_iters: int = 5_000_000,
+                step_mode: StepMode = StepMode.practical) -> SolveReport:
+    """Config-5 cascade: coarse levels replicated, the finest level cut into
+    row slabs (emulated on one device when comm is None, else this rank's slab
+    of an NCCL decomposition; the returned finest fields hold the owned rows)."""
+    levels = len(rho_levels)
+    nf = rho_levels[-1].shape[0] - 1
+    flat = np.ascontiguousarray(np.concatenate([np.ravel(r) for r in rho_levels]))
+    prm, keep = _ml_params(levels, p, step_mode, rel_tol, eps, max_iters)
+    g = GridSpec(nf)
+    m, phi = FluxField(g), ScalarField(g)
+    st = (LevelStatsC * levels)()
+    rep = CPReport()
+    check(_lib.lib().w1mg_ml_slab_cp_run(_ctx(), None if comm is None else comm.h, nslabs, nf,
+                                         ptr(flat), C.byref(prm), ptr(m.x_edges), ptr(m.y_edges),
+                                         ptr(phi.values), st, C.byref(rep)))
+    del keep
+    lv = [LevelStats(s.h, s.eps, s.iters, s.fpr_final, s.seconds) for s in st]
+    return SolveReport(rep.distance, rep.dual_value, bool(rep.converged), rep.iterations, m, phi,
+                       None, lv, np.zeros(0), rep.seconds)
+
+
 def slab_bounds(n: int, nslabs: int) -> list:
     """Node-row bounds of the row-slab partition (slab r owns [b[r], b[r+1]))."""
     out = (C.c_int * (nslabs + 1))()

@@ -81,6 +81,31 @@ def test_slab_nccl_single_rank(oracle):
         comm.close()
 
 
+@pytest.mark.parametrize("nslabs", [1, 3, 8])
+def test_ml_slab_cascade_bit_exact(oracle, nslabs):
+    """Config-5 shape at 512^2 (64 -> 512): replicated coarse levels + slab
+    finest level, fixed sweeps per level: bit-exact against the oracle."""
+    img0, img1 = instances.config5_images(m=512)
+    rhos = instances.ml_sources(img0, img1, 4)
+    eps = [-1.0] * 4
+    rep = w1mg.ml_slab_run(rhos, nslabs=nslabs, eps=eps, max_iters=30)
+    ref = oracle.ml_cp_run(rhos, p=1, eps=eps, max_iters=30)
+    assert np.array_equal(rep.potential.values, ref.phi)
+    assert np.array_equal(rep.flux.x_edges, ref.mx)
+    assert np.array_equal(rep.flux.y_edges, ref.my)
+    assert abs(rep.distance - ref.distance) <= 1e-12 * ref.distance
+    assert [l.iters for l in rep.levels] == [30] * 4
+
+
+def test_ml_slab_cascade_converged(oracle):
+    img0, img1 = instances.config5_images(m=256)
+    rhos = instances.ml_sources(img0, img1, 3)
+    rep = w1mg.ml_slab_run(rhos, nslabs=4, rel_tol=1e-5)
+    ref = oracle.ml_cp_run(rhos, p=1, rel_tol=1e-5)
+    assert abs(rep.distance - ref.distance) <= 1e-4 * ref.distance
+    assert all(abs(a.iters - b) <= 1 for a, b in zip(rep.levels, ref.level_iters))
+
+
 def test_slab_bounds_partition():
     b = w1mg.slab_bounds(4096, 8)
     assert b[0] == 0 and b[-1] == 4097 and len(b) == 9
