@@ -31,7 +31,7 @@ namespace w1mg_dev {
 // control block (identical updates).  With nred == 1 `red` already holds the
 // global sums (NCCL all-reduce result).
 __global__ void slab_finalize_kernel(SweepArgs a, PairCtl* ctl_all, int nslab, const double* red,
-                                     int nred, int parity) {
+                                     int nred, int parity, int* ndone) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     if (ctl_all[0].done) return;
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -43,10 +43,8 @@ __global__ void slab_finalize_kernel(SweepArgs a, PairCtl* ctl_all, int nslab, c
     for (int r = 0; r < nslab; ++r) {
         SweepArgs b = a;
         b.ctl = ctl_all + r;
-        if (r > 0) {
-            b.hist = nullptr;
-            b.ndone = nullptr;
-        }
+        b.ndone = (r == 0) ? ndone : nullptr;  // the host watches one counter
+        if (r > 0) b.hist = nullptr;
         finalize_pair<false>(b, 0, parity, s0, s1, s2);
     }
 }
@@ -223,7 +221,7 @@ void slab_iteration(w1mg_ctx* c, SlabSet& s, int pn, int parity) {
         nred = 1;
     }
     slab_finalize_kernel<<<1, 32, 0, c->stream>>>(s.lv[0].args, s.ctl, (int)s.lv.size(), red, nred,
-                                                 parity);
+                                                 parity, s.ndone);
     CK(cudaGetLastError());
     c->launches += (long)s.lv.size() + 1;
 }

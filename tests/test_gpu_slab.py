@@ -98,9 +98,15 @@ def test_ml_slab_cascade_bit_exact(oracle, nslabs):
 
 
 def test_ml_slab_cascade_converged(oracle):
+    import time
+
     img0, img1 = instances.config5_images(m=256)
     rhos = instances.ml_sources(img0, img1, 3)
+    t = time.perf_counter()
     rep = w1mg.ml_slab_run(rhos, nslabs=4, rel_tol=1e-5)
+    # the host loop must notice the device-side stop (regression: a lost done
+    # counter kept launching early-exit graphs up to the 5e6-sweep cap)
+    assert time.perf_counter() - t < 20.0
     ref = oracle.ml_cp_run(rhos, p=1, rel_tol=1e-5)
     assert abs(rep.distance - ref.distance) <= 1e-4 * ref.distance
     assert all(abs(a.iters - b) <= 1 for a, b in zip(rep.levels, ref.level_iters))
