@@ -25,6 +25,7 @@
 #include "level_kernels.cuh"
 #include "ref_kernels.cuh"
 #include "cp2_kernels.cuh"
+#include "cluster_kernels.cuh"
 
 using namespace w1mg_dev;
 
@@ -328,7 +329,11 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
 // Runs sweeps on every pair of the level until each pair's stop flag is set
 // (device-side, solver_cp.cpp:128-136 semantics).  The host only watches a
 // done-counter one graph behind, so it never stalls the GPU per iteration.
-int g_resident = 1;  // shared-memory-resident engine for small levels (W1MG_RESIDENT=0 off)
+// level-resident engines (W1MG_RESIDENT): 1 = auto (cluster engine for small
+// batches with n <= 128, single-CTA engine for n <= 64 otherwise; default),
+// 2 = single-CTA engine only, 3 = cluster engine wherever it fits (n <= 256),
+// 0 = off (streaming sweeps only)
+int g_resident = 1;
 
 template <int PN>
 void launch_resident_pn(const Level& lv, cudaStream_t s) {
@@ -342,11 +347,74 @@ void launch_resident_pn(const Level& lv, cudaStream_t s) {
 }
 
 bool resident_ok(const Level& lv) {
-    return g_resident && resident_bytes(lv.n) <= kResidentMaxBytes;
+    return (g_resident == 1 || g_resident == 2) && !lv.slab &&
+           resident_bytes(lv.n) <= kResidentMaxBytes;
+}
+
+// Cluster size for the level-resident cluster engine (0: not used).
+// Smallest C whose rows fit the shared-memory budget; with few pairs, grow C
+// (up to 16, >= 8 rows per CTA) to spread one pair over more SMs.  Measured
+// (tools/engines.py): clusters win for n <= 128 when they spread pairs over
+// more SMs (C >= 2); a one-CTA level (big batches, n <= 64) is faster on the
+// single-CTA engine, and n = 256 is faster streaming.  g_resident == 3 forces
+// the cluster engine wherever it fits (tests).
+int cluster_size(const Level& lv, int num_sms) {
+    if (lv.slab || lv.n > 256 || (g_resident != 1 && g_resident != 3)) return 0;
+    int C = 0;
+    for (int q = 1; q <= 16; ++q)
+        if (cluster_smem_bytes(lv.n, q) <= kClusterSmemBudget && (lv.n + 1) / q >= 2) {
+            C = q;
+            break;
+        }
+    if (!C) return 0;
+    while (C * 2 <= 16 && (long)lv.B * C * 2 <= num_sms && (lv.n + 1) / (C * 2) >= 8) C *= 2;
+    if (g_resident == 1 && (C == 1 || lv.n > 128)) return 0;
+    return C;
+}
+
+template <int PN>
+bool launch_cluster_pn(const Level& lv, int C, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(cp_cluster_kernel<PN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(kClusterSmemBudget + 1024)));
+        CK(cudaFuncSetAttribute(cp_cluster_kernel<PN>,
+                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(lv.B * C);
+    cfg.blockDim = dim3(kClusterThreads);
+    cfg.dynamicSmemBytes = cluster_smem_bytes(lv.n, C);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, cp_cluster_kernel<PN>, &cfg) != cudaSuccess ||
+        nclusters < 1) {
+        cudaGetLastError();
+        return false;
+    }
+    CK(cudaLaunchKernelEx(&cfg, cp_cluster_kernel<PN>, lv.args, C));
+    return true;
 }
 
 void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
     if (max_iters <= 0) return;
+    if (const int C = cluster_size(lv, c->num_sms)) {  // whole level in one cluster launch
+        bool ok = (pn == 0)   ? launch_cluster_pn<0>(lv, C, c->stream)
+                  : (pn == 1) ? launch_cluster_pn<1>(lv, C, c->stream)
+                              : launch_cluster_pn<2>(lv, C, c->stream);
+        if (ok) {
+            ++c->launches;
+            return;
+        }
+    }
     if (resident_ok(lv)) {  // whole level in one launch, stop rule on device
         if (pn == 0) launch_resident_pn<0>(lv, c->stream);
         else if (pn == 1) launch_resident_pn<1>(lv, c->stream);
@@ -556,7 +624,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
                               : (std::string(v) == "tma") ? kTma
                               : (std::string(v) == "tma2") ? kTma2
                                                            : kAuto;
-        if (const char* v = std::getenv("W1MG_RESIDENT")) g_resident = std::atoi(v) != 0;
+        if (const char* v = std::getenv("W1MG_RESIDENT")) g_resident = std::atoi(v);
         auto* c = new w1mg_ctx();
         c->device = device;
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -1025,7 +1093,7 @@ int w1mg_set_sweep_engine(int engine) {
 }
 
 int w1mg_set_resident_engine(int on) {
-    g_resident = on ? 1 : 0;
+    g_resident = (on >= 0 && on <= 3) ? on : 1;
     return W1MG_OK;
 }
 

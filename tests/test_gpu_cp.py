@@ -51,13 +51,15 @@ def _random_source(n, seed):
     return instances.make_source(a, b, n)
 
 
-ENGINES = {"resident": (1, 2), "stream-tma2": (0, 2), "stream-tma": (0, 1), "stream-ldg": (0, 0)}
+ENGINES = {"auto": (1, 3), "cluster": (3, 3), "resident-1cta": (2, 3), "stream-tma2": (0, 2),
+           "stream-tma": (0, 1), "stream-ldg": (0, 0)}
 
 
 @pytest.fixture(params=list(ENGINES))
 def engine(request):
-    """Every small-level test runs on all sweep engines: shared-memory
-    resident, two-sweep TMA (temporal blocking), one-sweep TMA, one-sweep LDG."""
+    """Every small-level test runs on all sweep engines: thread-block-cluster
+    level-resident, single-CTA resident, two-sweep TMA (temporal blocking),
+    one-sweep TMA, one-sweep LDG."""
     from paper_1810_00118_b200 import _lib
 
     L = _lib.lib()
@@ -199,6 +201,30 @@ def test_source_field_gate():
         _src(np.ones((n + 1, n + 1)))
     with pytest.raises(ValueError, match="GridSpec: cells_per_side must be positive"):
         w1mg.GridSpec(0)
+
+
+@pytest.mark.parametrize("n", [32, 64, 100, 128, 200, 256])
+def test_cluster_engine_levels_bit_exact(oracle, n):
+    """Cluster engine across its range (C from 1 to 16 CTAs per pair): a
+    batched cascade level with fixed sweeps, every pair bit-exact."""
+    from paper_1810_00118_b200 import _lib
+
+    _lib.lib().w1mg_set_resident_engine(3)  # force the cluster engine
+    B = 5
+    rng = np.random.default_rng(n)
+    img0 = rng.random((B, n, n)) + 0.2
+    img1 = rng.random((B, n, n)) + 0.2
+    dist, _, iters, _ = w1mg.ml_run_batch(img0, img1, 1, eps=[-1.0], max_iters=123)
+    assert (iters == 123).all()
+    for b in (0, B - 1):
+        rho = instances.ml_sources(img0[b], img1[b], 1)[0]
+        ref = oracle.cp_run(rho, p=1, tol=-1.0, max_iters=123)
+        assert _rel(dist[b], ref.distance) <= RED_TOL
+    single = _run(instances.ml_sources(img0[0], img1[0], 1)[0], 1, 123)
+    ref = oracle.cp_run(instances.ml_sources(img0[0], img1[0], 1)[0], p=1, tol=-1.0,
+                        max_iters=123)
+    _assert_fields_equal(single, ref)
+    _lib.lib().w1mg_set_resident_engine(1)
 
 
 @pytest.mark.parametrize("p", [0, 1, 2])
