@@ -70,7 +70,6 @@ cp_cluster_kernel(const SweepArgs a, const int C) {
     const int nr_lo = (c > 0) ? cluster_rows(n, C, c - 1) : 0;
     const double* lo_my = (c > 0) ? cluster.map_shared_rank(my, c - 1) + (nr_lo - 1) * W : nullptr;
     const double* lo_dy = (c > 0) ? cluster.map_shared_rank(ddy, c - 1) + (nr_lo - 1) * W : nullptr;
-    double* red0 = cluster.map_shared_rank(red, 0);
 
     const int T = blockDim.x;
     const int tid = threadIdx.x;
@@ -167,24 +166,27 @@ cp_cluster_kernel(const SweepArgs a, const int C) {
             wred[warp][2] = s_cr;
         }
         __syncthreads();
-        if (tid == 0) {
+        if (tid < C) {
+            // push this CTA's partials into slot c of EVERY CTA (fire-and-forget
+            // DSMEM stores); after the barrier each CTA reads only its own copy
             double t0 = 0.0, t1 = 0.0, t2 = 0.0;
             for (int w = 0; w < T / 32; ++w) {
                 t0 += wred[w][0];
                 t1 += wred[w][1];
                 t2 += wred[w][2];
             }
-            red0[c * 3 + 0] = t0;  // DSMEM store into CTA 0
-            red0[c * 3 + 1] = t1;
-            red0[c * 3 + 2] = t2;
+            double* dst = cluster.map_shared_rank(red, tid);
+            dst[c * 3 + 0] = t0;
+            dst[c * 3 + 1] = t1;
+            dst[c * 3 + 2] = t2;
         }
         cluster.sync();  // phi^{k+1} and all partials visible
-        if (tid == 0) {  // one DSMEM reader per CTA; rank order = identical sums everywhere
+        if (tid == 0) {  // local reads; rank order = identical sums everywhere
             double sdm2 = 0.0, sdp2 = 0.0, scr = 0.0;
             for (int q = 0; q < C; ++q) {
-                sdm2 += red0[q * 3 + 0];
-                sdp2 += red0[q * 3 + 1];
-                scr += red0[q * 3 + 2];
+                sdm2 += red[q * 3 + 0];
+                sdp2 += red[q * 3 + 1];
+                scr += red[q * 3 + 2];
             }
             const double f = a.h2 * (sdm2 / mu + sdp2 / tau - 2.0 * scr);
             if (c == 0 && a.hist && it < a.hist_cap) a.hist[(long)pair * a.hist_cap + it] = f;
