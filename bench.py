@@ -197,12 +197,23 @@ def cpu_cascade_oracle(pair, use_reference=False):
     """One pair through the CPU cascade: the C oracle (port) or the reference
     build (oracle/_ref cp_run per level with Eq. 14/15 warm starts restated in
     the oracle).  Returns (W1, sweeps per level, seconds)."""
-    from oracle import Oracle, Reference
+    return solve_cascade_cpu(pair_sources(pair), use_reference)
+
+
+def pair_sources(pair):
+    """Per-level sources of config-4 pair `pair` (host restriction rule)."""
+    from oracle import Oracle
     from paper_1810_00118_b200 import instances
 
     a, b = instances.config4_pair(pair)
+    return Oracle().ml_sources(a, b, LEVELS)
+
+
+def solve_cascade_cpu(rhos, use_reference=False):
+    """CPU cascade over prepared sources; times only the solve."""
+    from oracle import Oracle, Reference
+
     O = Oracle()
-    rhos = O.ml_sources(a, b, LEVELS)
     t = time.perf_counter()
     if not use_reference:
         r = O.ml_cp_run(rhos, p=1, rel_tol=REL_TOL)
@@ -234,17 +245,19 @@ def run_reference_arm(args):
     use_ref = have_reference()
     per_step = cores
     rates = []
-    first = 0
+    # inputs are prepared once, outside the timed region (as for the GPU arm);
+    # every step re-solves the same pairs, one per core, in parallel threads
+    # (ctypes releases the GIL around the reference's C++ solves)
+    srcs = [pair_sources(i) for i in range(per_step)]
 
     def one(i):
-        return cpu_cascade_oracle(i, use_reference=use_ref)
+        return solve_cascade_cpu(srcs[i], use_reference=use_ref)
 
     with ThreadPoolExecutor(max_workers=cores) as ex:
         for s in range(args.warmup + args.steps):
             t = time.perf_counter()
-            res = list(ex.map(one, range(first, first + per_step)))
+            res = list(ex.map(one, range(per_step)))
             dt = time.perf_counter() - t
-            first += per_step
             if s >= args.warmup:
                 cu = cell_updates([r[1] for r in res])
                 rates.append((cu, dt, per_step))

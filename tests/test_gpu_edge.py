@@ -62,8 +62,8 @@ def test_batch_single_pair_single_level(oracle):
 def test_cascade_divisibility_error():
     rhos = [np.zeros((13, 13)), np.zeros((25, 25))]  # 12 -> 24 is fine
     w1mg.ml_run(rhos, eps=[1.0, 1.0], max_iters=1)
-    with pytest.raises(ValueError, match="divisible"):
-        w1mg.ml_run([np.zeros((4, 4)), np.zeros((7, 7))], eps=[1.0, 1.0], max_iters=1)
+    with pytest.raises(ValueError, match="divisible"):  # 5 cells cannot be halved
+        w1mg.ml_run([np.zeros((3, 3)), np.zeros((6, 6))], eps=[1.0, 1.0], max_iters=1)
 
 
 def test_grid_mismatch_errors():
