@@ -182,6 +182,8 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
         double r_prev = 0.0;
         double uyB = 0.0, dyB = 0.0;  // B's y-flux below the row it processes
 
+        // (unrolling by two removes the row-window copies but raises the
+        //  register count to 126 and costs more in occupancy: measured slower)
         for (int t = 0; t <= j1 - rA0; ++t, o += P) {
             const int rA = rA0 + t;  // A row of this step (rA == n+1: virtual)
             const int rB = rA - 1;   // B row of this step
