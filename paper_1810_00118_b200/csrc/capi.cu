@@ -26,6 +26,7 @@
 #include "ref_kernels.cuh"
 #include "cp2_kernels.cuh"
 #include "cluster_kernels.cuh"
+#include "cp2w_kernels.cuh"
 
 using namespace w1mg_dev;
 
@@ -131,6 +132,8 @@ struct Level {
     dim3 grid;
     SweepArgs args2{};  // two-sweep engine
     dim3 grid2;
+    SweepArgs args2w{};  // two-sweep engine, two column sets per lane
+    dim3 grid2w;
     bool slab = false;  // row slab of a decomposed grid (one-sweep engine only)
 };
 
@@ -196,10 +199,26 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     a2.nsy = (nrows + H2 - 1) / H2;
     a2.ntiles = a2.ncx * a2.nsy;
     lv.grid2 = dim3((a2.ntiles + kSweepWarps - 1) / kSweepWarps, B, 1);
+    // wide two-sweep geometry: 61 owned columns per warp, 4-warp blocks
+    SweepArgs& aw = lv.args2w;
+    aw = a2;
+    aw.ncx = (n + 1 + kOwnW - 1) / kOwnW;
+    int HW = 64;
+    while (HW > 4) {
+        long tiles = (long)B * aw.ncx * ((nrows + HW - 1) / HW);
+        if (tiles >= target / 2) break;
+        HW >>= 1;
+    }
+    aw.H = HW;
+    aw.nsy = (nrows + HW - 1) / HW;
+    aw.ntiles = aw.ncx * aw.nsy;
+    lv.grid2w = dim3((aw.ntiles + kWarpsW - 1) / kWarpsW, B, 1);
     lv.partial = c->get<double>(
-        tag + ".partial", (size_t)B * std::max<size_t>(lv.grid.x * 3, lv.grid2.x * 6));
+        tag + ".partial",
+        (size_t)B * std::max<size_t>({lv.grid.x * 3, lv.grid2.x * 6, lv.grid2w.x * 6}));
     a.partial = lv.partial;
     a2.partial = lv.partial;
+    aw.partial = lv.partial;
     CK(cudaMemsetAsync(lv.ticket, 0, sizeof(unsigned) * B, c->stream));
     return lv;
 }
@@ -277,10 +296,22 @@ int g_sweep_variant = kAuto;
 
 bool two_sweep(const Level& lv) {
     if (lv.slab) return false;  // slabs exchange a one-row halo per sweep
-    return g_sweep_variant == kTma2 || (g_sweep_variant == kAuto && lv.n >= 96);
+    return g_sweep_variant == kTma2 || g_sweep_variant == 4 /* kTma2W */ ||
+           (g_sweep_variant == kAuto && lv.n >= 96);
 }
 
+constexpr int kTma2W = 4;  // two-sweep, two column sets per lane (cp2w_kernels.cuh)
+
 void launch_sweep2(const Level& lv, int pn, int parity, cudaStream_t s) {
+    if (g_sweep_variant == kTma2W) {
+        dim3 blk(kWarpsW * 32);
+        switch (pn) {
+            case 0: cp_sweep2w_tma_kernel<0><<<lv.grid2w, blk, kTmaSmemW, s>>>(lv.args2w, parity); break;
+            case 1: cp_sweep2w_tma_kernel<1><<<lv.grid2w, blk, kTmaSmemW, s>>>(lv.args2w, parity); break;
+            default: cp_sweep2w_tma_kernel<2><<<lv.grid2w, blk, kTmaSmemW, s>>>(lv.args2w, parity); break;
+        }
+        return;
+    }
     dim3 blk(kSweepWarps * 32);
     switch (pn) {
         case 0: cp_sweep2_tma_kernel<0><<<lv.grid2, blk, kTmaSmem, s>>>(lv.args2, parity); break;
@@ -1087,7 +1118,7 @@ int w1mg_interpolate_flux(w1mg_ctx* c, int nc, const double* cx, const double* c
 // Kernel probe: `iters` fused sweeps on B pairs of an n-cell level with the
 // stop rule disabled, after `warm` untimed sweeps; returns ms per sweep.
 int w1mg_set_sweep_engine(int engine) {
-    if (engine < kLdg || engine > kAuto) return W1MG_EINVAL;
+    if (engine < kLdg || engine > kTma2W) return W1MG_EINVAL;
     g_sweep_variant = engine;
     return W1MG_OK;
 }

@@ -30,10 +30,11 @@ constexpr int kOwn2 = 29;  // owned columns per warp in the two-sweep march
 
 // Reduction of both sweeps' residual sums (6 per block) and the two-sweep
 // stop rule; partial holds [pairs][blocks][6].
+template <int NW = kSweepWarps>  // warps per block
 __device__ __forceinline__ void finish_sweep2(const SweepArgs& a, int pair, int parity,
                                               double a0, double a1, double a2, double b0,
                                               double b1, double b2) {
-    __shared__ double red[kSweepWarps][6];
+    __shared__ double red[NW][6];
     __shared__ bool is_last;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -48,7 +49,7 @@ __device__ __forceinline__ void finish_sweep2(const SweepArgs& a, int pair, int 
     double* part = a.partial + (long)pair * nblk * 6;
     if (threadIdx.x == 0) {
         double t[6] = {0, 0, 0, 0, 0, 0};
-        for (int w = 0; w < kSweepWarps; ++w)
+        for (int w = 0; w < NW; ++w)
 #pragma unroll
             for (int q = 0; q < 6; ++q) t[q] += red[w][q];
 #pragma unroll
@@ -75,7 +76,7 @@ __device__ __forceinline__ void finish_sweep2(const SweepArgs& a, int pair, int 
     __syncthreads();
     if (threadIdx.x != 0) return;
     double s[6] = {0, 0, 0, 0, 0, 0};
-    for (int w = 0; w < kSweepWarps; ++w)
+    for (int w = 0; w < NW; ++w)
 #pragma unroll
         for (int q = 0; q < 6; ++q) s[q] += red[w][q];
     PairCtl* ctl = a.ctl + pair;

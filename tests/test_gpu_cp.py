@@ -52,7 +52,7 @@ def _random_source(n, seed):
 
 
 ENGINES = {"auto": (1, 3), "cluster": (3, 3), "resident-1cta": (2, 3), "stream-tma2": (0, 2),
-           "stream-tma": (0, 1), "stream-ldg": (0, 0)}
+           "stream-tma2w": (0, 4), "stream-tma": (0, 1), "stream-ldg": (0, 0)}
 
 
 @pytest.fixture(params=list(ENGINES))
@@ -227,14 +227,22 @@ def test_cluster_engine_levels_bit_exact(oracle, n):
     _lib.lib().w1mg_set_resident_engine(1)
 
 
+@pytest.mark.parametrize("eng", [2, 4])
 @pytest.mark.parametrize("p", [0, 1, 2])
-def test_two_sweep_engine_odd_stop_1024(oracle, p):
-    """Two-sweep launches with an odd sweep cap: the last launch stops after
-    its first sweep and the fix-up replay must reproduce the reference state."""
-    n = 1024
-    rng = np.random.default_rng(1024 + p)
+@pytest.mark.parametrize("n", [300, 1024])
+def test_two_sweep_engine_odd_stop(oracle, n, p, eng):
+    """Two-sweep launches (one or two column sets per lane, interior fast
+    paths included) with an odd sweep cap: the last launch stops after its
+    first sweep and the fix-up replay must reproduce the reference state."""
+    from paper_1810_00118_b200 import _lib
+
+    _lib.lib().w1mg_set_sweep_engine(eng)
+    rng = np.random.default_rng(n + p)
     rho = instances.make_source(rng.random((n + 1, n + 1)), rng.random((n + 1, n + 1)), n)
-    rep = _run(rho, p, 33)
+    try:
+        rep = _run(rho, p, 33)
+    finally:
+        _lib.lib().w1mg_set_sweep_engine(3)
     ref = oracle.cp_run(rho, p=p, tol=-1.0, max_iters=33)
     assert rep.iterations == 33
     _assert_fields_equal(rep, ref)

@@ -35,7 +35,7 @@ if __name__ == "__main__":
         for e in engines:
             ctx.L.w1mg_set_sweep_engine(e)
             r = probe(ctx, n, B)
-            r["engine"] = ["ldg", "tma", "tma2", "auto"][e]
+            r["engine"] = ["ldg", "tma", "tma2", "auto", "tma2w"][e]
             print(json.dumps(r), flush=True)
 
 
