@@ -505,9 +505,11 @@ def main():
                        for n, s_, c_ in zip(level_sizes(), lev_s, lev_cu)],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": measured_traffic(),
-                         "kernel": "w1mg_dev::cp_sweep2_tma_kernel<1> (two fused PD sweeps per "
-                                   "HBM pass, 512^2 level); achieved = algorithmic 8(3V+4E) "
-                                   "bytes per sweep / device time per sweep",
+                         "kernel": "w1mg_dev::cp_sweep2_tmap_kernel<1,4> (two fused PD sweeps "
+                                   "per HBM pass, tensor-map ring, 512^2 level); achieved = "
+                                   "algorithmic one-sweep 8(3V+4E) bytes per sweep / device "
+                                   "time per sweep; traffic = ncu DRAM bytes of one launch "
+                                   "(2 sweeps, 256 pairs x 512^2)",
                          "bytes_per_sweep": alg_bytes_per_sweep(M), "peak_kind": peak_kind},
             "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "cpu_baseline": cpu, "parity_sample": parity,

@@ -252,12 +252,20 @@ int w1mg_ml_slab_cp_run(w1mg_ctx* ctx, w1mg_slab_comm* comm, int nslabs, int n_f
 /* Select the engine of the fused sweep for subsequent launches in this
  * process: 0 = register-pipelined LDG, 1 = one-sweep TMA bulk-copy ring,
  * 2 = two-sweep (temporally blocked) TMA ring, 3 = auto (default: two-sweep
- * for n >= 384, one-sweep below).  Also W1MG_SWEEP=ldg|tma|tma2|auto. */
+ * for n >= 96, one-sweep below), 4 = two-sweep with two column sets per lane.
+ * Also W1MG_SWEEP=ldg|tma|tma2|auto|tma2w.  Results are bit-identical across
+ * engines. */
 int w1mg_set_sweep_engine(int engine);
-/* Levels with n <= 64 run in one launch per level, one CTA per pair, state
- * resident in shared memory (1 = on, default) or through the streaming sweep
- * (0).  Also W1MG_RESIDENT=0|1. */
+/* Level-resident engines (whole level in one launch, state in shared memory):
+ * 1 = auto (default: thread-block-cluster engine for small batches with
+ * n <= 128, one CTA per pair for n <= 64), 2 = one-CTA engine only,
+ * 3 = cluster engine wherever it fits (n <= 256), 0 = off (streaming sweeps
+ * only).  Also W1MG_RESIDENT=0..3. */
 int w1mg_set_resident_engine(int on);
+/* Tail compaction of batched levels (1 = on, default): once at most half of
+ * the pairs still run, sweep grids span only the running pairs.  Also
+ * W1MG_COMPACT=0|1. */
+int w1mg_set_tail_compaction(int on);
 /* Times the fused sweep kernel alone: `iters` sweeps over B pairs of an
  * n-cell level (synthetic source, stop rule off) after `warm` untimed ones;
  * writes the mean milliseconds per sweep launch (CUDA events). */

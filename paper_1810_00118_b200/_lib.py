@@ -131,6 +131,7 @@ def lib():
                                           C.POINTER(LevelStatsC), C.POINTER(CPReport)]
         L.w1mg_set_sweep_engine.argtypes = [C.c_int]
         L.w1mg_set_resident_engine.argtypes = [C.c_int]
+        L.w1mg_set_tail_compaction.argtypes = [C.c_int]
         _lib = L
         return L
 

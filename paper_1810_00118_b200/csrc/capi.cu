@@ -8,6 +8,8 @@
 //   grid operators   proj/src/grid.cpp:45-142
 //   ml_run (spec)
 #include <cublas_v2.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -134,8 +136,82 @@ struct Level {
     dim3 grid2;
     SweepArgs args2w{};  // two-sweep engine, two column sets per lane
     dim3 grid2w;
+    dim3 grid2t;  // two-sweep tensor-map engine (args2 geometry, kWarpsT-warp blocks)
     bool slab = false;  // row slab of a decomposed grid (one-sweep engine only)
+    int* act = nullptr;   // [B] running pairs of a compacted launch (null: B == 1 or slab)
+    int* nact = nullptr;  // their count
+    alignas(64) CUtensorMap tmap{};  // (column, row, plane) view for the tensor-map engine
+    bool has_tmap = false;
 };
+
+// Tensor map over a whole-grid level: x = column (pitch), y = row (n+1 rows,
+// rows beyond are zero-filled), z = pair * NSLOT + slot; box {kChunk, 1, 8} at
+// plane stride 2 = one row of PHI_p, MX_p, MY_p, RHO_p for parity p.
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            fail(W1MG_ECUDA, "cuTensorMapEncodeTiled not available");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+void make_level_tmap(Level& lv) {
+    const Layout& L = lv.L;
+    cuuint64_t dims[3] = {(cuuint64_t)L.pitch, (cuuint64_t)L.n + 1, (cuuint64_t)lv.B * NSLOT};
+    cuuint64_t strides[2] = {(cuuint64_t)L.pitch * 8, (cuuint64_t)L.plane * 8};
+    cuuint32_t box[3] = {(cuuint32_t)kChunk, 1, 8};
+    cuuint32_t estr[3] = {1, 1, 2};
+    CUresult r = tmap_encoder()(&lv.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                                lv.base + L.at(0, 0), dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(W1MG_ECUDA, "cuTensorMapEncodeTiled failed");
+    lv.has_tmap = true;
+}
+
+// RHO -> RHO2 for every pair of the level (one strided copy).
+void mirror_rho(w1mg_ctx* c, const Level& lv) {
+    const size_t w = (size_t)lv.L.plane * 8, sp = (size_t)NSLOT * lv.L.plane * 8;
+    CK(cudaMemcpy2DAsync(lv.base + RHO2 * lv.L.plane, sp, lv.base + RHO * lv.L.plane, sp, w, lv.B,
+                         cudaMemcpyDeviceToDevice, c->stream));
+}
+
+// warps per block of the tensor-map two-sweep kernel (W1MG_TMAP_NW = 2|4|8)
+int g_tmap_nw = kWarpsT;
+
+// Strip geometry of the three streaming engines for a launch over `pairs`
+// pairs: the tallest strips (<= 64 rows) that still give about 32 warps per
+// SM overall, so a grid over few pairs splits each pair finer.
+void strip_geometry(SweepArgs& a, int own, long pairs, long target, int hmin) {
+    const int nrows = a.jhi - a.jlo;
+    a.ncx = (a.L.n + 1 + own - 1) / own;
+    int H = 64;
+    while (H > hmin) {
+        long tiles = pairs * a.ncx * ((nrows + H - 1) / H);
+        if (tiles >= target) break;
+        H >>= 1;
+    }
+    a.H = H;
+    a.nsy = (nrows + H - 1) / H;
+    a.ntiles = a.ncx * a.nsy;
+}
+
+void set_geometry(Level& lv, int pairs, int num_sms) {
+    const long target = (long)num_sms * 32;
+    strip_geometry(lv.args, kOwn, pairs, target, 2);       // 31 owned columns per warp
+    strip_geometry(lv.args2, kOwn2, pairs, target, 4);     // two-sweep: 29 per warp
+    strip_geometry(lv.args2w, kOwnW, pairs, target / 2, 4);  // wide: 61 per warp, 4-warp blocks
+    lv.grid = dim3((lv.args.ntiles + kSweepWarps - 1) / kSweepWarps, pairs, 1);
+    lv.grid2 = dim3((lv.args2.ntiles + kSweepWarps - 1) / kSweepWarps, pairs, 1);
+    lv.grid2w = dim3((lv.args2w.ntiles + kWarpsW - 1) / kWarpsW, pairs, 1);
+    lv.grid2t = dim3((lv.args2.ntiles + g_tmap_nw - 1) / g_tmap_nw, pairs, 1);
+}
 
 // jhi < 0: whole grid.  Otherwise a row slab owning global rows [jlo, jhi),
 // stored with one halo row below and two above (Layout::make_slab).
@@ -149,7 +225,6 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
         jlo = 0;
         jhi = n + 1;
     }
-    const int nrows = jhi - jlo;
     lv.L = lv.slab ? Layout::make_slab(n, jlo - 1, jhi + 2) : Layout::make(n);
     lv.base = c->get<double>(tag + ".base", (size_t)B * NSLOT * lv.L.plane);
     lv.ctl = c->get<PairCtl>(tag + ".ctl", B);
@@ -159,21 +234,9 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     SweepArgs& a = lv.args;
     a.base = lv.base;
     a.L = lv.L;
-    a.ncx = (n + 1 + kOwn - 1) / kOwn;
-    // strip height: the tallest that still gives >= 32 warps per SM overall
-    const long target = (long)c->num_sms * 32;
-    int H = 64;
-    while (H > 2) {
-        long tiles = (long)B * a.ncx * ((nrows + H - 1) / H);
-        if (tiles >= target) break;
-        H >>= 1;
-    }
-    a.H = H;
     a.jlo = jlo;
     a.jhi = jhi;
     a.red_out = nullptr;
-    a.nsy = (nrows + H - 1) / H;
-    a.ntiles = a.ncx * a.nsy;
     a.mu = mu;
     a.tau = tau;
     const double h = 1.0 / n;
@@ -184,41 +247,28 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     a.hist = hist;
     a.hist_cap = hist_cap;
     a.ndone = lv.ndone;
-    lv.grid = dim3((a.ntiles + kSweepWarps - 1) / kSweepWarps, B, 1);
-    // two-sweep geometry: 29 owned columns per warp
-    SweepArgs& a2 = lv.args2;
-    a2 = a;
-    a2.ncx = (n + 1 + kOwn2 - 1) / kOwn2;
-    int H2 = 64;
-    while (H2 > 4) {
-        long tiles = (long)B * a2.ncx * ((nrows + H2 - 1) / H2);
-        if (tiles >= target) break;
-        H2 >>= 1;
-    }
-    a2.H = H2;
-    a2.nsy = (nrows + H2 - 1) / H2;
-    a2.ntiles = a2.ncx * a2.nsy;
-    lv.grid2 = dim3((a2.ntiles + kSweepWarps - 1) / kSweepWarps, B, 1);
-    // wide two-sweep geometry: 61 owned columns per warp, 4-warp blocks
-    SweepArgs& aw = lv.args2w;
-    aw = a2;
-    aw.ncx = (n + 1 + kOwnW - 1) / kOwnW;
-    int HW = 64;
-    while (HW > 4) {
-        long tiles = (long)B * aw.ncx * ((nrows + HW - 1) / HW);
-        if (tiles >= target / 2) break;
-        HW >>= 1;
-    }
-    aw.H = HW;
-    aw.nsy = (nrows + HW - 1) / HW;
-    aw.ntiles = aw.ncx * aw.nsy;
-    lv.grid2w = dim3((aw.ntiles + kWarpsW - 1) / kWarpsW, B, 1);
+    a.act = nullptr;
+    a.nact = nullptr;
+    lv.args2 = a;
+    lv.args2w = a;
+    set_geometry(lv, B, c->num_sms);
+    // a compacted launch over fewer pairs uses shorter strips (more tiles per
+    // pair), so size the partials for the one-pair geometry
+    Level one = lv;
+    set_geometry(one, 1, c->num_sms);
     lv.partial = c->get<double>(
         tag + ".partial",
-        (size_t)B * std::max<size_t>({lv.grid.x * 3, lv.grid2.x * 6, lv.grid2w.x * 6}));
+        (size_t)B * std::max<size_t>({(size_t)one.args.ntiles * 3, (size_t)one.args2.ntiles * 6,
+                                      (size_t)one.args2w.ntiles * 6, (size_t)lv.args.ntiles * 3,
+                                      (size_t)lv.args2.ntiles * 6, (size_t)lv.args2w.ntiles * 6}));
     a.partial = lv.partial;
-    a2.partial = lv.partial;
-    aw.partial = lv.partial;
+    lv.args2.partial = lv.partial;
+    lv.args2w.partial = lv.partial;
+    if (B > 1 && !lv.slab) {
+        lv.act = c->get<int>(tag + ".act", B);
+        lv.nact = c->get<int>(tag + ".nact", 1);
+    }
+    if (!lv.slab) make_level_tmap(lv);
     CK(cudaMemsetAsync(lv.ticket, 0, sizeof(unsigned) * B, c->stream));
     return lv;
 }
@@ -291,18 +341,43 @@ void reduce_pairs(w1mg_ctx* c, F f, int w, int rows, int B, double s1, double s2
 // sweeps per HBM pass, falling back to the single-sweep TMA kernel for the
 // short loops and the stop fix-up
 constexpr int kTma2 = 2;
-constexpr int kAuto = 3;  // two-sweep TMA for n >= 96 (faster from 128 up, measured), one-sweep below
+// auto: two-sweep for n >= 96 (faster from 128 up, measured), one-sweep below;
+// the two-sweep launches use the tensor-map ring with 4-warp blocks (measured
+// 3-14 % faster than the bulk-copy ring for batched 128..512 levels,
+// tools/probe.py; profiles/r1_summary.md)
+constexpr int kAuto = 3;
 int g_sweep_variant = kAuto;
+
+constexpr int kTma2W = 4;  // two-sweep, two column sets per lane (cp2w_kernels.cuh)
+constexpr int kTma2T = 5;  // two-sweep, ring fed by one tensor-map box per row
+
+template <int NW>
+void launch_tmap(const Level& lv, int pn, int parity, cudaStream_t s) {
+    const dim3 blk(NW * 32);
+    const int sm = tmap_smem(NW);
+    switch (pn) {
+        case 0: cp_sweep2_tmap_kernel<0, NW><<<lv.grid2t, blk, sm, s>>>(lv.args2, parity, lv.tmap); break;
+        case 1: cp_sweep2_tmap_kernel<1, NW><<<lv.grid2t, blk, sm, s>>>(lv.args2, parity, lv.tmap); break;
+        default: cp_sweep2_tmap_kernel<2, NW><<<lv.grid2t, blk, sm, s>>>(lv.args2, parity, lv.tmap); break;
+    }
+}
 
 bool two_sweep(const Level& lv) {
     if (lv.slab) return false;  // slabs exchange a one-row halo per sweep
-    return g_sweep_variant == kTma2 || g_sweep_variant == 4 /* kTma2W */ ||
+    return g_sweep_variant == kTma2 || g_sweep_variant == kTma2W || g_sweep_variant == kTma2T ||
            (g_sweep_variant == kAuto && lv.n >= 96);
 }
 
-constexpr int kTma2W = 4;  // two-sweep, two column sets per lane (cp2w_kernels.cuh)
-
 void launch_sweep2(const Level& lv, int pn, int parity, cudaStream_t s) {
+    if (g_sweep_variant == kTma2T || g_sweep_variant == kAuto) {
+        if (!lv.has_tmap) fail(W1MG_ELOGIC, "tensor-map sweep on a level without a map");
+        switch (g_tmap_nw) {
+            case 2: launch_tmap<2>(lv, pn, parity, s); break;
+            case 8: launch_tmap<8>(lv, pn, parity, s); break;
+            default: launch_tmap<4>(lv, pn, parity, s); break;
+        }
+        return;
+    }
     if (g_sweep_variant == kTma2W) {
         dim3 blk(kWarpsW * 32);
         switch (pn) {
@@ -337,14 +412,22 @@ void launch_sweep(const Level& lv, int pn, int parity, cudaStream_t s) {
     }
 }
 
+// Graph of K sweep launches.  A compacted level (lv.args.act set: the tail of
+// a batch, grid over lv.grid.y <= B pairs) first rebuilds the running-pair
+// list on device, so the launches only span pairs that can still run.
 cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
     std::string key(reinterpret_cast<const char*>(&lv.args), sizeof(SweepArgs));
     key += std::to_string(pn) + ":" + std::to_string(K) + ":" + std::to_string(lv.grid.x) + ":" +
-           std::to_string(lv.grid.y) + ":v" + std::to_string(g_sweep_variant);
+           std::to_string(lv.grid.y) + ":" + std::to_string(lv.grid2.x) + ":" +
+           std::to_string(lv.grid2w.x) + ":" + std::to_string(lv.grid2t.x) + ":B" +
+           std::to_string(lv.B) + ":v" +
+           std::to_string(g_sweep_variant);
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) return it->second;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    if (lv.args.act)
+        compact_active_kernel<<<1, kCompactThreads, 0, c->stream>>>(lv.ctl, lv.B, lv.act, lv.nact);
     for (int k = 0; k < K; ++k) {
         if (two_sweep(lv)) launch_sweep2(lv, pn, k & 1, c->stream);
         else launch_sweep(lv, pn, k & 1, c->stream);
@@ -355,6 +438,23 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
     CK(cudaGraphDestroy(g));
     c->graphs[key] = ex;
     return ex;
+}
+
+// Tail compaction (W1MG_COMPACT, default on): once at most half of a batch
+// is still running, launch grids span only a power-of-two bucket >= the
+// running count, with strips re-split for that many pairs.  Pair results do
+// not depend on the launch geometry (each pair's sweep and residual order are
+// fixed), so this only removes the early-exit blocks of stopped pairs.
+bool g_compact = true;
+
+Level compacted(const Level& lv, int pairs, int num_sms) {
+    Level b = lv;
+    set_geometry(b, pairs, num_sms);
+    for (SweepArgs* a : {&b.args, &b.args2, &b.args2w}) {
+        a->act = lv.act;
+        a->nact = lv.nact;
+    }
+    return b;
 }
 
 // Runs sweeps on every pair of the level until each pair's stop flag is set
@@ -437,6 +537,7 @@ bool launch_cluster_pn(const Level& lv, int C, cudaStream_t s) {
 
 void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
     if (max_iters <= 0) return;
+    if (lv.has_tmap) mirror_rho(c, lv);
     if (const int C = cluster_size(lv, c->num_sms)) {  // whole level in one cluster launch
         bool ok = (pn == 0)   ? launch_cluster_pn<0>(lv, C, c->stream)
                   : (pn == 1) ? launch_cluster_pn<1>(lv, C, c->stream)
@@ -464,16 +565,27 @@ void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
     cudaGraphExec_t ex = sweep_graph(c, lv, pn, K);
     const long per_launch = two_sweep(lv) ? 2 : 1;
     long launched = 0;
+    int span = lv.B;  // pairs the current graph's grids cover
     for (long g = 0;; ++g) {
         CK(cudaGraphLaunch(ex, c->stream));
         launched += K * per_launch;
-        c->launches += K;
+        c->launches += K + (span < lv.B ? 1 : 0);
         CK(cudaMemcpyAsync(c->pinned + (g & 1), lv.ndone, sizeof(int), cudaMemcpyDeviceToHost,
                            c->stream));
         CK(cudaEventRecord(c->ev[g & 1], c->stream));
         if (g > 0) {
             CK(cudaEventSynchronize(c->ev[(g - 1) & 1]));
-            if (c->pinned[(g - 1) & 1] >= lv.B) break;
+            const int done = c->pinned[(g - 1) & 1];
+            if (done >= lv.B) break;
+            // pairs never restart, so B - done bounds the running count of
+            // every later graph
+            const int running = lv.B - done;
+            if (g_compact && lv.act && 2 * running <= span) {
+                int b = 1;
+                while (b < running) b <<= 1;
+                span = b;
+                ex = sweep_graph(c, compacted(lv, span, c->num_sms), pn, K);
+            }
         }
         if (launched >= max_iters + K * per_launch) break;  // every pair hit its cap by now
     }
@@ -654,8 +766,15 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
             g_sweep_variant = (std::string(v) == "ldg") ? kLdg
                               : (std::string(v) == "tma") ? kTma
                               : (std::string(v) == "tma2") ? kTma2
-                                                           : kAuto;
+                              : (std::string(v) == "tma2w") ? kTma2W
+                              : (std::string(v) == "tma2t") ? kTma2T
+                                                            : kAuto;
         if (const char* v = std::getenv("W1MG_RESIDENT")) g_resident = std::atoi(v);
+        if (const char* v = std::getenv("W1MG_COMPACT")) g_compact = std::atoi(v) != 0;
+        if (const char* v = std::getenv("W1MG_TMAP_NW")) {
+            const int w = std::atoi(v);
+            g_tmap_nw = (w == 2 || w == 8) ? w : kWarpsT;
+        }
         auto* c = new w1mg_ctx();
         c->device = device;
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -1118,13 +1237,18 @@ int w1mg_interpolate_flux(w1mg_ctx* c, int nc, const double* cx, const double* c
 // Kernel probe: `iters` fused sweeps on B pairs of an n-cell level with the
 // stop rule disabled, after `warm` untimed sweeps; returns ms per sweep.
 int w1mg_set_sweep_engine(int engine) {
-    if (engine < kLdg || engine > kTma2W) return W1MG_EINVAL;
+    if (engine < kLdg || engine > kTma2T) return W1MG_EINVAL;
     g_sweep_variant = engine;
     return W1MG_OK;
 }
 
 int w1mg_set_resident_engine(int on) {
     g_resident = (on >= 0 && on <= 3) ? on : 1;
+    return W1MG_OK;
+}
+
+int w1mg_set_tail_compaction(int on) {
+    g_compact = on != 0;
     return W1MG_OK;
 }
 
@@ -1140,6 +1264,7 @@ int w1mg_sweep_probe(w1mg_ctx* c, int n, int B, int pnorm, long warm, long iters
         probe_fill_kernel<<<node_grid(n, B, blk), blk, 0, c->stream>>>(lv.base, lv.L);
         ++c->launches;
         CK(cudaGetLastError());
+        mirror_rho(c, lv);
         init_level_ctl(c, lv, 0.0, -1.0, 2 * (warm + iters) + 64);
         // kTma2: each launch is two sweeps; iters counts sweeps
         const int per = two_sweep(lv) ? 2 : 1;

@@ -22,6 +22,8 @@
 // it, reproducing the reference's first-k stop exactly.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (type only; encoded through the runtime entry point)
+
 #include "cp_kernels.cuh"
 
 namespace w1mg_dev {
@@ -110,11 +112,16 @@ __device__ __forceinline__ void finish_sweep2(const SweepArgs& a, int pair, int 
 // The two-sweep march of one warp over its tile.  kInt: the tile's 32 columns
 // and all rows it touches lie strictly inside the grid (no absent edges, no
 // boundary rows), so every mask folds to a constant.
-template <int PN, bool kInt>
+//
+// kTM: the ring is fed by one strided 3-D tensor-map box per row (planes
+// PHI_p, MX_p, MY_p, RHO_p of the same row; box q = row rA0 + q) instead of
+// four bulk copies (phi one row ahead).  Step t then reads m, rho from box t
+// and phi^k(row+1) from box t+1.
+template <int PN, bool kInt, bool kTM = false>
 __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity, int cx, int j0,
                                        int j1, int lane, double* ring, uint64_t* bars,
                                        double& a_dm2, double& a_dp2, double& a_cr, double& b_dm2,
-                                       double& b_dp2, double& b_cr) {
+                                       double& b_dp2, double& b_cr, const void* tm = nullptr) {
     {
         const Layout L = a.L;
         const int n = L.n;
@@ -134,8 +141,9 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
         const double mu = a.mu, tau = a.tau, ih = a.ih;
 
         const int ilo = cx * kOwn2 - 2;  // column of lane 0 (warp-uniform)
-        const int a0 = ilo & ~1;
+        const int a0 = ilo & ~1;  // 16-B aligned box / chunk start (TMA requirement)
         const int sh = ilo - a0;
+        const int zb = pair * NSLOT + PHI0 + parity;  // box planes zb, zb+2, zb+4, zb+6
         const long c0 = L.at(a0, 0);
         if (lane == 0) {
 #pragma unroll
@@ -145,19 +153,24 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
         __syncwarp();
         auto issue = [&](int st, int row) {
             double* dst = ring + st * kStreams * kChunk;
-            const long orow = c0 + (long)row * P;
             mbar_expect_tx(&bars[st], kStageBytes);
-            bulk_g2s(dst + 0 * kChunk, phr + orow + P, kChunk * 8, &bars[st]);
-            bulk_g2s(dst + 1 * kChunk, mxr + orow, kChunk * 8, &bars[st]);
-            bulk_g2s(dst + 2 * kChunk, myr + orow, kChunk * 8, &bars[st]);
-            bulk_g2s(dst + 3 * kChunk, rho + orow, kChunk * 8, &bars[st]);
+            if constexpr (kTM) {
+                tmap_g2s_3d(dst, tm, a0, row, zb, &bars[st]);
+            } else {
+                const long orow = c0 + (long)row * P;
+                bulk_g2s(dst + 0 * kChunk, phr + orow + P, kChunk * 8, &bars[st]);
+                bulk_g2s(dst + 1 * kChunk, mxr + orow, kChunk * 8, &bars[st]);
+                bulk_g2s(dst + 2 * kChunk, myr + orow, kChunk * 8, &bars[st]);
+                bulk_g2s(dst + 3 * kChunk, rho + orow, kChunk * 8, &bars[st]);
+            }
         };
         // A rows rA0 .. rA1 (inclusive); B rows rA0-1 .. j1-1
         const int rA0 = max(j0 - 1, 0);
         const int rA1 = min(j1, n);
         const int nA = rA1 - rA0 + 1;
+        const int nbox = kTM ? nA + 1 : nA;  // kTM: rows rA0 .. rA1+1
         if (lane == 0) {
-            for (int t = 0; t < kStages && t < nA; ++t) issue(t, rA0 + t);
+            for (int t = 0; t < kStages && t < nbox; ++t) issue(t, rA0 + t);
         }
 
         // A's y-flux below row rA0 (m-only warm-up, direct loads)
@@ -175,8 +188,15 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
             dyA = dy;
         }
         long o = L.at(i, rA0);
-        double pc = in ? __ldg(phr + o) : 0.0;  // phi^k(i, r)
-        double pr = hx ? __ldg(phr + o + 1) : 0.0;  // phi^k(i+1, r)
+        double pc, pr;  // phi^k(i, r), phi^k(i+1, r)
+        if constexpr (kTM) {
+            mbar_wait(&bars[0], 0u);
+            pc = in ? ring[sh + lane] : 0.0;
+            pr = hx ? ring[sh + lane + 1] : 0.0;
+        } else {
+            pc = in ? __ldg(phr + o) : 0.0;
+            pr = hx ? __ldg(phr + o + 1) : 0.0;
+        }
 
         // B state: A's outputs of the previous row, rho of the previous row
         double fA_prev = 0.0, mxA_prev = 0.0, myA_prev = 0.0;
@@ -192,16 +212,23 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
             double pu = 0.0, pur = 0.0;
             if (kInt || rA <= rA1) {
                 const int st = t % kStages;
-                mbar_wait(&bars[st], (uint32_t)((t / kStages) & 1));
                 const double* c = ring + st * kStreams * kChunk + sh + lane;
+                const double* cph = c;  // phi^k(row rA+1)
+                if constexpr (kTM) {
+                    const int su = (t + 1) % kStages;
+                    mbar_wait(&bars[su], (uint32_t)(((t + 1) / kStages) & 1));
+                    cph = ring + su * kStreams * kChunk + sh + lane;
+                } else {
+                    mbar_wait(&bars[st], (uint32_t)((t / kStages) & 1));
+                }
                 const bool hy = kInt || (in && (rA < n));
-                pu = hy ? c[0] : 0.0;
-                pur = (kInt || (hx && rA < n)) ? c[1] : 0.0;
+                pu = hy ? cph[0] : 0.0;
+                pur = (kInt || (hx && rA < n)) ? cph[1] : 0.0;
                 const double mxo = hx ? c[kChunk] : 0.0;
                 const double myo = hy ? c[2 * kChunk] : 0.0;
                 r = in ? c[3 * kChunk] : 0.0;
                 __syncwarp();
-                if (lane == 0 && t + kStages < nA) {
+                if (lane == 0 && t + kStages < nbox) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     issue(st, rA + kStages);
                 }
@@ -260,8 +287,8 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
 template <int PN>
 __global__ void __launch_bounds__(kSweepWarps * 32, 2)
 cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
-    const int pair = blockIdx.y;
-    if (*(volatile int*)&a.ctl[pair].done) return;
+    const int pair = sweep_pair(a);
+    if (pair < 0 || *(volatile int*)&a.ctl[pair].done) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
@@ -289,6 +316,45 @@ cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
                               b_dm2, b_dp2, b_cr);
     }
     finish_sweep2(a, pair, parity, a_dm2, a_dp2, a_cr, b_dm2, b_dp2, b_cr);
+}
+
+// Same march, ring fed by one tensor-map box per row.  `tm` views the level
+// buffer as (column, row, plane) with plane = pair * NSLOT + slot, box
+// {kChunk, 1, 8} at plane stride 2 (capi.cu: make_level_tmap).  NW warps per
+// block: small blocks let an SM refill as soon as a few strips finish.
+constexpr int kWarpsT = 4;
+constexpr int tmap_smem(int nw) { return nw * (kStages * kStageBytes + kStages * 8); }
+
+template <int PN, int NW>
+__global__ void __launch_bounds__(NW * 32, 24 / NW)
+cp_sweep2_tmap_kernel(const SweepArgs a, const int parity, const __grid_constant__ CUtensorMap tm) {
+    const int pair = sweep_pair(a);
+    if (pair < 0 || *(volatile int*)&a.ctl[pair].done) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    const int tile = blockIdx.x * NW + warp;
+    double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * kStages * kStreams * kChunk;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + NW * kStages * kStageBytes) +
+                     warp * kStages;
+    double a_dm2 = 0.0, a_dp2 = 0.0, a_cr = 0.0;
+    double b_dm2 = 0.0, b_dp2 = 0.0, b_cr = 0.0;
+    if (tile < a.ntiles) {
+        const int cx = tile % a.ncx;
+        const int sy = tile / a.ncx;
+        const int j0 = a.jlo + sy * a.H;
+        const int j1 = min(j0 + a.H, a.jhi);
+        const int ilo = cx * kOwn2 - 2;
+        const int n = a.L.n;
+        const bool interior = (ilo >= 0) && (ilo + 31 < n) && (j0 >= 2) && (j1 < n);
+        if (interior)
+            march2<PN, true, true>(a, pair, parity, cx, j0, j1, lane, ring, bars, a_dm2, a_dp2,
+                                   a_cr, b_dm2, b_dp2, b_cr, &tm);
+        else
+            march2<PN, false, true>(a, pair, parity, cx, j0, j1, lane, ring, bars, a_dm2, a_dp2,
+                                    a_cr, b_dm2, b_dp2, b_cr, &tm);
+    }
+    finish_sweep2<NW>(a, pair, parity, a_dm2, a_dp2, a_cr, b_dm2, b_dp2, b_cr);
 }
 
 }  // namespace w1mg_dev

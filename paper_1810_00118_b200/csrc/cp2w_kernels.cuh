@@ -212,8 +212,8 @@ __device__ __forceinline__ void march2w(const SweepArgs& a, int pair, int parity
 template <int PN>
 __global__ void __launch_bounds__(kWarpsW * 32, 3)
 cp_sweep2w_tma_kernel(const SweepArgs a, const int parity) {
-    const int pair = blockIdx.y;
-    if (*(volatile int*)&a.ctl[pair].done) return;
+    const int pair = sweep_pair(a);
+    if (pair < 0 || *(volatile int*)&a.ctl[pair].done) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);

@@ -74,7 +74,16 @@ struct SweepArgs {
     double* hist;       // [pairs][hist_cap] (may be null)
     long hist_cap;
     int* ndone;         // number of stopped pairs
+    const int* act;     // compacted launch: blockIdx.y indexes act[0, *nact) (null: pair = blockIdx.y)
+    const int* nact;
 };
+
+// Pair of this block.  In a compacted launch (the tail of a batched level, see
+// run_sweeps) the grid only spans the pairs still running; -1 = no work.
+__device__ __forceinline__ int sweep_pair(const SweepArgs& a) {
+    if (!a.act) return blockIdx.y;
+    return (int)blockIdx.y < *a.nact ? a.act[blockIdx.y] : -1;
+}
 
 constexpr int kSweepWarps = 8;  // warps per block
 constexpr int kOwn = 31;        // owned columns per warp
@@ -295,9 +304,9 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
 template <int PN>
 __global__ void __launch_bounds__(kSweepWarps * 32)
 cp_sweep_kernel(const SweepArgs a, const int parity_arg) {
-    const int pair = blockIdx.y;
+    const int pair = sweep_pair(a);
     int parity;
-    if (!sweep_gate(a.ctl + pair, parity_arg, parity)) return;
+    if (pair < 0 || !sweep_gate(a.ctl + pair, parity_arg, parity)) return;
     const int lane = threadIdx.x & 31;
     const int tile = blockIdx.x * kSweepWarps + (threadIdx.x >> 5);
     double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
@@ -375,12 +384,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// One 3-D tensor-map box (TMA tiled mode) into shared memory: coordinates
+// (column, row, plane) of the box origin; completes on `bar` like bulk_g2s.
+__device__ __forceinline__ void tmap_g2s_3d(void* dst, const void* tmap, int x, int y, int z,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];"
+        ::"r"(smem_u32(dst)), "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
 template <int PN>
 __global__ void __launch_bounds__(kSweepWarps * 32, 3)
 cp_sweep_tma_kernel(const SweepArgs a, const int parity_arg) {
-    const int pair = blockIdx.y;
+    const int pair = sweep_pair(a);
     int parity;
-    if (!sweep_gate(a.ctl + pair, parity_arg, parity)) return;
+    if (pair < 0 || !sweep_gate(a.ctl + pair, parity_arg, parity)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     // warp index broadcast from lane 0: the compiler then keeps every TMA

@@ -231,6 +231,41 @@ __global__ void init_ctl_kernel(PairCtl* ctl, int npairs, const double* __restri
     ctl[b] = c;
 }
 
+// Active-pair list for a compacted sweep launch: act = running pairs in
+// ascending order, *nact = their count.  One block; each thread scans a
+// contiguous run of pairs, then a block-wide exclusive scan places the runs.
+constexpr int kCompactThreads = 1024;
+__global__ void __launch_bounds__(kCompactThreads)
+compact_active_kernel(const PairCtl* __restrict__ ctl, int npairs, int* __restrict__ act,
+                      int* __restrict__ nact) {
+    __shared__ int wsum[kCompactThreads / 32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int per = (npairs + kCompactThreads - 1) / kCompactThreads;
+    const int lo = min(t * per, npairs), hi = min(lo + per, npairs);
+    int cnt = 0;
+    for (int b = lo; b < hi; ++b) cnt += ctl[b].done ? 0 : 1;
+    int incl = cnt;  // warp inclusive scan
+    for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += v;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        int s = wsum[lane];
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, s, d);
+            if (lane >= d) s += v;
+        }
+        wsum[lane] = s;  // inclusive over warps
+    }
+    __syncthreads();
+    int pos = incl - cnt + (w > 0 ? wsum[w - 1] : 0);
+    for (int b = lo; b < hi; ++b)
+        if (!ctl[b].done) act[pos++] = b;
+    if (t == kCompactThreads - 1) *nact = pos;
+}
+
 // per-level bookkeeping into caller-visible arrays
 __global__ void harvest_kernel(const PairCtl* __restrict__ ctl, int npairs, int level, int levels,
                                long* iters, double* fpr, double* tol) {

@@ -52,7 +52,8 @@ def _random_source(n, seed):
 
 
 ENGINES = {"auto": (1, 3), "cluster": (3, 3), "resident-1cta": (2, 3), "stream-tma2": (0, 2),
-           "stream-tma2w": (0, 4), "stream-tma": (0, 1), "stream-ldg": (0, 0)}
+           "stream-tma2w": (0, 4), "stream-tma2t": (0, 5), "stream-tma": (0, 1),
+           "stream-ldg": (0, 0)}
 
 
 @pytest.fixture(params=list(ENGINES))
@@ -227,7 +228,7 @@ def test_cluster_engine_levels_bit_exact(oracle, n):
     _lib.lib().w1mg_set_resident_engine(1)
 
 
-@pytest.mark.parametrize("eng", [2, 4])
+@pytest.mark.parametrize("eng", [2, 4, 5])
 @pytest.mark.parametrize("p", [0, 1, 2])
 @pytest.mark.parametrize("n", [300, 1024])
 def test_two_sweep_engine_odd_stop(oracle, n, p, eng):

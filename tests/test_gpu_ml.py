@@ -63,6 +63,32 @@ def test_batch_matches_single_pair(oracle):
         assert all(abs(int(a) - c) <= 1 for a, c in zip(iters[b], ref.level_iters))
 
 
+def test_tail_compaction_same_results(oracle):
+    """Tail compaction (grids over running pairs only) on the streaming
+    levels must not change any pair's result: same W1 and sweep counts as
+    with compaction off, and pair 0 against the oracle."""
+    from paper_1810_00118_b200 import _lib
+
+    L = _lib.lib()
+    img0s, img1s = instances.config4_pairs(0, 24, m=256)
+    runs = []
+    for on in (0, 1):
+        L.w1mg_set_tail_compaction(on)
+        try:
+            runs.append(w1mg.ml_run_batch(img0s, img1s, 4, p=w1mg.PNorm.p2, rel_tol=1e-5))
+        finally:
+            L.w1mg_set_tail_compaction(1)
+    (d0, _, it0, c0), (d1, _, it1, c1) = runs
+    assert c0.all() and c1.all()
+    fin = it1[:, -1]
+    assert np.median(fin) < fin.max()  # the finest level had a tail to compact
+    assert np.abs(it0 - it1).max() <= 1
+    np.testing.assert_allclose(d1, d0, rtol=1e-12, atol=0)
+    ref = oracle.ml_cp_run(instances.ml_sources(img0s[0], img1s[0], 4), p=1, rel_tol=1e-5)
+    assert abs(d1[0] - ref.distance) <= 1e-4 * ref.distance
+    assert all(abs(int(a) - c) <= 1 for a, c in zip(it1[0], ref.level_iters))
+
+
 def test_config5_full_size_fixed_iterations(oracle):
     """BASELINE.json configs[4] at full size: two 20-component anisotropic
     mixtures on 4096^2, 7 levels 64 -> 4096.  The oracle cannot converge a
