@@ -6,6 +6,10 @@ the hot path.
       --out report.json --export-flux flux.csv --export-potential phi.csv
   python -m paper_1810_00118_b200.cli gen --kind two_blobs --n 64 --seed 1 --out-a a.pgm --out-b b.pgm
   python -m paper_1810_00118_b200.cli oracle --a a.csv --b b.csv
+  python -m paper_1810_00118_b200.cli bench --kind two_blobs --n 128 --algos ml-pdhg \\
+      --levels 1,4 --alphas -1,0 --out sweep.csv
+  python -m paper_1810_00118_b200.cli bench --images im0.pgm ... im9.pgm --levels 4  # 45 pairs
+  python -m paper_1810_00118_b200.cli validate --kind two_blobs --n 128 --count 4 --levels 3
 
 Inputs: PGM (P2 ASCII or P5 binary, maxval <= 65535) or CSV (one image row
 per line).  An M x M image is solved on N = M cells; densities
@@ -245,30 +249,9 @@ def solve(args) -> int:
 def gen(args) -> int:
     from . import instances
 
-    n = args.n
-    rng = np.random.default_rng(args.seed)
-    t = (np.arange(n) + 0.5) / n
-    X, Y = np.meshgrid(t, t, indexing="xy")
-    if args.kind == "two_blobs":
-        c = rng.uniform(0.2, 0.8, size=(2, 2))
-        a = np.exp(-((X - c[0, 0]) ** 2 + (Y - c[0, 1]) ** 2) / (2 * 0.08 ** 2))
-        b = np.exp(-((X - c[1, 0]) ** 2 + (Y - c[1, 1]) ** 2) / (2 * 0.08 ** 2))
-    elif args.kind == "annulus_pair":
-        r = np.hypot(X - 0.5, Y - 0.5)
-        a = np.exp(-((r - 0.15) / 0.03) ** 2)
-        b = np.exp(-((r - 0.35) / 0.03) ** 2)
-    elif args.kind == "dirac_pair":
-        a = np.zeros((n, n))
-        b = np.zeros((n, n))
-        a[0, 0] = 1.0
-        b[0, n - 1] = 1.0
-    elif args.kind == "config2":
-        a, b = instances.config2_images(seed=args.seed, m=n)
-    elif args.kind == "config3":
-        a = instances.blurred_noise_image(2 * args.seed, m=n)
-        b = instances.blurred_noise_image(2 * args.seed + 1, m=n)
-    else:
+    if args.kind not in instances.SYNTH_KINDS:
         return EXIT_USAGE
+    a, b = instances.synth_instance(args.kind, args.n, args.seed)
     for img, path in ((a, args.out_a), (b, args.out_b)):
         if path.lower().endswith(".csv"):
             np.savetxt(path, img, delimiter=",", fmt="%.17g")
@@ -287,6 +270,86 @@ def oracle_cmd(args) -> int:
     rho = discretize(a, n) - discretize(b, n)
     rho -= rho.mean()
     print(json.dumps({"w1_exact_p1": exact.w1_exact_p1(rho), "n": n}))
+    return EXIT_OK
+
+
+def _instance(args, seed_offset: int = 0):
+    from . import instances
+
+    if getattr(args, "a", None) and getattr(args, "b", None):
+        a, b = read_image(args.a), read_image(args.b)
+        if a.shape != b.shape:
+            raise FormatError("images differ in size")
+        return a, b
+    if args.kind not in instances.SYNTH_KINDS:
+        raise FormatError(f"unknown instance kind {args.kind!r}")
+    return instances.synth_instance(args.kind, args.n, args.seed + seed_offset)
+
+
+def _csv_list(text: str, conv):
+    try:
+        return [conv(x) for x in text.split(",") if x.strip()]
+    except ValueError as e:
+        raise FormatError(f"bad list {text!r}: {e}") from None
+
+
+def _emit(path, header, rows) -> None:
+    lines = [",".join(header)] + [",".join(str(v) for v in r) for r in rows]
+    text = "\n".join(lines) + "\n"
+    if path:
+        with open(path, "w") as f:
+            f.write(text)
+    else:
+        sys.stdout.write(text)
+
+
+def bench_cmd(args) -> int:
+    """Timing / iteration sweeps (paper Tables 4-6 shape), or the
+    all-vs-all pair timing on the batched engine (--images ...)."""
+    from . import studies, w1mg
+
+    p = w1mg.pnorm_from_string(args.p)
+    if args.images:
+        imgs = [read_image(pth) for pth in args.images]
+        if len(imgs) < 2:
+            raise FormatError("--images needs at least two files")
+        levels = int(args.levels.split(",")[0])
+        rows = studies.all_pairs(imgs, levels, p=p, rel_tol=args.rel_tol,
+                                 max_iters=args.max_iters)
+        _emit(args.out, ["i", "j", "n", "levels", "p", "distance", "dual_value", "iters",
+                         "converged", "batch_pairs", "batch_seconds"],
+              [[r["i"], r["j"], r["n"], r["levels"], args.p, repr(r["distance"]),
+                repr(r["dual_value"]), "/".join(map(str, r["iters"])), int(r["converged"]),
+                r["batch_pairs"], f"{r['batch_seconds']:.6f}"] for r in rows])
+        return EXIT_OK if all(r["converged"] for r in rows) else EXIT_NUMERIC
+    a, b = _instance(args)
+    algos = _csv_list(args.algos, str)
+    for al in algos:
+        if al not in ("cp", "pdhg", "ml-cp", "ml-pdhg"):
+            raise FormatError(f"unknown algorithm {al!r}")
+    rows = studies.sweep(a, b, algos, _csv_list(args.levels, int), _csv_list(args.alphas, float),
+                         args.eps, p=p, max_iters=args.max_iters)
+    _emit(args.out, ["algo", "levels", "alpha", "p", "n", "eps_finest", "distance", "iters",
+                     "finest_iters", "seconds", "converged"],
+          [[r.algo, r.levels, r.alpha, args.p, r.n, r.eps_finest, repr(r.distance),
+            "/".join(map(str, r.iters)), r.iters[-1], f"{r.seconds:.6f}", int(r.converged)]
+           for r in rows])
+    return EXIT_OK if all(r.converged for r in rows) else EXIT_NUMERIC
+
+
+def validate_cmd(args) -> int:
+    """validate_assumptions as a Table-3-shaped CSV."""
+    from . import studies, w1mg
+
+    p = w1mg.pnorm_from_string(args.p)
+    insts = [_instance(args, k) for k in range(args.count)]
+    rep = studies.validate_assumptions(insts, args.levels, eps=args.eps, p=p,
+                                       max_iters=args.max_iters)
+    rows = [[r.level, repr(r.h), repr(r.z_norm2), repr(r.y_norm2),
+             "" if r.z_disc is None else repr(r.z_disc),
+             "" if r.y_disc is None else repr(r.y_disc)] for r in rep.rows]
+    rows.append(["fit", "", "", "", f"r={rep.r!r}", f"nu={rep.nu!r}"])
+    _emit(args.out, ["level", "h", "z_norm2", "y_norm2", "z_disc", "y_disc"], rows)
     return EXIT_OK
 
 
@@ -316,6 +379,33 @@ def main(argv=None) -> int:
     o = sub.add_parser("oracle")
     o.add_argument("--a", required=True)
     o.add_argument("--b", required=True)
+    bn = sub.add_parser("bench")
+    bn.add_argument("--a")
+    bn.add_argument("--b")
+    bn.add_argument("--kind", default="two_blobs")
+    bn.add_argument("--n", type=int, default=64)
+    bn.add_argument("--seed", type=int, default=0)
+    bn.add_argument("--p", default="2", choices=["1", "2", "inf"])
+    bn.add_argument("--algos", default="cp,ml-cp,pdhg,ml-pdhg")
+    bn.add_argument("--levels", default="1,2,3,4")
+    bn.add_argument("--alphas", default="-1")
+    bn.add_argument("--eps", type=float, default=1e-6)
+    bn.add_argument("--rel-tol", type=float, default=1e-5)
+    bn.add_argument("--max-iters", type=int, default=5_000_000)
+    bn.add_argument("--images", nargs="*")
+    bn.add_argument("--out")
+    va = sub.add_parser("validate")
+    va.add_argument("--a")
+    va.add_argument("--b")
+    va.add_argument("--kind", default="two_blobs")
+    va.add_argument("--n", type=int, default=64)
+    va.add_argument("--seed", type=int, default=0)
+    va.add_argument("--count", type=int, default=4)
+    va.add_argument("--levels", type=int, default=3)
+    va.add_argument("--eps", type=float, default=1e-8)
+    va.add_argument("--p", default="2", choices=["1", "2", "inf"])
+    va.add_argument("--max-iters", type=int, default=5_000_000)
+    va.add_argument("--out")
     try:
         args = ap.parse_args(argv)
     except SystemExit:
@@ -324,7 +414,8 @@ def main(argv=None) -> int:
         ap.print_usage()
         return EXIT_USAGE
     try:
-        return {"solve": solve, "gen": gen, "oracle": oracle_cmd}[args.cmd](args)
+        return {"solve": solve, "gen": gen, "oracle": oracle_cmd, "bench": bench_cmd,
+                "validate": validate_cmd}[args.cmd](args)
     except FormatError as e:
         print(f"input format error: {e}", file=sys.stderr)
         return EXIT_FORMAT

@@ -38,6 +38,8 @@ __all__ = [
     "image_to_nodes",
     "block_sum",
     "ml_sources",
+    "synth_instance",
+    "SYNTH_KINDS",
 ]
 
 
@@ -244,3 +246,38 @@ def anisotropic_mixture_image(m: int, rng: np.random.Generator, k: int = 20,
 def config5_images(seed: int = 5, m: int = 4096):
     rng = np.random.default_rng(seed)
     return anisotropic_mixture_image(m, rng), anisotropic_mixture_image(m, rng)
+
+
+SYNTH_KINDS = ("two_blobs", "annulus_pair", "dirac_pair", "config2", "config3")
+
+
+def synth_instance(kind: str, n: int, seed: int = 0):
+    """Two n x n cell images of a named synthetic family (SPEC.md synth_instance;
+    stand-ins for the paper's DOTmark / two-circle / "cat" inputs): truncated
+    Gaussian blobs, an annulus pair mimicking Fig. 3's circles, one-pixel
+    Diracs at opposite corners of the bottom row, or the config-2/3 generators.
+    Deterministic in (kind, n, seed)."""
+    rng = np.random.default_rng(seed)
+    t = (np.arange(n) + 0.5) / n
+    X, Y = np.meshgrid(t, t, indexing="xy")
+    if kind == "two_blobs":
+        c = rng.uniform(0.2, 0.8, size=(2, 2))
+        a = np.exp(-((X - c[0, 0]) ** 2 + (Y - c[0, 1]) ** 2) / (2 * 0.08 ** 2))
+        b = np.exp(-((X - c[1, 0]) ** 2 + (Y - c[1, 1]) ** 2) / (2 * 0.08 ** 2))
+    elif kind == "annulus_pair":
+        r = np.hypot(X - 0.5, Y - 0.5)
+        a = np.exp(-((r - 0.15) / 0.03) ** 2)
+        b = np.exp(-((r - 0.35) / 0.03) ** 2)
+    elif kind == "dirac_pair":
+        a = np.zeros((n, n))
+        b = np.zeros((n, n))
+        a[0, 0] = 1.0
+        b[0, n - 1] = 1.0
+    elif kind == "config2":
+        a, b = config2_images(seed=seed, m=n)
+    elif kind == "config3":
+        a = blurred_noise_image(2 * seed, m=n)
+        b = blurred_noise_image(2 * seed + 1, m=n)
+    else:
+        raise ValueError(f"unknown instance kind {kind!r}")
+    return a, b
