@@ -259,8 +259,10 @@ int w1mg_set_sweep_engine(int engine);
 /* Level-resident engines (whole level in one launch, state in shared memory):
  * 1 = auto (default: thread-block-cluster engine for small batches with
  * n <= 128, one CTA per pair for n <= 64), 2 = one-CTA engine only,
- * 3 = cluster engine wherever it fits (n <= 256), 0 = off (streaming sweeps
- * only).  Also W1MG_RESIDENT=0..3. */
+ * 3 = cluster engine wherever it fits (n <= 256), 4 = cooperative-grid engine
+ * for every one-pair level (L2-resident, one launch per level; slower than
+ * streaming as measured, kept for A/B), 0 = off (streaming sweeps only).
+ * Also W1MG_RESIDENT=0..4. */
 int w1mg_set_resident_engine(int on);
 /* Tail compaction of batched levels (1 = on, default): once at most half of
  * the pairs still run, sweep grids span only the running pairs.  Also

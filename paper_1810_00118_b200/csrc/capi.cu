@@ -29,6 +29,7 @@
 #include "cp2_kernels.cuh"
 #include "cluster_kernels.cuh"
 #include "cp2w_kernels.cuh"
+#include "grid_kernels.cuh"
 
 using namespace w1mg_dev;
 
@@ -461,10 +462,40 @@ Level compacted(const Level& lv, int pairs, int num_sms) {
 // (device-side, solver_cp.cpp:128-136 semantics).  The host only watches a
 // done-counter one graph behind, so it never stalls the GPU per iteration.
 // level-resident engines (W1MG_RESIDENT): 1 = auto (cluster engine for small
-// batches with n <= 128, single-CTA engine for n <= 64 otherwise; default),
-// 2 = single-CTA engine only, 3 = cluster engine wherever it fits (n <= 256),
-// 0 = off (streaming sweeps only)
+// batches with n <= 128, single-CTA engine for n <= 64 otherwise, cooperative
+// grid engine for one pair on an L2-sized level; default), 2 = single-CTA
+// engine only, 3 = cluster engine wherever it fits (n <= 256), 4 = grid engine
+// for every one-pair level, 0 = off (streaming sweeps only)
 int g_resident = 1;
+
+// Cooperative-grid engine (grid_kernels.cuh): one pair, whole level in one
+// launch, state in L2.  Only on request (W1MG_RESIDENT=4): measured per sweep
+// it costs 7.2 us at 32^2, 7.6 us at 256^2 and 9.7 us at 512^2 (grid barrier
+// + L2 round trips of the strip ramps), vs 6.0 / 7.9 us for the streaming
+// two-sweep launches of one pair, so auto never picks it.
+bool grid_ok(const w1mg_ctx* c, const Level& lv) {
+    (void)c;
+    return g_resident == 4 && !lv.slab && lv.B == 1;
+}
+
+template <int PN>
+void launch_grid_pn(w1mg_ctx* c, const Level& lv) {
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cp_grid_kernel<PN>, kGridWarps * 32, 0));
+    if (occ < 1) fail(W1MG_ECUDA, "grid engine: kernel does not fit an SM");
+    const int G = c->num_sms * std::min(occ, 2);
+    SweepArgs ag = lv.args;
+    const long TW = (long)G * kGridWarps;
+    const int nrows = ag.jhi - ag.jlo;
+    const long per_col = std::max(1L, TW / ag.ncx);
+    ag.H = std::max(2, (int)((nrows + per_col - 1) / per_col));
+    ag.nsy = (nrows + ag.H - 1) / ag.H;
+    ag.ntiles = ag.ncx * ag.nsy;
+    double* gp = c->get<double>("grid.partial", (size_t)2 * G * 3);
+    void* args[] = {(void*)&ag, (void*)&gp};
+    CK(cudaLaunchCooperativeKernel((const void*)cp_grid_kernel<PN>, dim3(G), dim3(kGridWarps * 32),
+                                   args, 0, c->stream));
+}
 
 template <int PN>
 void launch_resident_pn(const Level& lv, cudaStream_t s) {
@@ -537,6 +568,13 @@ bool launch_cluster_pn(const Level& lv, int C, cudaStream_t s) {
 
 void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
     if (max_iters <= 0) return;
+    if (grid_ok(c, lv)) {  // whole one-pair level in one cooperative launch
+        if (pn == 0) launch_grid_pn<0>(c, lv);
+        else if (pn == 1) launch_grid_pn<1>(c, lv);
+        else launch_grid_pn<2>(c, lv);
+        ++c->launches;
+        return;
+    }
     if (lv.has_tmap) mirror_rho(c, lv);
     if (const int C = cluster_size(lv, c->num_sms)) {  // whole level in one cluster launch
         bool ok = (pn == 0)   ? launch_cluster_pn<0>(lv, C, c->stream)
@@ -1243,7 +1281,7 @@ int w1mg_set_sweep_engine(int engine) {
 }
 
 int w1mg_set_resident_engine(int on) {
-    g_resident = (on >= 0 && on <= 3) ? on : 1;
+    g_resident = (on >= 0 && on <= 4) ? on : 1;
     return W1MG_OK;
 }
 

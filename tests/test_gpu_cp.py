@@ -51,7 +51,8 @@ def _random_source(n, seed):
     return instances.make_source(a, b, n)
 
 
-ENGINES = {"auto": (1, 3), "cluster": (3, 3), "resident-1cta": (2, 3), "stream-tma2": (0, 2),
+ENGINES = {"auto": (1, 3), "cluster": (3, 3), "resident-1cta": (2, 3), "grid": (4, 3),
+           "stream-tma2": (0, 2),
            "stream-tma2w": (0, 4), "stream-tma2t": (0, 5), "stream-tma": (0, 1),
            "stream-ldg": (0, 0)}
 
