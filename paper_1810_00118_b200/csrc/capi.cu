@@ -352,15 +352,22 @@ int g_sweep_variant = kAuto;
 constexpr int kTma2W = 4;  // two-sweep, two column sets per lane (cp2w_kernels.cuh)
 constexpr int kTma2T = 5;  // two-sweep, ring fed by one tensor-map box per row
 
-template <int NW>
-void launch_tmap(const Level& lv, int pn, int parity, cudaStream_t s) {
+template <int NW, bool U>
+void launch_tmap_u(const Level& lv, int pn, int parity, cudaStream_t s) {
     const dim3 blk(NW * 32);
     const int sm = tmap_smem(NW);
     switch (pn) {
-        case 0: cp_sweep2_tmap_kernel<0, NW><<<lv.grid2t, blk, sm, s>>>(lv.args2, parity, lv.tmap); break;
-        case 1: cp_sweep2_tmap_kernel<1, NW><<<lv.grid2t, blk, sm, s>>>(lv.args2, parity, lv.tmap); break;
-        default: cp_sweep2_tmap_kernel<2, NW><<<lv.grid2t, blk, sm, s>>>(lv.args2, parity, lv.tmap); break;
+        case 0: cp_sweep2_tmap_kernel<0, NW, U><<<lv.grid2t, blk, sm, s>>>(lv.args2, parity, lv.tmap); break;
+        case 1: cp_sweep2_tmap_kernel<1, NW, U><<<lv.grid2t, blk, sm, s>>>(lv.args2, parity, lv.tmap); break;
+        default: cp_sweep2_tmap_kernel<2, NW, U><<<lv.grid2t, blk, sm, s>>>(lv.args2, parity, lv.tmap); break;
     }
+}
+
+// the unrolled march is faster on batches, slower on one big grid (cp2_kernels.cuh)
+template <int NW>
+void launch_tmap(const Level& lv, int pn, int parity, cudaStream_t s) {
+    if (lv.B > 1) launch_tmap_u<NW, true>(lv, pn, parity, s);
+    else launch_tmap_u<NW, false>(lv, pn, parity, s);
 }
 
 bool two_sweep(const Level& lv) {
