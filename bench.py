@@ -505,7 +505,7 @@ def main():
                        for n, s_, c_ in zip(level_sizes(), lev_s, lev_cu)],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": measured_traffic(),
-                         "kernel": "w1mg_dev::cp_sweep2_tmap_kernel<1,4> (two fused PD sweeps "
+                         "kernel": "w1mg_dev::cp_sweep2_tmap_kernel<1,4,true> (two fused PD sweeps "
                                    "per HBM pass, tensor-map ring, 512^2 level); achieved = "
                                    "algorithmic one-sweep 8(3V+4E) bytes per sweep / device "
                                    "time per sweep; traffic = ncu DRAM bytes of one launch "
