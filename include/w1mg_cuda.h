@@ -230,12 +230,23 @@ int w1mg_nccl_unique_id(unsigned char* id128);
 int w1mg_slab_comm_create(w1mg_ctx* ctx, int world, int rank, const unsigned char* id128,
                           w1mg_slab_comm** out);
 void w1mg_slab_comm_destroy(w1mg_slab_comm* comm);
+/* Fused peer transport for slab runs of an n-cell grid on this comm
+ * (collective): allocates this rank's IPC-shared arena (slab buffer, residual
+ * mailbox, arrival counter), exchanges CUDA IPC handles with ncclAllGather and
+ * maps every peer's arena (NVLink P2P).  Afterwards the sweeps store halo rows
+ * directly into the neighbours' buffers and post residual sums to every
+ * rank's mailbox -- no NCCL calls per sweep. */
+int w1mg_slab_comm_enable_peer(w1mg_ctx* ctx, w1mg_slab_comm* comm, int n);
+/* Transport of emulated slabs (comm == NULL): 1 = fused peer stores between
+ * the slabs (default), 0 = device-copy halos. */
+int w1mg_set_slab_transport(int peer);
 /* cp_run on a decomposed grid.  comm == NULL: `nslabs` slabs emulated on the
- * context's device (halo exchange by device copies).  comm != NULL: this
- * rank's slab of comm's world (halos by ncclSend/ncclRecv, residual by
- * ncclAllReduce, all on the context stream inside CUDA graphs).  Inputs are
- * full-grid host arrays; outputs are written for the owned rows only; W1,
- * dual, iterations and history are global. */
+ * context's device (see w1mg_set_slab_transport).  comm != NULL: this rank's
+ * slab of comm's world (fused peer transport after
+ * w1mg_slab_comm_enable_peer, else halos by ncclSend/ncclRecv and the
+ * residual by ncclAllReduce; all on the context stream inside CUDA graphs).
+ * Inputs are full-grid host arrays; outputs are written for the owned rows
+ * only; W1, dual, iterations and history are global. */
 int w1mg_slab_cp_run(w1mg_ctx* ctx, w1mg_slab_comm* comm, int n, int nslabs, const double* rho,
                      const double* m0x, const double* m0y, const double* phi0, int pnorm,
                      double mu, double tau, double tol, long max_iters, double* mx, double* my,

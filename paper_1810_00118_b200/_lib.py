@@ -122,6 +122,8 @@ def lib():
         L.w1mg_slab_comm_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p,
                                             C.POINTER(C.c_void_p)]
         L.w1mg_slab_comm_destroy.argtypes = [C.c_void_p]
+        L.w1mg_slab_comm_enable_peer.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+        L.w1mg_set_slab_transport.argtypes = [C.c_int]
         L.w1mg_slab_cp_run.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, _dp, _dp, _dp,
                                        _dp, C.c_int, C.c_double, C.c_double, C.c_double,
                                        C.c_long, _dp, _dp, _dp, _dp, C.c_long,

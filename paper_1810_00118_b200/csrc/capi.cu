@@ -216,8 +216,11 @@ void set_geometry(Level& lv, int pairs, int num_sms) {
 
 // jhi < 0: whole grid.  Otherwise a row slab owning global rows [jlo, jhi),
 // stored with one halo row below and two above (Layout::make_slab).
+// ext_base: use this buffer (B * NSLOT planes) instead of a context buffer
+// (row slabs whose buffer is shared with peers through CUDA IPC).
 Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, double tau,
-                 double* hist, long hist_cap, int jlo = 0, int jhi = -1) {
+                 double* hist, long hist_cap, int jlo = 0, int jhi = -1,
+                 double* ext_base = nullptr) {
     Level lv;
     lv.n = n;
     lv.B = B;
@@ -227,7 +230,7 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
         jhi = n + 1;
     }
     lv.L = lv.slab ? Layout::make_slab(n, jlo - 1, jhi + 2) : Layout::make(n);
-    lv.base = c->get<double>(tag + ".base", (size_t)B * NSLOT * lv.L.plane);
+    lv.base = ext_base ? ext_base : c->get<double>(tag + ".base", (size_t)B * NSLOT * lv.L.plane);
     lv.ctl = c->get<PairCtl>(tag + ".ctl", B);
     lv.ticket = c->get<unsigned>(tag + ".ticket", B);
     lv.ndone = c->get<int>(tag + ".ndone", 1);

@@ -76,6 +76,21 @@ struct SweepArgs {
     int* ndone;         // number of stopped pairs
     const int* act;     // compacted launch: blockIdx.y indexes act[0, *nact) (null: pair = blockIdx.y)
     const int* nact;
+    // row slab with the fused peer transport (slab_engine.cuh): the sweep
+    // stores its top owned row into the upper neighbour's lower halo row and
+    // its first row's phi into the lower neighbour's upper halo row (peer
+    // memory: NVLink P2P stores, or another slab on the same device), and the
+    // last block posts the slab's residual sums to every rank's mailbox.
+    double* up_base;    // upper neighbour's level buffer (null: none)
+    long up_plane;
+    int up_row0;
+    double* dn_base;    // lower neighbour's level buffer (null: none)
+    long dn_plane;
+    int dn_row0;
+    double* const* mail;                // [pworld] mailboxes, each [2][pworld][3]
+    unsigned long long* const* arrive;  // [pworld] arrival counters
+    int prank, pworld;
+    int psys;  // peers on other GPUs: system-scope fences/atomics (0: same device)
 };
 
 // Pair of this block.  In a compacted launch (the tail of a batched level, see
@@ -113,6 +128,7 @@ __device__ __forceinline__ void node_flux(bool hx, bool hy, double pc, double pr
 // Everything a warp needs about its strip.
 struct Strip {
     int i, j0, j1;
+    int wpar;  // buffer parity written by this sweep
     bool in, hx, own;
     const double* phr;
     const double* mxr;
@@ -132,6 +148,7 @@ __device__ __forceinline__ Strip make_strip(const SweepArgs& a, int pair, int pa
     s.i = cx * kOwn - 1 + lane;
     s.j0 = a.jlo + sy * a.H;
     s.j1 = min(s.j0 + a.H, a.jhi);
+    s.wpar = 1 - parity;
     double* pb = a.base + (long)pair * NSLOT * L.plane;
     s.phr = pb + (PHI0 + parity) * L.plane;
     s.mxr = pb + (MX0 + parity) * L.plane;
@@ -190,6 +207,15 @@ __device__ __forceinline__ void row_update(const SweepArgs& a, const Strip& s, i
         s_dm2 += dx * dx + dy * dy;
         s_dp2 += d * d;
         s_cr += d * divd;
+        if (a.up_base && j == a.jhi - 1) {  // top owned row -> upper neighbour's halo
+            const long po = 32 + (long)(j - a.up_row0) * a.L.pitch + s.i;
+            a.up_base[(PHI0 + s.wpar) * a.up_plane + po] = pc + d;
+            if (s.hx) a.up_base[(MX0 + s.wpar) * a.up_plane + po] = ux;
+            if (hy) a.up_base[(MY0 + s.wpar) * a.up_plane + po] = uy;
+        }
+        if (a.dn_base && j == a.jlo)  // first owned row's phi -> lower neighbour's halo
+            a.dn_base[(PHI0 + s.wpar) * a.dn_plane + 32 + (long)(j - a.dn_row0) * a.L.pitch + s.i] =
+                pc + d;
     }
     uyb = uy;
     dyb = dy;
@@ -254,7 +280,19 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
         part[bid * 3 + 0] = t0;
         part[bid * 3 + 1] = t1;
         part[bid * 3 + 2] = t2;
-        __threadfence();
+        // peer transport: a block that stored halo rows into a neighbour
+        // makes them visible at the neighbour's scope before the last block
+        // signals arrival (blocks of the first / last strip row only)
+        bool remote = false;
+        if (a.mail && a.psys)
+            for (int w = 0; w < kSweepWarps; ++w) {
+                const int t = bid * kSweepWarps + w;
+                if (t >= a.ntiles) break;
+                const int sy = t / a.ncx;
+                remote |= (sy == 0 && a.dn_base) || (sy == a.nsy - 1 && a.up_base);
+            }
+        if (remote) __threadfence_system();
+        else __threadfence();
         unsigned t = atomicAdd(a.ticket + pair, 1u);
         is_last = (t == (unsigned)nblk - 1);
     }
@@ -287,7 +325,23 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
             scr += red[w][2];
         }
         a.ticket[pair] = 0u;
-        if (a.red_out) {
+        if (a.mail) {
+            // peer transport: post the slab's sums to every rank's mailbox
+            // (slot [parity][prank]), then count one arrival on every rank
+            for (int q = 0; q < a.pworld; ++q) {
+                double* mb = a.mail[q] + ((long)parity * a.pworld + a.prank) * 3;
+                mb[0] = sdm2;
+                mb[1] = sdp2;
+                mb[2] = scr;
+            }
+            if (a.psys) {
+                __threadfence_system();
+                for (int q = 0; q < a.pworld; ++q) atomicAdd_system(a.arrive[q], 1ull);
+            } else {
+                __threadfence();
+                for (int q = 0; q < a.pworld; ++q) atomicAdd(a.arrive[q], 1ull);
+            }
+        } else if (a.red_out) {
             // row slab: publish this slab's sums; the cross-slab reduction
             // (device copy or NCCL all-reduce) then runs finalize_pair
             a.red_out[(long)pair * 3 + 0] = sdm2;

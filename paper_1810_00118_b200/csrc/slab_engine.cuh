@@ -16,11 +16,23 @@
 // fields are bit-identical to the undecomposed solve; only the residual sum is
 // reassociated.
 //
-// Transports: `emulated` keeps all slabs on one device and exchanges halos
-// with device copies (used by the parity tests on a single B200); `nccl` runs
-// one slab per rank (one process per GPU) with ncclSend/ncclRecv for the
-// halos and an ncclAllReduce of the three sums, all on the context stream and
-// captured in the same CUDA graph as the sweeps.
+// Transports:
+//   * peer (default): the exchange is fused into the sweep.  The rows a
+//     neighbour needs are stored straight into its halo rows by the warps
+//     that compute them (row_update, peer pointers), and the last block posts
+//     the slab's three sums into every rank's mailbox and bumps every rank's
+//     arrival counter (system-scope fence + atomic).  A one-thread finalize
+//     kernel then waits for the world's arrivals of this sweep, reduces the
+//     mailbox in rank order and applies the stop rule -- no copies, no
+//     collectives.  Emulated on one device the peers are the other slabs;
+//     across processes (one GPU each) the level buffers, mailboxes and
+//     counters live in one IPC-shared arena per rank
+//     (w1mg_slab_comm_enable_peer) and the stores travel over NVLink.
+//   * copies / nccl: emulated slabs exchange halos with device copies; a
+//     communicator without peer memory uses ncclSend/ncclRecv for the halos
+//     and an ncclAllReduce of the three sums (the collective baseline).
+// Both run on the context stream and are captured in one CUDA graph per 16
+// sweeps.
 #pragma once
 
 #include <nccl.h>
@@ -44,6 +56,52 @@ __global__ void slab_finalize_kernel(SweepArgs a, PairCtl* ctl_all, int nslab, c
         SweepArgs b = a;
         b.ctl = ctl_all + r;
         b.ndone = (r == 0) ? ndone : nullptr;  // the host watches one counter
+        if (r > 0) b.hist = nullptr;
+        finalize_pair<false>(b, 0, parity, s0, s1, s2);
+    }
+}
+
+// Peer transport: wait until every rank has posted sweep `it` (arrivals
+// counted since `base`), reduce the mailbox in rank order, stop rule for every
+// local slab.  A peer that never arrives (dead process) trips the time bound:
+// every local slab is stopped with nonfinite = 2 and the host fails loudly.
+__global__ void slab_peer_finalize_kernel(SweepArgs a, PairCtl* ctl_all, int nloc,
+                                          const double* mail, unsigned long long* const* arrive_loc,
+                                          unsigned long long base, int world, int parity,
+                                          int* ndone) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (ctl_all[0].done) return;
+    const unsigned long long target = base + (unsigned long long)world * (ctl_all[0].it + 1);
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int q = 0; q < nloc; ++q) {
+        const volatile unsigned long long* cnt = arrive_loc[q];
+        while (*cnt < target) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 30ull * 1000000000ull) {  // 30 s without the peers
+                for (int r = 0; r < nloc; ++r) {
+                    ctl_all[r].nonfinite = 2;
+                    ctl_all[r].done = 1;
+                }
+                atomicAdd(ndone, 1);
+                return;
+            }
+            __nanosleep(64);
+        }
+    }
+    __threadfence_system();
+    const volatile double* mb = mail + (long)parity * world * 3;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int r = 0; r < world; ++r) {
+        s0 += mb[r * 3 + 0];
+        s1 += mb[r * 3 + 1];
+        s2 += mb[r * 3 + 2];
+    }
+    for (int r = 0; r < nloc; ++r) {
+        SweepArgs b = a;
+        b.ctl = ctl_all + r;
+        b.ndone = (r == 0) ? ndone : nullptr;
         if (r > 0) b.hist = nullptr;
         finalize_pair<false>(b, 0, parity, s0, s1, s2);
     }
@@ -83,6 +141,15 @@ struct w1mg_slab_comm {
     ncclComm_t comm = nullptr;
     int rank = 0;
     int world = 1;
+    // peer transport (w1mg_slab_comm_enable_peer): one IPC-shared arena per
+    // rank = [level buffer of its slab][mailbox 2 x world x 3][arrival counter]
+    int peer_n = 0;                     // grid the arena is laid out for (0: no peer memory)
+    void* arena = nullptr;              // mine
+    std::vector<char*> peer_arena;      // every rank's arena in my address space
+    std::vector<size_t> mail_off;       // per rank: mailbox offset in its arena
+    double** mail_ptrs = nullptr;       // device array [world]
+    unsigned long long** arrive_ptrs = nullptr;  // device array [world]
+    unsigned long long arrive_base = 0; // arrivals counted on my counter so far
 };
 
 namespace {
@@ -103,7 +170,21 @@ struct SlabSet {
     double* sums = nullptr;  // [3] (NCCL all-reduce target)
     int* ndone = nullptr;
     w1mg_slab_comm* comm = nullptr;  // null: emulated on one device
+    // peer transport
+    bool peer = false;
+    const double* mail = nullptr;              // my (first local slab's) mailbox
+    unsigned long long** arrive_loc = nullptr; // device array [nloc]: local counters
+    unsigned long long base = 0;               // arrivals before this run
 };
+
+// emulated-slab transport: 1 = fused peer stores (default), 0 = device copies
+int g_slab_peer = 1;
+
+Layout slab_layout(int n, const std::vector<int>& b, int r) {
+    return Layout::make_slab(n, b[r] - 1, b[r + 1] + 2);
+}
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 void check_nccl(ncclResult_t r, const char* what) {
     if (r != ncclSuccess) fail(W1MG_ECUDA, std::string("NCCL ") + what + ": " + ncclGetErrorString(r));
@@ -125,11 +206,15 @@ SlabSet make_slabs(w1mg_ctx* c, const std::string& tag, int n, int R, w1mg_slab_
     s.red = c->get<double>(tag + ".red", 3 * nloc);
     s.sums = c->get<double>(tag + ".sums", 3);
     s.ndone = c->get<int>(tag + ".ndone_all", 1);
+    s.peer = comm ? (comm->peer_n > 0) : (g_slab_peer != 0);
+    if (comm && s.peer && comm->peer_n != n)
+        fail(W1MG_EINVAL, "slab comm peer memory was enabled for another grid size");
     for (int q = 0; q < nloc; ++q) {
         const int r = comm ? comm->rank : q;
         const bool first = comm ? (r == 0) : (q == 0);
+        double* ext = (comm && s.peer) ? static_cast<double*>(comm->arena) : nullptr;
         Level lv = make_level(c, tag + std::to_string(r), n, 1, mu, tau, first ? hist : nullptr,
-                              first ? hist_cap : 0, s.bounds[r], s.bounds[r + 1]);
+                              first ? hist_cap : 0, s.bounds[r], s.bounds[r + 1], ext);
         lv.ctl = s.ctl + q;
         lv.args.ctl = lv.ctl;
         lv.args2.ctl = lv.ctl;
@@ -138,6 +223,69 @@ SlabSet make_slabs(w1mg_ctx* c, const std::string& tag, int n, int R, w1mg_slab_
         lv.args.ndone = nullptr;
         s.lv.push_back(lv);
     }
+    if (!s.peer) return s;
+    // peer transport wiring: neighbours' buffers, every rank's mailbox/counter
+    const int W = s.R;
+    std::vector<double*> mails(W);
+    std::vector<unsigned long long*> arrives(W);
+    std::vector<double*> bases(W, nullptr);
+    if (comm) {
+        for (int r = 0; r < W; ++r) {
+            char* ar = comm->peer_arena[r];
+            bases[r] = reinterpret_cast<double*>(ar);
+            mails[r] = reinterpret_cast<double*>(ar + comm->mail_off[r]);
+            arrives[r] = reinterpret_cast<unsigned long long*>(ar + comm->mail_off[r] +
+                                                               align256((size_t)2 * W * 3 * 8));
+        }
+        s.base = comm->arrive_base;
+    } else {
+        double* mb = c->get<double>(tag + ".mail", (size_t)W * 2 * W * 3);
+        auto* cnt = c->get<unsigned long long>(tag + ".arrive", W);
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * W, c->stream));
+        for (int r = 0; r < W; ++r) {
+            bases[r] = s.lv[r].base;
+            mails[r] = mb + (size_t)r * 2 * W * 3;
+            arrives[r] = cnt + r;
+        }
+        s.base = 0;
+    }
+    double** dmail = comm ? comm->mail_ptrs : c->get<double*>(tag + ".mailp", W);
+    unsigned long long** darr = comm ? comm->arrive_ptrs : c->get<unsigned long long*>(tag + ".arrp", W);
+    if (!comm) {
+        CK(cudaMemcpyAsync(dmail, mails.data(), sizeof(double*) * W, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(darr, arrives.data(), sizeof(void*) * W, cudaMemcpyHostToDevice, c->stream));
+    }
+    const int me0 = comm ? comm->rank : 0;
+    s.mail = mails[me0];
+    s.arrive_loc = c->get<unsigned long long*>(tag + ".arrloc", nloc);
+    std::vector<unsigned long long*> loc(nloc);
+    for (int q = 0; q < nloc; ++q) loc[q] = arrives[comm ? comm->rank : q];
+    CK(cudaMemcpyAsync(s.arrive_loc, loc.data(), sizeof(void*) * nloc, cudaMemcpyHostToDevice,
+                       c->stream));
+    for (int q = 0; q < nloc; ++q) {
+        const int r = comm ? comm->rank : q;
+        SweepArgs& a = s.lv[q].args;
+        a.red_out = nullptr;
+        a.mail = dmail;
+        a.arrive = darr;
+        a.prank = r;
+        a.pworld = W;
+        a.psys = comm ? 1 : 0;
+        if (r + 1 < W) {
+            const Layout U = slab_layout(n, s.bounds, r + 1);
+            a.up_base = bases[r + 1];
+            a.up_plane = U.plane;
+            a.up_row0 = U.row0;
+        }
+        if (r > 0) {
+            const Layout D = slab_layout(n, s.bounds, r - 1);
+            a.dn_base = bases[r - 1];
+            a.dn_plane = D.plane;
+            a.dn_row0 = D.row0;
+        }
+    }
+    // the host-side copies above must land before the captured graph runs
+    CK(cudaStreamSynchronize(c->stream));
     return s;
 }
 
@@ -211,6 +359,14 @@ void slab_exchange(w1mg_ctx* c, SlabSet& s, int w) {
 void slab_iteration(w1mg_ctx* c, SlabSet& s, int pn, int parity) {
     for (auto& lv : s.lv) launch_sweep(lv, pn, parity, c->stream);
     CK(cudaGetLastError());
+    if (s.peer) {  // exchange and sums already posted by the sweeps
+        slab_peer_finalize_kernel<<<1, 32, 0, c->stream>>>(s.lv[0].args, s.ctl, (int)s.lv.size(),
+                                                          s.mail, s.arrive_loc, s.base, s.R,
+                                                          parity, s.ndone);
+        CK(cudaGetLastError());
+        c->launches += (long)s.lv.size() + 1;
+        return;
+    }
     slab_exchange(c, s, 1 - parity);
     const double* red = s.red;
     int nred = (int)s.lv.size();
@@ -232,6 +388,11 @@ void slab_run(w1mg_ctx* c, SlabSet& s, int pn, double tol, long max_iters) {
     ++c->launches;
     CK(cudaGetLastError());
     for (auto& lv : s.lv) CK(cudaMemsetAsync(lv.ticket, 0, sizeof(unsigned), c->stream));
+    if (s.comm && s.peer && s.comm->world > 1) {
+        // every rank has loaded its slab before any peer stores into it
+        double* d = c->get<double>("slab.barrier", 1);
+        check_nccl(ncclAllReduce(d, d, 1, ncclDouble, ncclSum, s.comm->comm, c->stream), "barrier");
+    }
     if (max_iters <= 0) return;
     constexpr int K = 16;
     if (max_iters < K) {
@@ -264,6 +425,13 @@ void slab_run(w1mg_ctx* c, SlabSet& s, int pn, double tol, long max_iters) {
     }
     CK(cudaStreamSynchronize(c->stream));
     CK(cudaGraphExecDestroy(ex));
+}
+
+// After a run: peer arrivals consumed on my counter, and the time-bound check.
+void slab_after_run(SlabSet& s, const PairCtl& hc) {
+    if (!s.peer) return;
+    if (hc.nonfinite == 2) fail(W1MG_ECUDA, "slab peer transport: a peer did not arrive within 30 s");
+    if (s.comm) s.comm->arrive_base += (unsigned long long)s.comm->world * (unsigned long long)hc.it;
 }
 
 // Device-side load of slab rows from a whole-grid level (buffer 0 of pair 0).
@@ -340,6 +508,8 @@ int w1mg_ml_slab_cp_run(w1mg_ctx* c, w1mg_slab_comm* comm, int nslabs, int n_fin
         CK(cudaEventRecord(e1, c->stream));
         PairCtl hc;
         CK(cudaMemcpyAsync(&hc, s.ctl, sizeof(PairCtl), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        slab_after_run(s, hc);
         std::vector<long> hit(levels - 1);
         std::vector<double> hff(levels - 1), htl(levels - 1);
         CK(cudaMemcpyAsync(hit.data(), it, (levels - 1) * sizeof(long), cudaMemcpyDeviceToHost, c->stream));
@@ -439,8 +609,82 @@ int w1mg_slab_comm_create(w1mg_ctx* c, int world, int rank, const unsigned char*
 
 void w1mg_slab_comm_destroy(w1mg_slab_comm* s) {
     if (!s) return;
+    for (int r = 0; r < (int)s->peer_arena.size(); ++r)
+        if (r != s->rank && s->peer_arena[r]) cudaIpcCloseMemHandle(s->peer_arena[r]);
+    if (s->arena) cudaFree(s->arena);
+    if (s->mail_ptrs) cudaFree(s->mail_ptrs);
+    if (s->arrive_ptrs) cudaFree(s->arrive_ptrs);
     if (s->comm) ncclCommDestroy(s->comm);
     delete s;
+}
+
+// Peer transport for a multi-process slab decomposition of an n-cell grid:
+// allocate this rank's arena (its slab's level buffer, mailbox, arrival
+// counter), exchange CUDA IPC handles over the communicator (ncclAllGather)
+// and map every other rank's arena (NVLink peer access).  Collective over the
+// communicator.  Afterwards slab runs on this comm with grid n use the fused
+// peer transport instead of NCCL send/recv + all-reduce.
+int w1mg_slab_comm_enable_peer(w1mg_ctx* c, w1mg_slab_comm* s, int n) {
+    return guard([&] {
+        check_n(n);
+        if (!s) fail(W1MG_EINVAL, "null comm");
+        if (s->peer_n) fail(W1MG_ELOGIC, "peer memory already enabled on this comm");
+        CK(cudaSetDevice(c->device));
+        const int R = s->world;
+        const std::vector<int> b = slab_bounds(n, R);
+        for (int r = 1; r <= R; ++r)
+            if (b[r] - b[r - 1] < 2) fail(W1MG_EINVAL, "slab decomposition: fewer than 2 rows per slab");
+        s->mail_off.resize(R);
+        for (int r = 0; r < R; ++r)
+            s->mail_off[r] = align256((size_t)NSLOT * slab_layout(n, b, r).plane * 8);
+        const size_t bytes = s->mail_off[s->rank] + align256((size_t)2 * R * 3 * 8) + 256;
+        CK(cudaMalloc(&s->arena, bytes));
+        CK(cudaMemset(s->arena, 0, bytes));
+        s->peer_arena.assign(R, nullptr);
+        s->peer_arena[s->rank] = static_cast<char*>(s->arena);
+        if (R > 1) {
+            cudaIpcMemHandle_t mine;
+            CK(cudaIpcGetMemHandle(&mine, s->arena));
+            char* dh = nullptr;
+            CK(cudaMalloc(&dh, sizeof(cudaIpcMemHandle_t) * R));
+            CK(cudaMemcpy(dh + sizeof(cudaIpcMemHandle_t) * s->rank, &mine, sizeof(mine),
+                          cudaMemcpyHostToDevice));
+            check_nccl(ncclAllGather(dh + sizeof(cudaIpcMemHandle_t) * s->rank, dh,
+                                     sizeof(cudaIpcMemHandle_t), ncclChar, s->comm, c->stream),
+                       "allgather IPC handles");
+            std::vector<cudaIpcMemHandle_t> all(R);
+            CK(cudaMemcpyAsync(all.data(), dh, sizeof(cudaIpcMemHandle_t) * R, cudaMemcpyDeviceToHost,
+                               c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            CK(cudaFree(dh));
+            for (int r = 0; r < R; ++r) {
+                if (r == s->rank) continue;
+                void* p = nullptr;
+                CK(cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess));
+                s->peer_arena[r] = static_cast<char*>(p);
+            }
+        }
+        std::vector<double*> mails(R);
+        std::vector<unsigned long long*> arr(R);
+        for (int r = 0; r < R; ++r) {
+            mails[r] = reinterpret_cast<double*>(s->peer_arena[r] + s->mail_off[r]);
+            arr[r] = reinterpret_cast<unsigned long long*>(s->peer_arena[r] + s->mail_off[r] +
+                                                          align256((size_t)2 * R * 3 * 8));
+        }
+        CK(cudaMalloc(&s->mail_ptrs, sizeof(double*) * R));
+        CK(cudaMalloc(&s->arrive_ptrs, sizeof(void*) * R));
+        CK(cudaMemcpy(s->mail_ptrs, mails.data(), sizeof(double*) * R, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(s->arrive_ptrs, arr.data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
+        s->arrive_base = 0;
+        s->peer_n = n;
+    });
+}
+
+// Transport of emulated slabs (comm == NULL): 1 = fused peer stores
+// (default), 0 = device-copy halos + host-ordered reduction.
+int w1mg_set_slab_transport(int peer) {
+    g_slab_peer = peer ? 1 : 0;
+    return W1MG_OK;
 }
 
 // CP solve of one grid decomposed into row slabs.  comm == NULL: `nslabs`
@@ -465,6 +709,7 @@ int w1mg_slab_cp_run(w1mg_ctx* c, w1mg_slab_comm* comm, int n, int nslabs, const
         PairCtl hc;
         CK(cudaMemcpyAsync(&hc, s.ctl, sizeof(PairCtl), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
+        slab_after_run(s, hc);
         // W1 / dual over owned rows, summed over slabs (and ranks)
         double* vals = c->get<double>("slab.vals", 2 * s.lv.size());
         for (size_t q = 0; q < s.lv.size(); ++q) {

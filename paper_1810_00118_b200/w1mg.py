@@ -663,10 +663,21 @@ class SlabComm:
         check(_lib.lib().w1mg_nccl_unique_id(buf))
         return buf.raw
 
+    def enable_peer(self, n: int, device: int = 0) -> None:
+        """Fused peer transport for grid n (collective over the comm): IPC
+        arenas exchanged over NCCL, halos and residual sums stored straight
+        into the peers' memory by the sweep kernels."""
+        check(_lib.lib().w1mg_slab_comm_enable_peer(_lib.default_context(device).h, self.h, n))
+
     def close(self):
         if self.h:
             _lib.lib().w1mg_slab_comm_destroy(self.h)
             self.h = None
+
+
+def set_slab_transport(peer: bool) -> None:
+    """Emulated slabs: fused peer stores (True, default) or device copies."""
+    check(_lib.lib().w1mg_set_slab_transport(1 if peer else 0))
 
 
 def slab_cp_run(rho: SourceField, params: SolverParams, nslabs: int = 2,

@@ -1,8 +1,9 @@
 """GPU parity of the row-slab decomposition (config 5): the fused sweep on
 row slabs with a one-row halo exchange and a cross-slab residual sum must give
 fields bit-identical to the undecomposed oracle.  Slabs are emulated on one
-B200 (device-copy halos), and the NCCL transport is exercised with a
-single-rank communicator (the multi-rank protocol itself is covered on CPU by
+B200 with both transports (fused peer stores between the slabs, device-copy
+halos), and the NCCL and peer transports are exercised with a single-rank
+communicator (the multi-rank protocol itself is covered on CPU by
 tests/test_slab_gloo.py)."""
 import numpy as np
 import pytest
@@ -11,6 +12,13 @@ from paper_1810_00118_b200 import instances
 from paper_1810_00118_b200 import w1mg
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(params=["peer", "copies"])
+def transport(request):
+    w1mg.set_slab_transport(request.param == "peer")
+    yield request.param
+    w1mg.set_slab_transport(True)
 
 
 def _src(rho):
@@ -24,7 +32,7 @@ def _rand(n, seed):
 
 @pytest.mark.parametrize("nslabs", [1, 2, 3, 5])
 @pytest.mark.parametrize("n", [64, 100, 257])
-def test_slab_fixed_iterations_bit_exact(oracle, n, nslabs):
+def test_slab_fixed_iterations_bit_exact(oracle, n, nslabs, transport):
     rho = _random = _rand(n, n + nslabs)
     prm = w1mg.SolverParams(p=w1mg.PNorm.p2, tolerance=-1.0, max_iters=75)
     rep = w1mg.slab_cp_run(_src(rho), prm, nslabs=nslabs)
@@ -52,7 +60,7 @@ def test_slab_warm_start_and_converged(oracle):
     assert abs(rep.distance - ref.distance) <= 1e-4 * ref.distance
 
 
-def test_slab_4096_full_size(oracle):
+def test_slab_4096_full_size(oracle, transport):
     """Config-5 finest grid in 8 slabs (the 8-GPU partition), 4 sweeps."""
     n = 4096
     rho = _rand(n, 4096)
@@ -82,7 +90,7 @@ def test_slab_nccl_single_rank(oracle):
 
 
 @pytest.mark.parametrize("nslabs", [1, 3, 8])
-def test_ml_slab_cascade_bit_exact(oracle, nslabs):
+def test_ml_slab_cascade_bit_exact(oracle, nslabs, transport):
     """Config-5 shape at 512^2 (64 -> 512): replicated coarse levels + slab
     finest level, fixed sweeps per level: bit-exact against the oracle."""
     img0, img1 = instances.config5_images(m=512)
@@ -97,7 +105,7 @@ def test_ml_slab_cascade_bit_exact(oracle, nslabs):
     assert [l.iters for l in rep.levels] == [30] * 4
 
 
-def test_ml_slab_cascade_converged(oracle):
+def test_ml_slab_cascade_converged(oracle, transport):
     import time
 
     img0, img1 = instances.config5_images(m=256)
@@ -110,6 +118,28 @@ def test_ml_slab_cascade_converged(oracle):
     ref = oracle.ml_cp_run(rhos, p=1, rel_tol=1e-5)
     assert abs(rep.distance - ref.distance) <= 1e-4 * ref.distance
     assert all(abs(a.iters - b) <= 1 for a, b in zip(rep.levels, ref.level_iters))
+
+
+def test_slab_peer_single_rank(oracle):
+    """The peer transport on a communicator (IPC arena, mailbox, arrival
+    counter; a one-rank world has no neighbours to map)."""
+    uid = w1mg.SlabComm.new_unique_id()
+    comm = w1mg.SlabComm(1, 0, uid)
+    try:
+        n = 128
+        comm.enable_peer(n)
+        rho = _rand(n, 9)
+        for rep_i in range(2):  # arrival counting carries across runs
+            prm = w1mg.SolverParams(p=w1mg.PNorm.p2, tolerance=-1.0, max_iters=40 + rep_i)
+            rep = w1mg.slab_cp_run(_src(rho), prm, comm=comm)
+            ref = oracle.cp_run(rho, p=1, tol=-1.0, max_iters=40 + rep_i)
+            assert rep.iterations == 40 + rep_i
+            assert np.array_equal(rep.potential.values, ref.phi)
+            assert np.array_equal(rep.flux.x_edges, ref.mx)
+        with pytest.raises(ValueError):  # arena laid out for another grid
+            w1mg.slab_cp_run(_src(_rand(64, 1)), prm, comm=comm)
+    finally:
+        comm.close()
 
 
 def test_slab_bounds_partition():

@@ -101,19 +101,31 @@ def config5(nslabs=None):
         obj = [uid]
         dist.broadcast_object_list(obj, 0)
         comm = w1mg.SlabComm(world, rank, obj[0], device=int(os.environ.get("LOCAL_RANK", 0)))
+        peer = os.environ.get("W1MG_SLAB_PEER", "1") != "0"
+        if peer:  # fused P2P transport (IPC arenas over NVLink), else NCCL per sweep
+            comm.enable_peer(4096, device=int(os.environ.get("LOCAL_RANK", 0)))
         r = w1mg.ml_slab_run(rhos, comm=comm, rel_tol=1e-5)
         t = torch.tensor([r.total_seconds], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         if rank == 0:
-            line(config=5, what=f"4096^2 cascade 64->4096, finest level in {world} NCCL slabs",
+            line(config=5, what=f"4096^2 cascade 64->4096, finest level in {world} slabs "
+                 f"({'fused peer' if peer else 'NCCL'} transport)",
                  device_s=float(t.item()), W1=r.distance, iters=[l.iters for l in r.levels],
                  level_s=[l.seconds for l in r.levels])
         comm.close()
         dist.destroy_process_group()
         return
     if nslabs:
-        r = w1mg.ml_slab_run(rhos, nslabs=nslabs, rel_tol=1e-5)
-        what = f"4096^2 cascade 64->4096, finest level in {nslabs} emulated slabs (1 GPU)"
+        for peer in (True, False):
+            w1mg.set_slab_transport(peer)
+            r = w1mg.ml_slab_run(rhos, nslabs=nslabs, rel_tol=1e-5)
+            what = (f"4096^2 cascade 64->4096, finest level in {nslabs} emulated slabs (1 GPU, "
+                    f"{'fused peer stores' if peer else 'device-copy halos'})")
+            line(config=5, what=what, device_s=r.total_seconds, W1=r.distance,
+                 iters=[l.iters for l in r.levels], level_s=[l.seconds for l in r.levels],
+                 finest_sweep_us=1e6 * r.levels[-1].seconds / max(r.levels[-1].iters, 1))
+        w1mg.set_slab_transport(True)
+        return
     else:
         w1mg.ml_run(rhos[:3], rel_tol=1e-5)  # warm the small levels' engines
         r = w1mg.ml_run(rhos, rel_tol=1e-5)
