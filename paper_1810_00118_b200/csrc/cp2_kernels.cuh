@@ -22,7 +22,8 @@
 // it, reproducing the reference's first-k stop exactly.
 #pragma once
 
-#include <cuda.h>  // CUtensorMap (type only; encoded through the runtime entry point)
+#include <cuda.h>
+#include <type_traits>  // CUtensorMap (type only; encoded through the runtime entry point)
 
 #include "cp_kernels.cuh"
 
@@ -204,7 +205,10 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
         double uyB = 0.0, dyB = 0.0;  // B's y-flux below the row it processes
 
         // One step of the march: sweep A at row rA0 + t, sweep B one row behind.
-        auto step = [&](const int t) {
+        // mode: 0 = decide at run time whether sweep B has a row (rB >= rA0),
+        // 1 = first step (no B row yet), 2 = a later step (B always runs).
+        auto step = [&](const int t, auto mode) {
+            constexpr int kMode = decltype(mode)::value;
             const int rA = rA0 + t;  // A row of this step (rA == n+1: virtual)
             const int rB = rA - 1;   // B row of this step
             double fA = 0.0, uxA = 0.0, uyAn = 0.0, dxA = 0.0, dyAn = 0.0, r = 0.0;
@@ -232,7 +236,7 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                     issue(st, rA + kStages);
                 }
                 // ---- sweep A at row rA
-                node_flux<PN>(hx, hy, pc, pr, pu, mxo, myo, mu, ih, uxA, uyAn, dxA, dyAn);
+                node_flux<PN, kTM && !kUnroll>(hx, hy, pc, pr, pu, mxo, myo, mu, ih, uxA, uyAn, dxA, dyAn);
                 const double uxl = __shfl_up_sync(0xffffffffu, uxA, 1);
                 const double dxl = __shfl_up_sync(0xffffffffu, dxA, 1);
                 const double divm = (uxA - uxl) * ih + (uyAn - uyA) * ih;
@@ -248,14 +252,14 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                 dyA = dyAn;
             }
             // ---- sweep B at row rB (inputs: A's rows rB and rB+1)
-            if (rB >= rA0) {
+            if (kMode == 2 || (kMode == 0 && rB >= rA0)) {
                 const bool hyB = kInt || (in && (rB < n));
                 const double pcB = fA_prev;
                 const double prB = __shfl_down_sync(0xffffffffu, fA_prev, 1);
                 const double puB = hyB ? fA : 0.0;
                 double ux, uy, dx, dy;
-                node_flux<PN>(hx, hyB, pcB, hx ? prB : 0.0, puB, mxA_prev, myA_prev, mu, ih, ux, uy,
-                              dx, dy);
+                node_flux<PN, kTM && !kUnroll>(hx, hyB, pcB, hx ? prB : 0.0, puB, mxA_prev, myA_prev, mu, ih,
+                                   ux, uy, dx, dy);
                 const double uxl = __shfl_up_sync(0xffffffffu, ux, 1);
                 const double dxl = __shfl_up_sync(0xffffffffu, dx, 1);
                 const double divm = (ux - uxl) * ih + (uy - uyB) * ih;
@@ -284,12 +288,16 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
         // window instead of copying it (~20 moves per step); measured 4-5 %
         // faster on batched 128..512 levels but 9 % slower on one 4096^2 grid
         // (80-register cap -> 3 spilled doubles), so it is a variant.
+        // (peeling the first step helps the rolled loop; the unrolled one
+        //  allocates registers better with the run-time test, measured)
         if constexpr (kUnroll) {
 #pragma unroll 2
-            for (int t = 0; t <= j1 - rA0; ++t, o += P) step(t);
+            for (int t = 0; t <= j1 - rA0; ++t, o += P) step(t, std::integral_constant<int, 0>{});
         } else {
+            step(0, std::integral_constant<int, 1>{});
+            o += P;
 #pragma unroll 1
-            for (int t = 0; t <= j1 - rA0; ++t, o += P) step(t);
+            for (int t = 1; t <= j1 - rA0; ++t, o += P) step(t, std::integral_constant<int, 2>{});
         }
     }
 }
