@@ -457,6 +457,7 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
 // not depend on the launch geometry (each pair's sweep and residual order are
 // fixed), so this only removes the early-exit blocks of stopped pairs.
 bool g_compact = true;
+int g_compact_step = 1 << 30;  // bucket granularity (W1MG_COMPACT_STEP; default: powers of two)
 
 Level compacted(const Level& lv, int pairs, int num_sms) {
     Level b = lv;
@@ -628,9 +629,13 @@ void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
             // pairs never restart, so B - done bounds the running count of
             // every later graph
             const int running = lv.B - done;
-            if (g_compact && lv.act && 2 * running <= span) {
-                int b = 1;
-                while (b < running) b <<= 1;
+            // bucket: running rounded up to a multiple of g_compact_step
+            // (powers of two below it); re-capture when the bucket shrinks
+            int b = 1;
+            while (b < running && b < g_compact_step) b <<= 1;
+            if (running > g_compact_step)
+                b = (running + g_compact_step - 1) / g_compact_step * g_compact_step;
+            if (g_compact && lv.act && b < span) {
                 span = b;
                 ex = sweep_graph(c, compacted(lv, span, c->num_sms), pn, K);
             }
@@ -819,6 +824,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
                                                             : kAuto;
         if (const char* v = std::getenv("W1MG_RESIDENT")) g_resident = std::atoi(v);
         if (const char* v = std::getenv("W1MG_COMPACT")) g_compact = std::atoi(v) != 0;
+        if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
             const int w = std::atoi(v);
             g_tmap_nw = (w == 2 || w == 8) ? w : kWarpsT;
