@@ -531,6 +531,10 @@ bool resident_ok(const Level& lv) {
 // more SMs (C >= 2); a one-CTA level (big batches, n <= 64) is faster on the
 // single-CTA engine, and n = 256 is faster streaming.  g_resident == 3 forces
 // the cluster engine wherever it fits (tests).
+// cluster-size rule (W1MG_CLUSTER_PICK): 1 = fewest node passes per phase
+// (default), 0 = powers of two with >= 8 rows per CTA
+int g_cluster_pick = 1;
+
 int cluster_size(const Level& lv, int num_sms) {
     if (lv.slab || lv.n > 256 || (g_resident != 1 && g_resident != 3)) return 0;
     int C = 0;
@@ -540,7 +544,25 @@ int cluster_size(const Level& lv, int num_sms) {
             break;
         }
     if (!C) return 0;
-    while (C * 2 <= 16 && (long)lv.B * C * 2 <= num_sms && (lv.n + 1) / (C * 2) >= 8) C *= 2;
+    if (g_cluster_pick == 1) {
+        // fewest node passes per phase: each CTA thread handles
+        // ceil(rows * (n+1) / threads) nodes one after another, and that
+        // serial chain (not the cluster barrier) dominates a sweep; ties go
+        // to the smaller cluster
+        long best = -1;
+        const int C0 = C;
+        for (int q = C0; q <= 16; ++q) {
+            if ((long)lv.B * q > num_sms || (lv.n + 1) / q < 2) break;
+            const long rows = (lv.n + 1 + q - 1) / q;
+            const long passes = (rows * (lv.n + 1) + kClusterThreads - 1) / kClusterThreads;
+            if (best < 0 || passes < best) {
+                best = passes;
+                C = q;
+            }
+        }
+    } else {
+        while (C * 2 <= 16 && (long)lv.B * C * 2 <= num_sms && (lv.n + 1) / (C * 2) >= 8) C *= 2;
+    }
     if (g_resident == 1 && (C == 1 || lv.n > 128)) return 0;
     return C;
 }
@@ -824,6 +846,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
                                                             : kAuto;
         if (const char* v = std::getenv("W1MG_RESIDENT")) g_resident = std::atoi(v);
         if (const char* v = std::getenv("W1MG_COMPACT")) g_compact = std::atoi(v) != 0;
+        if (const char* v = std::getenv("W1MG_CLUSTER_PICK")) g_cluster_pick = std::atoi(v);
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
             const int w = std::atoi(v);
