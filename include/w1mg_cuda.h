@@ -88,6 +88,12 @@ typedef struct w1mg_ml_params {
 } w1mg_ml_params;
 
 /* ---------------------------------------------------------------- context */
+/* A context owns one stream, its device buffers, cached CUDA graphs and the
+ * cuBLAS handle of one device.  It is not thread-safe: use one per host
+ * thread.  w1mg_ctx_create makes `device` current on the calling thread;
+ * later calls on the context expect that device to be current (one process
+ * or thread per GPU, the model of the multi-GPU paths).  The engine switches
+ * (w1mg_set_*) are process-wide. */
 int w1mg_ctx_create(int device, w1mg_ctx** out);
 void w1mg_ctx_destroy(w1mg_ctx* ctx);
 const char* w1mg_last_error(void);

@@ -510,11 +510,13 @@ void launch_grid_pn(w1mg_ctx* c, const Level& lv) {
 
 template <int PN>
 void launch_resident_pn(const Level& lv, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // per-device: attributes are per device
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!(attr >> (dev & 63) & 1ull)) {
         CK(cudaFuncSetAttribute(cp_resident_kernel<PN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kResidentMaxBytes));
-        attr = true;
+        attr |= 1ull << (dev & 63);
     }
     cp_resident_kernel<PN><<<lv.B, kResidentThreads, resident_bytes(lv.n), s>>>(lv.args);
 }
@@ -569,13 +571,15 @@ int cluster_size(const Level& lv, int num_sms) {
 
 template <int PN>
 bool launch_cluster_pn(const Level& lv, int C, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
+    static unsigned long long attr = 0;  // per device
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!(attr >> (dev & 63) & 1ull)) {
         CK(cudaFuncSetAttribute(cp_cluster_kernel<PN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(kClusterSmemBudget + 1024)));
         CK(cudaFuncSetAttribute(cp_cluster_kernel<PN>,
                                 cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
+        attr |= 1ull << (dev & 63);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(lv.B * C);
