@@ -285,6 +285,10 @@ int w1mg_set_resident_engine(int on);
  * the pairs still run, sweep grids span only the running pairs.  Also
  * W1MG_COMPACT=0|1. */
 int w1mg_set_tail_compaction(int on);
+/* Level-resident PDHG (one CTA per pair, all iterations of a level in one
+ * launch): 1 = for m = n+1 <= 33 (default), 2 = for m <= 65, 0 = off.  Also
+ * W1MG_PDHG_SMALL. */
+int w1mg_set_pdhg_small(int mode);
 /* Times the fused sweep kernel alone: `iters` sweeps over B pairs of an
  * n-cell level (synthetic source, stop rule off) after `warm` untimed ones;
  * writes the mean milliseconds per sweep launch (CUDA events). */

@@ -134,6 +134,7 @@ def lib():
         L.w1mg_set_sweep_engine.argtypes = [C.c_int]
         L.w1mg_set_resident_engine.argtypes = [C.c_int]
         L.w1mg_set_tail_compaction.argtypes = [C.c_int]
+        L.w1mg_set_pdhg_small.argtypes = [C.c_int]
         _lib = L
         return L
 

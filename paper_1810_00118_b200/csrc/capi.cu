@@ -183,6 +183,9 @@ void mirror_rho(w1mg_ctx* c, const Level& lv) {
                          cudaMemcpyDeviceToDevice, c->stream));
 }
 
+// strip-height target: enough strips for this many warps per SM (W1MG_WARPS_PER_SM)
+int g_warps_per_sm = 32;
+
 // warps per block of the tensor-map two-sweep kernel (W1MG_TMAP_NW = 2|4|8)
 int g_tmap_nw = kWarpsT;
 
@@ -204,7 +207,7 @@ void strip_geometry(SweepArgs& a, int own, long pairs, long target, int hmin) {
 }
 
 void set_geometry(Level& lv, int pairs, int num_sms) {
-    const long target = (long)num_sms * 32;
+    const long target = (long)num_sms * g_warps_per_sm;
     strip_geometry(lv.args, kOwn, pairs, target, 2);       // 31 owned columns per warp
     strip_geometry(lv.args2, kOwn2, pairs, target, 4);     // two-sweep: 29 per warp
     strip_geometry(lv.args2w, kOwnW, pairs, target / 2, 4);  // wide: 61 per warp, 4-warp blocks
@@ -533,6 +536,9 @@ bool resident_ok(const Level& lv) {
 // more SMs (C >= 2); a one-CTA level (big batches, n <= 64) is faster on the
 // single-CTA engine, and n = 256 is faster streaming.  g_resident == 3 forces
 // the cluster engine wherever it fits (tests).
+// PDHG levels with m = n+1 <= 65 run level-resident (pdhg_engine.cuh)
+int g_pdhg_small = 1;
+
 // cluster-size rule (W1MG_CLUSTER_PICK): 1 = fewest node passes per phase
 // (default), 0 = powers of two with >= 8 rows per CTA
 int g_cluster_pick = 1;
@@ -851,6 +857,8 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_RESIDENT")) g_resident = std::atoi(v);
         if (const char* v = std::getenv("W1MG_COMPACT")) g_compact = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_CLUSTER_PICK")) g_cluster_pick = std::atoi(v);
+        if (const char* v = std::getenv("W1MG_PDHG_SMALL")) g_pdhg_small = std::atoi(v);
+        if (const char* v = std::getenv("W1MG_WARPS_PER_SM")) g_warps_per_sm = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
             const int w = std::atoi(v);
@@ -1325,6 +1333,12 @@ int w1mg_set_sweep_engine(int engine) {
 
 int w1mg_set_resident_engine(int on) {
     g_resident = (on >= 0 && on <= 4) ? on : 1;
+    return W1MG_OK;
+}
+
+int w1mg_set_pdhg_small(int mode) {
+    if (mode < 0 || mode > 2) return W1MG_EINVAL;
+    g_pdhg_small = mode;
     return W1MG_OK;
 }
 

@@ -10,6 +10,7 @@
 #pragma once
 
 #include "pdhg_kernels.cuh"
+#include "pdhg_small.cuh"
 
 namespace {
 
@@ -178,10 +179,37 @@ void pdhg_iteration(w1mg_ctx* c, const PLevel& lv, int q) {
     CK(cudaGetLastError());
 }
 
+// small levels: one launch per level, one CTA per pair (pdhg_small.cuh);
+// W1MG_PDHG_SMALL = 1 (default, m <= 33), 2 (m <= 65), 0 (streaming only)
+// (g_pdhg_small, capi.cu)
+
+template <int Q>
+void launch_pdhg_small(w1mg_ctx* c, const PLevel& lv) {
+    static unsigned long long attr = 0;  // per device
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!(attr >> (dev & 63) & 1ull)) {
+        CK(cudaFuncSetAttribute(pdhg_small_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)pdhg_small_smem(kPdhgSmallMaxM)));
+        attr |= 1ull << (dev & 63);
+    }
+    pdhg_small_kernel<Q><<<lv.B, kPdhgSmallThreads, pdhg_small_smem(lv.n + 1), c->stream>>>(
+        lv.args, lv.C, lv.S, lv.lam);
+    CK(cudaGetLastError());
+    ++c->launches;
+}
+
 // Iterate until every pair's stop flag is set (graph of K iterations, host
 // watches the done counter one graph behind, like run_sweeps).
 void run_pdhg_iters(w1mg_ctx* c, const PLevel& lv, int q, long max_iters) {
     if (max_iters <= 0) return;
+    if ((g_pdhg_small == 1 && lv.n + 1 <= kPdhgSmallAutoM) ||
+        (g_pdhg_small == 2 && lv.n + 1 <= kPdhgSmallMaxM)) {
+        if (q == 0) launch_pdhg_small<0>(c, lv);
+        else if (q == 1) launch_pdhg_small<1>(c, lv);
+        else launch_pdhg_small<2>(c, lv);
+        return;
+    }
     constexpr int K = 8;
     if (max_iters < K) {
         for (long k = 0; k < max_iters; ++k) pdhg_iteration(c, lv, q);

@@ -62,9 +62,18 @@ def test_project_affine(n):
     assert _rel(again.x_edges, out.x_edges) <= 1e-10
 
 
+@pytest.fixture(params=[0, 2], ids=["streaming", "resident"])
+def pdhg_engine(request):
+    from paper_1810_00118_b200 import _lib
+
+    _lib.lib().w1mg_set_pdhg_small(request.param)
+    yield request.param
+    _lib.lib().w1mg_set_pdhg_small(1)
+
+
+@pytest.mark.parametrize("n", [32, 64])
 @pytest.mark.parametrize("p", [0, 1, 2])
-def test_pdhg_fixed_iterations(p):
-    n = 32
+def test_pdhg_fixed_iterations(p, n, pdhg_engine):
     rho = instances.config1_source(n)
     prm = w1mg.SolverParams(p=w1mg.PNorm(p), tolerance=-1.0, max_iters=200)
     rep = w1mg.pdhg_run(_src(rho), prm)
@@ -118,7 +127,7 @@ def test_recover_potential_inverts_adjoint():
     assert np.linalg.norm(phi.values - (psi - psi.mean())) <= 1e-9
 
 
-def test_config3_cascade_matches_oracle():
+def test_config3_cascade_matches_oracle(pdhg_engine):
     """BASELINE.json configs[2] at reduced size (cascade 32->128 from a 128^2
     blurred-noise image pair), rel tol 1e-5 per level."""
     from oracle import Oracle
