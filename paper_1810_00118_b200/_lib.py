@@ -13,7 +13,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "lib")
-CUDA_SO = os.path.join(LIB_DIR, "libw1mg_cuda.so")
+# W1MG_CUDA_SO: load another build of the library (engine A/B experiments)
+CUDA_SO = os.environ.get("W1MG_CUDA_SO") or os.path.join(LIB_DIR, "libw1mg_cuda.so")
 API_SO = os.path.join(LIB_DIR, "libw1mg.so")
 
 W1MG_OK, W1MG_EINVAL, W1MG_ELOGIC, W1MG_ECUDA, W1MG_ENOMEM, W1MG_ENONFINITE = range(6)
