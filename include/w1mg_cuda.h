@@ -289,6 +289,14 @@ int w1mg_set_tail_compaction(int on);
  * launch): 1 = for m = n+1 <= 33 (default), 2 = for m <= 65, 0 = off.  Also
  * W1MG_PDHG_SMALL. */
 int w1mg_set_pdhg_small(int mode);
+/* Engine tuning switches by name (process-wide; each also has a W1MG_<NAME>
+ * environment variable read at context creation): "pdhg_fold" (folded DCTs
+ * in PDHG iterations: 1 = odd m >= 400 (default), 2 = every odd m, 0 = off),
+ * "pdhg_small" (0-2),
+ * "cluster_pick" (0/1), "compact" (0/1), "compact_step" (>= 1),
+ * "warps_per_sm" (strip target, default 32), "tmap_nw" (2/4/8).
+ * W1MG_EINVAL for an unknown name or value. */
+int w1mg_set_option(const char* name, long value);
 /* Times the fused sweep kernel alone: `iters` sweeps over B pairs of an
  * n-cell level (synthetic source, stop rule off) after `warm` untimed ones;
  * writes the mean milliseconds per sweep launch (CUDA events). */

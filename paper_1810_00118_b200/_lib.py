@@ -136,6 +136,7 @@ def lib():
         L.w1mg_set_resident_engine.argtypes = [C.c_int]
         L.w1mg_set_tail_compaction.argtypes = [C.c_int]
         L.w1mg_set_pdhg_small.argtypes = [C.c_int]
+        L.w1mg_set_option.argtypes = [C.c_char_p, C.c_long]
         _lib = L
         return L
 

@@ -538,6 +538,9 @@ bool resident_ok(const Level& lv) {
 // the cluster engine wherever it fits (tests).
 // PDHG levels with m = n+1 <= 65 run level-resident (pdhg_engine.cuh)
 int g_pdhg_small = 1;
+// PDHG iterations with symmetry-folded DCTs (pdhg_fold.cuh): 1 = auto (odd
+// m >= kFoldMinM), 2 = every odd m, 0 = dense sandwich only
+int g_pdhg_fold = 1;
 
 // cluster-size rule (W1MG_CLUSTER_PICK): 1 = fewest node passes per phase
 // (default), 0 = powers of two with >= 8 rows per CTA
@@ -858,6 +861,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_COMPACT")) g_compact = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_CLUSTER_PICK")) g_cluster_pick = std::atoi(v);
         if (const char* v = std::getenv("W1MG_PDHG_SMALL")) g_pdhg_small = std::atoi(v);
+        if (const char* v = std::getenv("W1MG_PDHG_FOLD")) g_pdhg_fold = std::atoi(v);
         if (const char* v = std::getenv("W1MG_WARPS_PER_SM")) g_warps_per_sm = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
@@ -1333,6 +1337,21 @@ int w1mg_set_sweep_engine(int engine) {
 
 int w1mg_set_resident_engine(int on) {
     g_resident = (on >= 0 && on <= 4) ? on : 1;
+    return W1MG_OK;
+}
+
+int w1mg_set_option(const char* name, long value) {
+    if (!name) return W1MG_EINVAL;
+    const std::string k(name);
+    const int v = (int)value;
+    if (k == "pdhg_fold" && v >= 0 && v <= 2) g_pdhg_fold = v;
+    else if (k == "pdhg_small" && v >= 0 && v <= 2) g_pdhg_small = v;
+    else if (k == "cluster_pick" && (v == 0 || v == 1)) g_cluster_pick = v;
+    else if (k == "compact") g_compact = v != 0;
+    else if (k == "compact_step" && v >= 1) g_compact_step = v;
+    else if (k == "warps_per_sm" && v >= 1) g_warps_per_sm = v;
+    else if (k == "tmap_nw" && (v == 2 || v == 4 || v == 8)) g_tmap_nw = v;
+    else return W1MG_EINVAL;
     return W1MG_OK;
 }
 

@@ -11,6 +11,7 @@
 
 #include "pdhg_kernels.cuh"
 #include "pdhg_small.cuh"
+#include "pdhg_fold.cuh"
 
 namespace {
 
@@ -46,7 +47,49 @@ struct PLevel {
     const double* C = nullptr;    // DCT-II matrix, m x m column-major: C(k, j) = 2 cos(pi (2j+1) k / 2m)
     const double* S = nullptr;    // DCT-III matrix: S(k, j) = j ? 2 cos(pi j (2k+1) / 2m) : 1
     const double* lam = nullptr;  // lambda_k, poisson.cpp:28-30
+    // symmetry-folded DCTs for the PDHG iteration (pdhg_fold.cuh), odd m >= kFoldMinM
+    bool fold = false;
+    FoldGeom fg{};
+    const double* const* gp = nullptr;  // device pointer arrays [4 stages][A,B,C][4B]
 };
+
+// folded DCT in the PDHG iteration from this m on (W1MG_PDHG_FOLD=0 disables).
+// Measured per level of config 3 (one pair): 513^2 176 vs 202 ms (folded vs
+// dense), 257^2 143 vs 128 ms, 129^2 157 vs 130 ms -- the batched half-size
+// GEMMs only win once the dense ones are large.
+constexpr int kFoldMinM = 400;
+
+// Folded DCT operators (h x h, ld h, zero padded): C_e, C_o, S_e, S_o.
+const double* fold_operators(w1mg_ctx* c, int n) {
+    const int m = n + 1, h = (m + 1) / 2, ho = h - 1;
+    const std::string key = "dctf." + std::to_string(m);
+    const bool fresh = c->bufs.find(key) == c->bufs.end();
+    double* d = c->get<double>(key, (size_t)4 * h * h);
+    if (fresh) {
+        std::vector<double> M((size_t)4 * h * h, 0.0);
+        const long double pi = 3.141592653589793238462643383279502884L;
+        auto Cf = [&](long k, long l) {  // C(k, l) = 2 cos(pi (2l+1) k / 2m)
+            return (double)(2.0L * cosl(pi * (((2 * l + 1) * k) % (4L * m)) / (2.0L * m)));
+        };
+        auto Sf = [&](long k, long j) {  // S(k, j) = j ? 2 cos(pi j (2k+1) / 2m) : 1
+            return j == 0 ? 1.0 : (double)(2.0L * cosl(pi * ((j * (2 * k + 1)) % (4L * m)) / (2.0L * m)));
+        };
+        double* Ce = M.data();
+        double* Co = Ce + (size_t)h * h;
+        double* Se = Co + (size_t)h * h;
+        double* So = Se + (size_t)h * h;
+        for (int col = 0; col < h; ++col)
+            for (int row = 0; row < h; ++row) {
+                const size_t e = (size_t)col * h + row;
+                Ce[e] = Cf(2L * row, col);
+                if (row < ho && col < ho) Co[e] = Cf(2L * row + 1, col);
+                Se[e] = Sf(row, 2L * col);
+                if (row < ho && col < ho) So[e] = Sf(row, 2L * col + 1);
+            }
+        CK(cudaMemcpy(d, M.data(), M.size() * 8, cudaMemcpyHostToDevice));
+    }
+    return d;
+}
 
 // DCT operators for m = n+1, built once per size on the host in long double
 // and cached on the device.
@@ -106,6 +149,36 @@ PLevel make_plevel(w1mg_ctx* c, const std::string& tag, int n, int B, double mu,
     a.ndone = lv.ndone;
     a.partial = c->get<double>(tag + ".partial", (size_t)B * lv.grid.x * lv.grid.y * 3);
     dct_operators(c, n, &lv.C, &lv.S, &lv.lam);
+    const int m = n + 1;
+    if ((m & 1) && m >= 3 && (g_pdhg_fold == 2 || (g_pdhg_fold == 1 && m >= kFoldMinM))) {
+        lv.fold = true;
+        lv.fg.h = (m + 1) / 2;
+        lv.fg.lq = lv.L.pitch / 2;
+        const int h = lv.fg.h;
+        const double* ops = fold_operators(c, n);
+        const double* Cm[2] = {ops, ops + (size_t)h * h};
+        const double* Sm[2] = {ops + 2 * (size_t)h * h, ops + 3 * (size_t)h * h};
+        // stage s, array t (A, B, C), entry e = 4 b + q
+        std::vector<const double*> P((size_t)12 * 4 * B);
+        auto at = [&](int st, int t, int e) -> const double*& { return P[((size_t)st * 3 + t) * 4 * B + e]; };
+        for (int b = 0; b < B; ++b)
+            for (int q = 0; q < 4; ++q) {
+                const int e = 4 * b + q, qa = q >> 1, qb = q & 1;
+                auto quad = [&](int slot) {
+                    return lv.base + ((long)b * P_NSLOT + slot) * lv.L.plane + lv.L.at(0, 0) +
+                           (long)q * h * lv.fg.lq;
+                };
+                at(0, 0, e) = Cm[qa]; at(0, 1, e) = quad(P_RES); at(0, 2, e) = quad(P_T);
+                at(1, 0, e) = quad(P_T); at(1, 1, e) = Cm[qb]; at(1, 2, e) = quad(P_RES);
+                at(2, 0, e) = Sm[qa]; at(2, 1, e) = quad(P_RES); at(2, 2, e) = quad(P_T);
+                at(3, 0, e) = quad(P_T); at(3, 1, e) = Sm[qb]; at(3, 2, e) = quad(P_PSI);
+            }
+        const double** dp = c->get<const double*>(tag + ".foldptr", P.size());
+        CK(cudaMemcpyAsync(dp, P.data(), P.size() * sizeof(void*), cudaMemcpyHostToDevice,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));  // host vector dies here
+        lv.gp = dp;
+    }
     CK(cudaMemsetAsync(lv.ticket, 0, sizeof(unsigned) * B, c->stream));
     return lv;
 }
@@ -167,7 +240,46 @@ void remove_mean(w1mg_ctx* c, const PLevel& lv, int slot) {
     CK(cudaGetLastError());
 }
 
+// The iteration with folded DCTs: pre (folding), 4 batched GEMM stages over
+// the (pair, quadrant) products with the divide after stage 2, post.
+void pdhg_iteration_fold(w1mg_ctx* c, const PLevel& lv, int q) {
+    const FoldGeom g = lv.fg;
+    const int h = g.h, nb = 4 * lv.B;
+    const dim3 fblk(32, 8);
+    pdhg_pre_fold_kernel<<<dim3((h + 31) / 32, (h + 7) / 8, lv.B), fblk, 0, c->stream>>>(lv.args, g);
+    CK(cudaGetLastError());
+    cublasHandle_t hb = blas(c);
+    const double one = 1.0, zero = 0.0;
+    const int m = lv.n + 1;
+    const double scale = 1.0 / (4.0 * double(m) * double(m));  // poisson.cpp:93
+    auto arr = [&](int st, int t) { return lv.gp + ((size_t)st * 3 + t) * nb; };
+    auto gemm = [&](int st, cublasOperation_t tb, const double* alpha, int lda, int ldb) {
+        blas_check(cublasDgemmBatched(hb, CUBLAS_OP_N, tb, h, h, h, alpha, arr(st, 0), lda,
+                                      arr(st, 1), ldb, &zero,
+                                      const_cast<double* const*>(arr(st, 2)), g.lq, nb),
+                   "dgemm batched");
+    };
+    gemm(0, CUBLAS_OP_N, &one, h, g.lq);     // T = C_a X
+    gemm(1, CUBLAS_OP_T, &one, g.lq, h);     // X = T C_b^T
+    spectral_divide_fold_kernel<<<dim3((h + 31) / 32, (h + 7) / 8, nb), fblk, 0, c->stream>>>(
+        lv.args, g, lv.lam);
+    CK(cudaGetLastError());
+    gemm(2, CUBLAS_OP_N, &one, h, g.lq);     // T = S_a Y
+    gemm(3, CUBLAS_OP_T, &scale, g.lq, h);   // P = T S_b^T / (4 m^2)
+    switch (q) {
+        case 0: pdhg_post_fold_kernel<0><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args, g); break;
+        case 1: pdhg_post_fold_kernel<1><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args, g); break;
+        default: pdhg_post_fold_kernel<2><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args, g); break;
+    }
+    CK(cudaGetLastError());
+    c->launches += 7;
+}
+
 void pdhg_iteration(w1mg_ctx* c, const PLevel& lv, int q) {
+    if (lv.fold) {
+        pdhg_iteration_fold(c, lv, q);
+        return;
+    }
     pdhg_pre_kernel<<<lv.grid, lv.blk, 0, c->stream>>>(lv.args);
     poisson_apply(c, lv, P_RES, true);
     switch (q) {
@@ -216,7 +328,7 @@ void run_pdhg_iters(w1mg_ctx* c, const PLevel& lv, int q, long max_iters) {
         return;
     }
     std::string key(reinterpret_cast<const char*>(&lv.args), sizeof(SweepArgs));
-    key += "pdhg:" + std::to_string(q) + ":" + std::to_string(lv.B);
+    key += "pdhg:" + std::to_string(q) + ":" + std::to_string(lv.B) + (lv.fold ? ":fold" : ":dense");
     cudaGraphExec_t ex;
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) {

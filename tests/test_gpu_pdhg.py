@@ -62,16 +62,22 @@ def test_project_affine(n):
     assert _rel(again.x_edges, out.x_edges) <= 1e-10
 
 
-@pytest.fixture(params=[0, 2], ids=["streaming", "resident"])
+@pytest.fixture(params=["streaming", "resident", "streaming-folded"])
 def pdhg_engine(request):
+    """streaming: 7-launch iteration with the dense DCT sandwich; resident:
+    one CTA per pair for m <= 65; streaming-folded: symmetry-folded DCTs
+    (forced on every odd m; auto uses them from m >= 400)."""
     from paper_1810_00118_b200 import _lib
 
-    _lib.lib().w1mg_set_pdhg_small(request.param)
+    L = _lib.lib()
+    L.w1mg_set_pdhg_small(2 if request.param == "resident" else 0)
+    L.w1mg_set_option(b"pdhg_fold", 2 if request.param == "streaming-folded" else 0)
     yield request.param
-    _lib.lib().w1mg_set_pdhg_small(1)
+    L.w1mg_set_pdhg_small(1)
+    L.w1mg_set_option(b"pdhg_fold", 1)
 
 
-@pytest.mark.parametrize("n", [32, 64])
+@pytest.mark.parametrize("n", [32, 64, 128, 256])
 @pytest.mark.parametrize("p", [0, 1, 2])
 def test_pdhg_fixed_iterations(p, n, pdhg_engine):
     rho = instances.config1_source(n)
