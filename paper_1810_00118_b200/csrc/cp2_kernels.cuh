@@ -338,7 +338,7 @@ cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
 
 // Same march, ring fed by one tensor-map box per row.  `tm` views the level
 // buffer as (column, row, plane) with plane = pair * NSLOT + slot, box
-// {kChunk, 1, 8} at plane stride 2 (capi.cu: make_level_tmap).  NW warps per
+// {kChunk, 1, 8} at plane stride 2 (level_engine.cuh: make_level_tmap).  NW warps per
 // block: small blocks let an SM refill as soon as a few strips finish.
 constexpr int kWarpsT = 4;
 constexpr int tmap_smem(int nw) { return nw * (kStages * kStageBytes + kStages * 8); }

@@ -293,7 +293,7 @@ void pdhg_iteration(w1mg_ctx* c, const PLevel& lv, int q) {
 
 // small levels: one launch per level, one CTA per pair (pdhg_small.cuh);
 // W1MG_PDHG_SMALL = 1 (default, m <= 33), 2 (m <= 65), 0 (streaming only)
-// (g_pdhg_small, capi.cu)
+// (g_pdhg_small, level_engine.cuh)
 
 template <int Q>
 void launch_pdhg_small(w1mg_ctx* c, const PLevel& lv) {
