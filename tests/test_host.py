@@ -66,6 +66,24 @@ def test_step_sizes_and_schedule_host():
     assert w1mg.default_levels(512) == 6
 
 
+def test_engine_switches_validate_host():
+    """Engine switches are host-only state: unknown names / values are
+    W1MG_EINVAL, valid ones OK (defaults restored)."""
+    from paper_1810_00118_b200 import _lib
+
+    L = _lib.lib()
+    assert L.w1mg_set_option(b"no_such_option", 1) == _lib.W1MG_EINVAL
+    assert L.w1mg_set_option(b"tmap_nw", 3) == _lib.W1MG_EINVAL
+    assert L.w1mg_set_option(b"pdhg_fold", 7) == _lib.W1MG_EINVAL
+    assert L.w1mg_set_option(None, 1) == _lib.W1MG_EINVAL
+    for name, val in ((b"tmap_nw", 4), (b"pdhg_fold", 1), (b"compact", 1), (b"cluster_pick", 1)):
+        assert L.w1mg_set_option(name, val) == _lib.W1MG_OK
+    assert L.w1mg_set_sweep_engine(6) == _lib.W1MG_EINVAL
+    assert L.w1mg_set_sweep_engine(3) == _lib.W1MG_OK
+    assert L.w1mg_set_pdhg_small(3) == _lib.W1MG_EINVAL
+    assert L.w1mg_set_pdhg_small(1) == _lib.W1MG_OK
+
+
 def test_source_gate_host():
     from paper_1810_00118_b200 import w1mg
     from paper_1810_00118_b200 import instances
