@@ -31,8 +31,46 @@ namespace w1mg_dev {
 
 constexpr int kOwn2 = 29;  // owned columns per warp in the two-sweep march
 
+// Block-wide sum of `count` 6-vectors at src (fixed order: thread-strided,
+// warp butterfly, then warps in order); the result is valid in thread 0.
+template <int NW>
+__device__ __forceinline__ void block_sum6(const double* src, int count, double (*red)[6],
+                                           double* s) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    double t[6] = {0, 0, 0, 0, 0, 0};
+    for (int b = threadIdx.x; b < count; b += blockDim.x) {
+        const volatile double* pv = src + b * 6;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) t[q] += pv[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) t[q] = warp_sum(t[q]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 6; ++q) red[warp][q] = t[q];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < 6; ++q) s[q] = 0.0;
+        for (int w = 0; w < NW; ++w)
+#pragma unroll
+            for (int q = 0; q < 6; ++q) s[q] += red[w][q];
+    }
+}
+
 // Reduction of both sweeps' residual sums (6 per block) and the two-sweep
-// stop rule; partial holds [pairs][blocks][6].
+// stop rule; partial holds [pairs][blocks][6].  With a.gpart set and more
+// than kRedTwoLevelMin blocks per pair the reduction is two-level: the last block
+// of each group of kRedGroup blocks sums the group, and the last group
+// finisher sums the groups -- a short serial tail when one pair spans
+// hundreds of blocks (one-pair levels), same fixed order every launch.
+constexpr int kRedGroup = 32;
+// two-level only for very wide launches: measured 129 -> 126.5 us per sweep
+// on one 4096^2 grid (2308 blocks), slower on one 256^2 grid (147 blocks)
+constexpr int kRedTwoLevelMin = 512;
+
 template <int NW = kSweepWarps>  // warps per block
 __device__ __forceinline__ void finish_sweep2(const SweepArgs& a, int pair, int parity,
                                               double a0, double a1, double a2, double b0,
@@ -49,6 +87,9 @@ __device__ __forceinline__ void finish_sweep2(const SweepArgs& a, int pair, int 
         for (int q = 0; q < 6; ++q) red[warp][q] = v[q];
     __syncthreads();
     const int nblk = gridDim.x;
+    const bool two = a.gpart && nblk > kRedTwoLevelMin;
+    const int ngrp = (nblk + kRedGroup - 1) / kRedGroup;
+    const int grp = blockIdx.x / kRedGroup;
     double* part = a.partial + (long)pair * nblk * 6;
     if (threadIdx.x == 0) {
         double t[6] = {0, 0, 0, 0, 0, 0};
@@ -58,30 +99,40 @@ __device__ __forceinline__ void finish_sweep2(const SweepArgs& a, int pair, int 
 #pragma unroll
         for (int q = 0; q < 6; ++q) part[blockIdx.x * 6 + q] = t[q];
         __threadfence();
-        unsigned tk = atomicAdd(a.ticket + pair, 1u);
-        is_last = (tk == (unsigned)nblk - 1);
+        if (two) {
+            const unsigned gsize = (unsigned)min(kRedGroup, nblk - grp * kRedGroup);
+            const unsigned tg = atomicAdd(a.gticket + (long)pair * a.gstride + grp, 1u);
+            is_last = (tg == gsize - 1);
+        } else {
+            const unsigned tk = atomicAdd(a.ticket + pair, 1u);
+            is_last = (tk == (unsigned)nblk - 1);
+        }
     }
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    double t[6] = {0, 0, 0, 0, 0, 0};
-    for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
-        const volatile double* pv = part + b * 6;
+    double s[6];
+    if (two) {
+        // group finisher: sum this group's blocks, post, count the group
+        const int b0_ = grp * kRedGroup;
+        block_sum6<NW>(part + b0_ * 6, min(kRedGroup, nblk - b0_), red, s);
+        double* gp = a.gpart + ((long)pair * a.gstride) * 6;
+        if (threadIdx.x == 0) {
 #pragma unroll
-        for (int q = 0; q < 6; ++q) t[q] += pv[q];
+            for (int q = 0; q < 6; ++q) gp[grp * 6 + q] = s[q];
+            a.gticket[(long)pair * a.gstride + grp] = 0u;
+            __threadfence();
+            const unsigned tk = atomicAdd(a.ticket + pair, 1u);
+            is_last = (tk == (unsigned)ngrp - 1);
+        }
+        __syncthreads();
+        if (!is_last) return;
+        __threadfence();
+        block_sum6<NW>(gp, ngrp, red, s);
+    } else {
+        block_sum6<NW>(part, nblk, red, s);
     }
-#pragma unroll
-    for (int q = 0; q < 6; ++q) t[q] = warp_sum(t[q]);
-    __syncthreads();
-    if (lane == 0)
-#pragma unroll
-        for (int q = 0; q < 6; ++q) red[warp][q] = t[q];
-    __syncthreads();
     if (threadIdx.x != 0) return;
-    double s[6] = {0, 0, 0, 0, 0, 0};
-    for (int w = 0; w < NW; ++w)
-#pragma unroll
-        for (int q = 0; q < 6; ++q) s[q] += red[w][q];
     PairCtl* ctl = a.ctl + pair;
     const double fA = a.h2 * (s[0] / a.mu + s[1] / a.tau - 2.0 * s[2]);
     const double fB = a.h2 * (s[3] / a.mu + s[4] / a.tau - 2.0 * s[5]);

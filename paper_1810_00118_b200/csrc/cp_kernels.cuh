@@ -91,6 +91,11 @@ struct SweepArgs {
     unsigned long long* const* arrive;  // [pworld] arrival counters
     int prank, pworld;
     int psys;  // peers on other GPUs: system-scope fences/atomics (0: same device)
+    // two-level residual reduction of the two-sweep kernels (finish_sweep2):
+    // group partials [pairs][gstride][6] and group tickets [pairs][gstride]
+    double* gpart;
+    unsigned* gticket;
+    int gstride;
 };
 
 // Pair of this block.  In a compacted launch (the tail of a batched level, see

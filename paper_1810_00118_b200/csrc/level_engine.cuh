@@ -159,6 +159,17 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     a.partial = lv.partial;
     lv.args2.partial = lv.partial;
     lv.args2w.partial = lv.partial;
+    if (!lv.slab) {  // two-level residual reduction of the two-sweep kernels
+        const int gs = (one.args2.ntiles + kRedGroup - 1) / kRedGroup + 1;
+        double* gp = c->get<double>(tag + ".gpart", (size_t)B * gs * 6);
+        unsigned* gt = c->get<unsigned>(tag + ".gticket", (size_t)B * gs);
+        CK(cudaMemsetAsync(gt, 0, sizeof(unsigned) * B * gs, c->stream));
+        for (SweepArgs* x : {&lv.args2, &lv.args2w}) {
+            x->gpart = gp;
+            x->gticket = gt;
+            x->gstride = gs;
+        }
+    }
     if (B > 1 && !lv.slab) {
         lv.act = c->get<int>(tag + ".act", B);
         lv.nact = c->get<int>(tag + ".nact", 1);
