@@ -70,6 +70,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_PDHG_SMALL")) g_pdhg_small = std::atoi(v);
         if (const char* v = std::getenv("W1MG_PDHG_FOLD")) g_pdhg_fold = std::atoi(v);
         if (const char* v = std::getenv("W1MG_WARPS_PER_SM")) g_warps_per_sm = std::max(1, std::atoi(v));
+        if (const char* v = std::getenv("W1MG_PDL")) g_pdl = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
             const int w = std::atoi(v);
@@ -557,6 +558,7 @@ int w1mg_set_option(const char* name, long value) {
     else if (k == "compact") g_compact = v != 0;
     else if (k == "compact_step" && v >= 1) g_compact_step = v;
     else if (k == "warps_per_sm" && v >= 1) g_warps_per_sm = v;
+    else if (k == "pdl" && (v == 0 || v == 1)) g_pdl = v;
     else if (k == "tmap_nw" && (v == 2 || v == 4 || v == 8)) g_tmap_nw = v;
     else return W1MG_EINVAL;
     return W1MG_OK;

@@ -396,7 +396,13 @@ constexpr int tmap_smem(int nw) { return nw * (kStages * kStageBytes + kStages *
 
 template <int PN, int NW, bool kUnroll>
 __global__ void __launch_bounds__(NW * 32, 24 / NW)
-cp_sweep2_tmap_kernel(const SweepArgs a, const int parity, const __grid_constant__ CUtensorMap tm) {
+cp_sweep2_tmap_kernel(const SweepArgs a, const int parity, const __grid_constant__ CUtensorMap tm,
+                      const int pdl_early) {
+    // programmatic dependent launch: everything below reads what the
+    // previous sweep wrote, so wait for it first (a no-op without PDL); a
+    // grid that fits in one wave lets the next launch start right away
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (pdl_early) asm volatile("griddepcontrol.launch_dependents;");
     const int pair = sweep_pair(a);
     if (pair < 0 || *(volatile int*)&a.ctl[pair].done) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
