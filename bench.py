@@ -460,6 +460,7 @@ def main():
 
     # ---- single-pair time-to-converged-W1 at 512^2 (device-resident input)
     t_single = None
+    t_single_e2e = None
     if rank == 0:
         one = [None]
 
@@ -480,6 +481,29 @@ def main():
             ts.append(time.perf_counter() - t0)
         t_single = min(ts)
         one[0] = float(dist_d[0].item())
+        # the same through the host API: H2D of the two 512^2 images, the
+        # cascade, D2H of W1 / dual / sweeps (SURVEY 8d "end-to-end time")
+        ha = img0[:1].cpu().numpy()
+        hb = img1[:1].cpu().numpy()
+        dp_ = C.POINTER(C.c_double)
+        hd = np.zeros(1)
+        hu = np.zeros(1)
+        hi = np.zeros((1, LEVELS), dtype=np.int64)
+        hc = np.zeros(1, dtype=np.int32)
+
+        def single_host():
+            check(L.w1mg_ml_cp_batch(ctx.h, 1, M, ha.ctypes.data_as(dp_), hb.ctypes.data_as(dp_),
+                                     C.byref(prm), hd.ctypes.data_as(dp_), hu.ctypes.data_as(dp_),
+                                     hi.ctypes.data_as(C.POINTER(C.c_long)),
+                                     hc.ctypes.data_as(C.POINTER(C.c_int))))
+
+        single_host()
+        te2e = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            single_host()
+            te2e.append(time.perf_counter() - t0)
+        t_single_e2e = min(te2e)
 
     # ---- CPU baseline + per-pair parity sample (rank 0, N = 1 only)
     cpu = None
@@ -508,6 +532,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(args, args.pairs * world),
             "pairs_per_s": pairs_per_s, "time_to_w1_512_s": t_single,
+            "time_to_w1_512_e2e_s": t_single_e2e,
             "levels": [{"n": n, "seconds_per_step": s_ / args.steps,
                         "cell_updates_per_s": c_ / s_}
                        for n, s_, c_ in zip(level_sizes(), lev_s, lev_cu)],
