@@ -303,6 +303,13 @@ int w1mg_set_option(const char* name, long value);
 int w1mg_sweep_probe(w1mg_ctx* ctx, int n, int B, int pnorm, long warm, long iters,
                      double* ms_per_sweep);
 
+/* Diagnostics: compares the kernels' branch-free sqrt / division / p = 2
+ * shrink (restated fast paths, device_common.cuh) with the library operators
+ * on `count` random and edge-case operands scaled around mu; bad[0..2] =
+ * mismatching sqrt, division, shrink results (0 expected). */
+int w1mg_rn_selftest(w1mg_ctx* ctx, long count, unsigned long long seed, double mu,
+                     unsigned long long* bad);
+
 #ifdef __cplusplus
 }
 #endif

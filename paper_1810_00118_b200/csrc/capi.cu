@@ -34,6 +34,7 @@
 #include "cluster_kernels.cuh"
 #include "cp2w_kernels.cuh"
 #include "grid_kernels.cuh"
+#include "tile_kernels.cuh"
 
 using namespace w1mg_dev;
 
@@ -71,6 +72,10 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_PDHG_FOLD")) g_pdhg_fold = std::atoi(v);
         if (const char* v = std::getenv("W1MG_WARPS_PER_SM")) g_warps_per_sm = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_PDL")) g_pdl = std::atoi(v) != 0;
+        if (const char* v = std::getenv("W1MG_TILE")) g_tile = std::atoi(v);
+        if (const char* v = std::getenv("W1MG_TILE_MIN")) g_tile_min = std::max(1, std::atoi(v));
+        if (const char* v = std::getenv("W1MG_TILE_MAX")) g_tile_max = std::max(1, std::atoi(v));
+        if (const char* v = std::getenv("W1MG_TILE_GRID")) g_tile_grid = std::max(0, std::atoi(v));
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
             const int w = std::atoi(v);
@@ -560,6 +565,10 @@ int w1mg_set_option(const char* name, long value) {
     else if (k == "warps_per_sm" && v >= 1) g_warps_per_sm = v;
     else if (k == "pdl" && (v == 0 || v == 1)) g_pdl = v;
     else if (k == "tmap_nw" && (v == 2 || v == 4 || v == 8)) g_tmap_nw = v;
+    else if (k == "tile" && v >= 0 && v <= 2) g_tile = v;
+    else if (k == "tile_min" && v >= 1) g_tile_min = v;
+    else if (k == "tile_max" && v >= 1) g_tile_max = v;
+    else if (k == "tile_grid" && v >= 0) g_tile_grid = v;
     else return W1MG_EINVAL;
     return W1MG_OK;
 }
@@ -573,6 +582,20 @@ int w1mg_set_pdhg_small(int mode) {
 int w1mg_set_tail_compaction(int on) {
     g_compact = on != 0;
     return W1MG_OK;
+}
+
+int w1mg_rn_selftest(w1mg_ctx* c, long count, unsigned long long seed, double mu,
+                     unsigned long long* bad) {
+    return guard([&] {
+        if (count < 0 || !(mu > 0.0)) fail(W1MG_EINVAL, "rn_selftest: bad arguments");
+        auto* d = c->get<unsigned long long>("selftest.bad", 3);
+        CK(cudaMemsetAsync(d, 0, 3 * sizeof(unsigned long long), c->stream));
+        rn_selftest_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(count, seed, mu, d);
+        ++c->launches;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(bad, d, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
 }
 
 int w1mg_sweep_probe(w1mg_ctx* c, int n, int B, int pnorm, long warm, long iters,

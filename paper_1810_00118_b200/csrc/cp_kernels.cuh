@@ -117,21 +117,17 @@ constexpr int kTmaSmem = kSweepWarps * (kStages * kStageBytes + kStages * 8);
 
 // One node of the m-update: returns the new flux and its increment, zero for
 // absent components (solver_cp.cpp:39-54; absent components enter shrink as 0).
-// kNB: branch-free p = 2 shrink (the division always runs, on mu when the
-// result is zero; selects give exactly the reference's +0.0) -- no
-// divergent region per node; used by the two-sweep march.
-template <int PN, bool kNB = false>
+// kNB: branch-free p = 2 shrink (shrink2_nb: the restated fast paths of
+// sqrt and division plus selects, bit-identical to shrink<1>) -- no
+// divergent region per node, so the scheduler can interleave nodes.
+template <int PN, bool kNB = true>
 __device__ __forceinline__ void node_flux(bool hx, bool hy, double pc, double pr, double pu,
                                           double mxo, double myo, double mu, double ih,
                                           double& ux, double& uy, double& dx, double& dy) {
     double vx = hx ? mxo - mu * ((pc - pr) * ih) : 0.0;
     double vy = hy ? myo - mu * ((pc - pu) * ih) : 0.0;
     if constexpr (kNB && PN == 1) {
-        const double nrm = sqrt(vx * vx + vy * vy);
-        const bool z = nrm <= mu;  // NaN -> false, as prox.cpp:33
-        const double sc = 1.0 - mu / (z ? mu : nrm);
-        ux = z ? 0.0 : sc * vx;
-        uy = z ? 0.0 : sc * vy;
+        shrink2_nb(vx, vy, mu, ux, uy);
     } else {
         shrink<PN>(vx, vy, mu, ux, uy);
     }
