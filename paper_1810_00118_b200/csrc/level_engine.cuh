@@ -539,12 +539,78 @@ bool launch_cluster_pn(const Level& lv, int C, cudaStream_t s) {
     return true;
 }
 
+// Level-persistent tile engine (tile_kernels.cuh): one pair, whole level in
+// one cooperative launch, TR x TC tiles in shared memory (one CTA per SM)
+// plus a controller CTA.  0 = off, 1 = auto (one-pair levels with
+// g_tile_min <= n <= g_tile_max), 2 = every one-pair level that fits.
+int g_tile = 0;
+int g_tile_min = 96;
+int g_tile_max = 640;
+int g_tile_grid = 0;  // tiles per side (0: floor(sqrt(SMs - 1)))
+
+struct TileGeom {
+    int TR = 0, TC = 0, LW = 0, LH = 0;
+};
+
+bool tile_geometry(const w1mg_ctx* c, const Level& lv, TileGeom& g) {
+    if (!g_tile || lv.slab || lv.B != 1) return false;
+    if (g_tile == 1 && (lv.n < g_tile_min || lv.n > g_tile_max)) return false;
+    int t = g_tile_grid ? g_tile_grid : (int)std::floor(std::sqrt((double)(c->num_sms - 1)));
+    t = std::min(t, (lv.n + 1) / 4);  // tiles at least 4 nodes wide
+    if (t < 1 || (long)lv.B * (t * t + 1) > c->num_sms) return false;
+    g.TR = g.TC = t;
+    g.LW = (lv.n + 1 + t - 1) / t + 2;
+    g.LH = g.LW;
+    return tile_smem_bytes(g.LW, g.LH) <= 200 * 1024;
+}
+
+template <int PN>
+void launch_tile_pn(w1mg_ctx* c, const Level& lv, const TileGeom& g) {
+    const int T = g.TR * g.TC;
+    const size_t B = lv.B;
+    TileArgs t;
+    t.a = lv.args;
+    t.TR = g.TR;
+    t.TC = g.TC;
+    t.LW = g.LW;
+    t.LH = g.LH;
+    t.ES = g.LW - 2;
+    t.edges = c->get<double>("tile.edges", B * 2 * T * kTileSecs * t.ES);
+    t.flags = c->get<unsigned>("tile.flags", B * T * kTileFlagStride);
+    t.part = c->get<double>("tile.part", B * kTileSlots * T * 3);
+    t.cnt = c->get<unsigned>("tile.cnt", B * kTileSlots);
+    t.dec = c->get<double>("tile.dec", B * kTileSlots * 2);
+    t.dseq = c->get<unsigned long long>("tile.dseq", B * kTileSlots);
+    t.err = c->get<int>("tile.err", 1);
+    CK(cudaMemsetAsync(t.flags, 0, sizeof(unsigned) * B * T * kTileFlagStride, c->stream));
+    CK(cudaMemsetAsync(t.cnt, 0, sizeof(unsigned) * B * kTileSlots, c->stream));
+    CK(cudaMemsetAsync(t.dseq, 0, sizeof(unsigned long long) * B * kTileSlots, c->stream));
+    CK(cudaMemsetAsync(t.err, 0, sizeof(int), c->stream));
+    const int smem = (int)tile_smem_bytes(g.LW, g.LH);
+    CK(cudaFuncSetAttribute(cp_tile_kernel<PN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cp_tile_kernel<PN>, kTileThreads, smem));
+    if ((long)occ * c->num_sms < (long)B * (T + 1))
+        fail(W1MG_ECUDA, "tile engine: the tiles do not fit co-resident");
+    void* args[] = {(void*)&t};
+    CK(cudaLaunchCooperativeKernel((const void*)cp_tile_kernel<PN>, dim3((unsigned)(B * (T + 1))),
+                                   dim3(kTileThreads), args, smem, c->stream));
+}
+
 void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
     if (max_iters <= 0) return;
     if (grid_ok(c, lv)) {  // whole one-pair level in one cooperative launch
         if (pn == 0) launch_grid_pn<0>(c, lv);
         else if (pn == 1) launch_grid_pn<1>(c, lv);
         else launch_grid_pn<2>(c, lv);
+        ++c->launches;
+        return;
+    }
+    TileGeom tg;
+    if (tile_geometry(c, lv, tg)) {  // whole one-pair level in one launch, tiles in shared memory
+        if (pn == 0) launch_tile_pn<0>(c, lv, tg);
+        else if (pn == 1) launch_tile_pn<1>(c, lv, tg);
+        else launch_tile_pn<2>(c, lv, tg);
         ++c->launches;
         return;
     }

@@ -1,0 +1,441 @@
+// tile_kernels.cuh -- level-persistent tile engine: a whole CP level of one
+// pair (or a few) in ONE launch, state resident in shared memory, neighbour
+// halos through L2, no grid-wide barrier on the data path.
+//
+// A one-pair level of n = 96..512 is too small to fill the GPU with the
+// streaming kernels (a 512^2 sweep is 14.7 MB, ~2 us of HBM time, but a
+// launch of it costs ~7 us of ramp, tail and reduction), and a cooperative
+// grid barrier per sweep costs as much.  Here the level is cut into
+// TR x TC tiles, one CTA per tile (one per SM, co-resident by a cooperative
+// launch), each holding its tile of phi, m, dm and rho in shared memory with
+// a one-node halo ring.  Per sweep k:
+//
+//   1. wait until the six neighbours that feed the halo (left, right, below,
+//      above, above-left, below-right) have finished sweep k-1 (per-tile step
+//      flags, acquire loads), read their published edges (phi, m) from L2;
+//   2. phase A: the m-update (node_flux) of the owned nodes and, recomputed,
+//      of the left halo column and the bottom halo row (their fluxes enter
+//      the divergence of the first owned column / row);
+//   3. phase B: the phi-update in the reference's divergence order;
+//   4. publish the edges of the new state (double-buffered by step parity),
+//      post the tile's three residual sums for sweep k, release the step flag.
+//
+// The stop rule (solver_cp.cpp:128-136) needs R^k, a sum over all tiles.  A
+// controller CTA per pair reduces the posted partials in a fixed order, writes
+// the residual history and the decision for every sweep; tiles read the
+// decision of sweep k - kTileLag at the start of sweep k, so the reduction is
+// off the critical path.  When sweep s is found to stop, every tile has run
+// exactly kTileLag sweeps past it; all tiles restore the checkpoint (written
+// every kTileCk sweeps into the level's two ping-pong buffers) at or below
+// s + 1 and replay to s + 1 -- the arithmetic is deterministic, so the final
+// state is bit-identical to stopping on time.  Node arithmetic is node_flux /
+// row_update's, so fields are bit-identical to the reference.
+//
+// Ordering: edge records of step q live in buffer q & 1; a tile overwrites
+// buffer q & 1 at step q + 2 only after every reader of step q (its
+// neighbours, which it waits for) posted step q + 1.  Residual slots are
+// reused after kTileSlots sweeps, by which time the controller has consumed
+// them (tiles wait for decision k - kTileLag, kTileSlots > kTileLag).
+#pragma once
+
+#include "cp_kernels.cuh"
+
+namespace w1mg_dev {
+
+constexpr int kTileThreads = 512;
+constexpr int kTileWarps = kTileThreads / 32;
+constexpr int kTileLag = 16;             // decisions are read this many sweeps late
+constexpr int kTileSlots = 2 * kTileLag; // residual ring
+constexpr int kTileCk = kTileLag;        // checkpoint period (>= lag: the restored slot is intact)
+constexpr int kTileFlagStride = 32;      // one 128-B line per step flag
+constexpr int kTileSecs = 8;             // edge sections, see below
+// edge sections of a tile's record: phi of the left/right columns and the
+// bottom/top rows, m_x, m_y of the right column and of the top row
+enum TileSec { E_PHI_L = 0, E_PHI_R, E_PHI_B, E_PHI_T, E_MX_R, E_MY_R, E_MX_T, E_MY_T };
+
+struct TileArgs {
+    SweepArgs a;           // level: base, L, mu, tau, ih, h2, ctl, hist, ndone
+    int TR, TC;            // tiles per pair (rows x columns of tiles)
+    int LW, LH;            // shared-memory pitch / rows (largest tile + halo ring)
+    int ES;                // edge section stride (largest tile side)
+    double* edges;         // [pairs][2][T][kTileSecs][ES]
+    unsigned* flags;       // [pairs][T][kTileFlagStride] steps completed
+    double* part;          // [pairs][kTileSlots][T][3]
+    unsigned* cnt;         // [pairs][kTileSlots] tiles posted
+    double* dec;           // [pairs][kTileSlots][2] residual, stop
+    unsigned long long* dseq;  // [pairs][kTileSlots] decided sweep + 1
+    int* err;              // set when a wait times out (then the kernel traps)
+};
+
+__host__ __device__ inline int tile_lo(int N1, int parts, int t) {
+    return (int)((long)N1 * t / parts);
+}
+__host__ inline long tile_smem_bytes(int LW, int LH) { return 6L * LW * LH * 8; }
+
+__device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_acq64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// bounded spin: a lost peer must fail the launch, not hang the GPU
+__device__ __noinline__ void tile_timeout(int* err) {
+    atomicExch(err, 1);
+    __trap();
+}
+constexpr unsigned long long kTileTimeoutNs = 20ull * 1000 * 1000 * 1000;
+
+// Controller of one pair: reduces sweep s's partials once every tile posted
+// them, records R^s, decides the stop (solver_cp.cpp:128-136), publishes it.
+__device__ void tile_controller(const TileArgs& t, int pair, int T, long k0) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const SweepArgs& a = t.a;
+    PairCtl* ctl = a.ctl + pair;
+    const long max_it = ctl->max_it;
+    const double tol = ctl->tol;
+    for (long s = k0;; ++s) {
+        const int slot = (int)(s % kTileSlots);
+        unsigned* cnt = t.cnt + (long)pair * kTileSlots + slot;
+        if (lane == 0) {
+            const unsigned long long t0 = gtimer();
+            while (ld_acq(cnt) < (unsigned)T)
+                if (gtimer() - t0 > kTileTimeoutNs) tile_timeout(t.err);
+        }
+        __syncwarp();
+        const double* p = t.part + ((long)pair * kTileSlots + slot) * T * 3;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+        for (int b = lane; b < T; b += 32) {
+            s0 += __ldcg(p + b * 3 + 0);
+            s1 += __ldcg(p + b * 3 + 1);
+            s2 += __ldcg(p + b * 3 + 2);
+        }
+        s0 = warp_sum(s0);
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+        int stop = 0;
+        if (lane == 0) {
+            const double fpr = a.h2 * (s0 / a.mu + s1 / a.tau - 2.0 * s2);  // Eq. 9
+            const bool finite = isfinite(fpr);
+            stop = (fpr < tol || s + 1 >= max_it || !finite) ? 1 : 0;
+            if (a.hist && s < a.hist_cap) a.hist[(long)pair * a.hist_cap + s] = fpr;
+            *cnt = 0u;  // the slot is reused only after tiles saw this decision
+            double* d = t.dec + ((long)pair * kTileSlots + slot) * 2;
+            d[0] = fpr;
+            d[1] = stop ? 1.0 : 0.0;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(t.dseq + (long)pair * kTileSlots + slot),
+                         "l"((unsigned long long)(s + 1))
+                         : "memory");
+        }
+        stop = __shfl_sync(0xffffffffu, stop, 0);
+        if (stop) return;
+    }
+}
+
+template <int PN>
+__global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs t) {
+    const int T = t.TR * t.TC;
+    const int pair = blockIdx.x / (T + 1);
+    const int tile = blockIdx.x % (T + 1);
+    const SweepArgs& a = t.a;
+    PairCtl* ctl = a.ctl + pair;
+    if (*(volatile int*)&ctl->done) return;  // uniform: nothing writes ctl before the end
+    const long k0 = ctl->it;
+    if (tile == T) {
+        tile_controller(t, pair, T, k0);
+        return;
+    }
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double wred[kTileWarps][3];
+    __shared__ int s_stop;
+    __shared__ long s_stop_at;
+    __shared__ double s_fpr;
+
+    const Layout L = a.L;
+    const int n = L.n;
+    const int tr = tile / t.TC, tc = tile % t.TC;
+    const int i0 = tile_lo(n + 1, t.TC, tc), j0 = tile_lo(n + 1, t.TR, tr);
+    const int w = tile_lo(n + 1, t.TC, tc + 1) - i0;
+    const int h = tile_lo(n + 1, t.TR, tr + 1) - j0;
+    const int LW = t.LW;
+    const int S = LW * t.LH;
+    double* phi = sm;
+    double* mx = sm + S;
+    double* my = sm + 2 * S;
+    double* ddx = sm + 3 * S;
+    double* ddy = sm + 4 * S;
+    double* rho = sm + 5 * S;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const double mu = a.mu, tau = a.tau, ih = a.ih;
+
+    // neighbours (tile index within the pair, -1 = none)
+    const int nL = tc > 0 ? tile - 1 : -1;
+    const int nR = tc + 1 < t.TC ? tile + 1 : -1;
+    const int nD = tr > 0 ? tile - t.TC : -1;
+    const int nU = tr + 1 < t.TR ? tile + t.TC : -1;
+    const int nUL = (tr + 1 < t.TR && tc > 0) ? tile + t.TC - 1 : -1;
+    const int nDR = (tr > 0 && tc + 1 < t.TC) ? tile - t.TC + 1 : -1;
+    const int wL = tc > 0 ? i0 - tile_lo(n + 1, t.TC, tc - 1) : 0;  // width of the left tile column
+
+    const long recs = (long)T * kTileSecs * t.ES;  // doubles per step buffer of one pair
+    double* ebase = t.edges + (long)pair * 2 * recs;
+    auto rec = [&](int buf, int who, int sec) -> double* {
+        return ebase + buf * recs + ((long)who * kTileSecs + sec) * t.ES;
+    };
+    unsigned* flags = t.flags + (long)pair * T * kTileFlagStride;
+    double* pb = a.base + (long)pair * NSLOT * L.plane;
+
+    // whole tile + halo ring from the level buffer planes of parity p
+    auto load_state = [&](int p) {
+        const double* gp = pb + (PHI0 + p) * L.plane;
+        const double* gx = pb + (MX0 + p) * L.plane;
+        const double* gy = pb + (MY0 + p) * L.plane;
+        const double* gr = pb + RHO * L.plane;
+        const int W2 = w + 2, cnt = W2 * (h + 2);
+        for (int q = tid; q < cnt; q += kTileThreads) {
+            const int li = q % W2, lj = q / W2;
+            const int i = i0 - 1 + li, j = j0 - 1 + lj;
+            const bool in = i >= 0 && i <= n && j >= 0 && j <= n;
+            const long o = in ? L.at(i, j) : 0;
+            const int k = lj * LW + li;
+            phi[k] = in ? __ldcg(gp + o) : 0.0;
+            mx[k] = (in && i < n) ? __ldcg(gx + o) : 0.0;
+            my[k] = (in && j < n) ? __ldcg(gy + o) : 0.0;
+            ddx[k] = 0.0;
+            ddy[k] = 0.0;
+            rho[k] = (in && li >= 1 && li <= w && lj >= 1 && lj <= h) ? __ldg(gr + o) : 0.0;
+        }
+    };
+    // owned phi, m -> planes of parity p (checkpoint / final state)
+    auto store_state = [&](int p) {
+        double* gp = pb + (PHI0 + p) * L.plane;
+        double* gx = pb + (MX0 + p) * L.plane;
+        double* gy = pb + (MY0 + p) * L.plane;
+        for (int q = tid; q < w * h; q += kTileThreads) {
+            const int li = 1 + q % w, lj = 1 + q / w;
+            const int i = i0 - 1 + li, j = j0 - 1 + lj;
+            const long o = L.at(i, j);
+            const int k = lj * LW + li;
+            __stcg(gp + o, phi[k]);
+            if (i < n) __stcg(gx + o, mx[k]);
+            if (j < n) __stcg(gy + o, my[k]);
+        }
+    };
+    // halo ring from the neighbours' records of step buffer `buf`
+    auto load_halo = [&](int buf) {
+        const int cnt = 4 * h + 4 * w + 2;
+        for (int q = tid; q < cnt; q += kTileThreads) {
+            if (q < 3 * h) {  // left column: phi, m_x, m_y of the left tile's right column
+                if (nL < 0) continue;
+                const int f = q / h, r = q % h;
+                const double v = __ldcg(rec(buf, nL, f == 0 ? E_PHI_R : (f == 1 ? E_MX_R : E_MY_R)) + r);
+                double* dst = f == 0 ? phi : (f == 1 ? mx : my);
+                dst[(1 + r) * LW] = v;
+            } else if (q < 3 * h + 3 * w) {  // bottom row from the lower tile's top row
+                if (nD < 0) continue;
+                const int q2 = q - 3 * h;
+                const int f = q2 / w, r = q2 % w;
+                const double v = __ldcg(rec(buf, nD, f == 0 ? E_PHI_T : (f == 1 ? E_MX_T : E_MY_T)) + r);
+                double* dst = f == 0 ? phi : (f == 1 ? mx : my);
+                dst[1 + r] = v;
+            } else if (q < 4 * h + 3 * w) {  // right column phi
+                if (nR < 0) continue;
+                const int r = q - 3 * h - 3 * w;
+                phi[(1 + r) * LW + w + 1] = __ldcg(rec(buf, nR, E_PHI_L) + r);
+            } else if (q < 4 * h + 4 * w) {  // top row phi
+                if (nU < 0) continue;
+                const int r = q - 4 * h - 3 * w;
+                phi[(h + 1) * LW + 1 + r] = __ldcg(rec(buf, nU, E_PHI_B) + r);
+            } else if (q == 4 * h + 4 * w) {  // above-left corner: that tile's bottom-right node
+                if (nUL >= 0) phi[(h + 1) * LW] = __ldcg(rec(buf, nUL, E_PHI_B) + wL - 1);
+            } else {  // below-right corner: that tile's top-left node
+                if (nDR >= 0) phi[w + 1] = __ldcg(rec(buf, nDR, E_PHI_T));
+            }
+        }
+    };
+
+    long k = k0;      // logical sweep index (state k in shared memory)
+    unsigned step = 0;  // steps executed (monotonic, also across a replay)
+    bool replay = false;
+    long target = -1;  // replay: stop at state target
+    double fin_fpr = 0.0;
+    long stop_at = -1;
+
+    load_state(ctl->cur);
+    if (tid == 0) s_stop = 0;
+    __syncthreads();
+    if (ctl->cur != 0) store_state(0);  // checkpoint of state k0 (slot 0)
+
+    for (;;) {
+        if (replay && k >= target) break;
+        // ---- phase A: fluxes of owned nodes + recomputed left / bottom halo
+        double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
+        const int bufw = (int)((step + 1) & 1);  // record buffer of the state this step produces
+        {
+            const int W1 = w + 1, cnt = W1 * (h + 1);
+            for (int q = tid; q < cnt; q += kTileThreads) {
+                const int li = q % W1, lj = q / W1;
+                const int i = i0 - 1 + li, j = j0 - 1 + lj;
+                if (i < 0 || j < 0 || (li == 0 && lj == 0)) continue;
+                const int kk = lj * LW + li;
+                const bool hx = i < n, hy = j < n;
+                const double pc = phi[kk];
+                const double pr = hx ? phi[kk + 1] : 0.0;
+                const double pu = hy ? phi[kk + LW] : 0.0;
+                double ux, uy, dx, dy;
+                node_flux<PN>(hx, hy, pc, pr, pu, mx[kk], my[kk], mu, ih, ux, uy, dx, dy);
+                mx[kk] = ux;
+                my[kk] = uy;
+                ddx[kk] = dx;
+                ddy[kk] = dy;
+                if (li >= 1 && lj >= 1) {
+                    s_dm2 += dx * dx + dy * dy;
+                    if (li == w) {
+                        rec(bufw, tile, E_MX_R)[lj - 1] = ux;
+                        rec(bufw, tile, E_MY_R)[lj - 1] = uy;
+                    }
+                    if (lj == h) {
+                        rec(bufw, tile, E_MX_T)[li - 1] = ux;
+                        rec(bufw, tile, E_MY_T)[li - 1] = uy;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ---- phase B: potential of owned nodes (row_update's divergence order)
+        for (int q = tid; q < w * h; q += kTileThreads) {
+            const int li = 1 + q % w, lj = 1 + q / w;
+            const int kk = lj * LW + li;
+            const double divm = (mx[kk] - mx[kk - 1]) * ih + (my[kk] - my[kk - LW]) * ih;
+            const double divd = (ddx[kk] - ddx[kk - 1]) * ih + (ddy[kk] - ddy[kk - LW]) * ih;
+            const double d = tau * (divm + divd - rho[kk]);
+            const double f = phi[kk] + d;
+            phi[kk] = f;
+            s_dp2 += d * d;
+            s_cr += d * divd;
+            if (li == 1) rec(bufw, tile, E_PHI_L)[lj - 1] = f;
+            if (li == w) rec(bufw, tile, E_PHI_R)[lj - 1] = f;
+            if (lj == 1) rec(bufw, tile, E_PHI_B)[li - 1] = f;
+            if (lj == h) rec(bufw, tile, E_PHI_T)[li - 1] = f;
+        }
+        s_dm2 = warp_sum(s_dm2);
+        s_dp2 = warp_sum(s_dp2);
+        s_cr = warp_sum(s_cr);
+        if (lane == 0) {
+            wred[warp][0] = s_dm2;
+            wred[warp][1] = s_dp2;
+            wred[warp][2] = s_cr;
+        }
+        __syncthreads();
+        ++k;
+        ++step;
+        const bool ckpt = !replay && ((k - k0) % kTileCk) == 0;
+        if (ckpt) store_state((int)(((k - k0) / kTileCk) & 1));
+        if (ckpt) __syncthreads();
+        // ---- post: residual partials of sweep k-1, step flag
+        if (tid == 0) {
+            const int slot = (int)((k - 1) % kTileSlots);
+            if (!replay) {
+                double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+                for (int q = 0; q < kTileWarps; ++q) {
+                    t0 += wred[q][0];
+                    t1 += wred[q][1];
+                    t2 += wred[q][2];
+                }
+                double* p = t.part + (((long)pair * kTileSlots + slot) * T + tile) * 3;
+                p[0] = t0;
+                p[1] = t1;
+                p[2] = t2;
+            }
+            __threadfence();
+            if (!replay) atomicAdd(t.cnt + (long)pair * kTileSlots + slot, 1u);
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flags + (long)tile * kTileFlagStride),
+                         "r"(step)
+                         : "memory");
+        }
+        // ---- wait: neighbours done with this step; decision of sweep k - lag
+        if (warp == 0) {
+            const unsigned long long t0 = gtimer();
+            int nb = -1;
+            if (lane == 0) nb = nL;
+            else if (lane == 1) nb = nR;
+            else if (lane == 2) nb = nD;
+            else if (lane == 3) nb = nU;
+            else if (lane == 4) nb = nUL;
+            else if (lane == 5) nb = nDR;
+            if (nb >= 0) {
+                while (ld_acq(flags + (long)nb * kTileFlagStride) < step)
+                    if (gtimer() - t0 > kTileTimeoutNs) tile_timeout(t.err);
+            }
+            const long kd = k - kTileLag;
+            if (lane == 6 && !replay && kd >= k0) {
+                const int slot = (int)(kd % kTileSlots);
+                const unsigned long long* sq = t.dseq + (long)pair * kTileSlots + slot;
+                while (ld_acq64(sq) != (unsigned long long)(kd + 1))
+                    if (gtimer() - t0 > kTileTimeoutNs) tile_timeout(t.err);
+                const double* d = t.dec + ((long)pair * kTileSlots + slot) * 2;
+                if (__ldcg(d + 1) != 0.0) {
+                    s_stop = 1;
+                    s_stop_at = kd;
+                    s_fpr = __ldcg(d);
+                }
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        if (!replay && s_stop) {
+            // sweep s = s_stop_at stopped: restore the checkpoint at or below
+            // s + 1 and replay to exactly s + 1 (every tile does the same)
+            stop_at = s_stop_at;
+            fin_fpr = s_fpr;
+            target = stop_at + 1;
+            const long c = k0 + ((target - k0) / kTileCk) * kTileCk;
+            load_state((int)(((c - k0) / kTileCk) & 1));
+            k = c;
+            replay = true;
+            __syncthreads();
+            continue;
+        }
+        load_halo((int)(step & 1));
+        __syncthreads();
+    }
+    // every neighbour finished its replay (and so its checkpoint reads)
+    // before the final state goes into buffer 0
+    if (warp == 0) {
+        const unsigned long long t0 = gtimer();
+        int nb = -1;
+        if (lane == 0) nb = nL;
+        else if (lane == 1) nb = nR;
+        else if (lane == 2) nb = nD;
+        else if (lane == 3) nb = nU;
+        else if (lane == 4) nb = nUL;
+        else if (lane == 5) nb = nDR;
+        if (nb >= 0)
+            while (ld_acq(flags + (long)nb * kTileFlagStride) < step)
+                if (gtimer() - t0 > kTileTimeoutNs) tile_timeout(t.err);
+        __syncwarp();
+    }
+    __syncthreads();
+    store_state(0);
+    if (tile == 0 && tid == 0) {
+        ctl->it = stop_at + 1;
+        ctl->fpr = fin_fpr;
+        ctl->cur = 0;
+        if (!isfinite(fin_fpr)) ctl->nonfinite = 1;
+        ctl->done = 1;
+        atomicAdd(a.ndone, 1);
+    }
+}
+
+}  // namespace w1mg_dev
