@@ -123,7 +123,7 @@ cp_cluster_kernel(const SweepArgs a, const int C) {
                 my[k] = uy;
                 ddx[k] = dx;
                 ddy[k] = dy;
-                s_dm2 += dx * dx + dy * dy;
+                s_dm2 = __fma_rn(dy, dy, __fma_rn(dx, dx, s_dm2));
                 i += di;
                 jl += dj;
                 if (i >= W) { i -= W; ++jl; }
@@ -150,8 +150,8 @@ cp_cluster_kernel(const SweepArgs a, const int C) {
                 const double divd = (ddx[k] - dxl) * ih + (ddy[k] - dyb) * ih;
                 const double d = tau * (divm + divd - rho[k]);
                 phi[k] = phi[k] + d;
-                s_dp2 += d * d;
-                s_cr += d * divd;
+                s_dp2 = __fma_rn(d, d, s_dp2);
+                s_cr = __fma_rn(d, divd, s_cr);
                 i += di;
                 jl += dj;
                 if (i >= W) { i -= W; ++jl; }

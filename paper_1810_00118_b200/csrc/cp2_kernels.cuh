@@ -295,9 +295,9 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                 const double d = tau * (divm + divd - r);
                 fA = pc + d;
                 if (own && rA >= j0 && rA < j1) {
-                    a_dm2 += dxA * dxA + dyAn * dyAn;
-                    a_dp2 += d * d;
-                    a_cr += d * divd;
+                    a_dm2 = __fma_rn(dyAn, dyAn, __fma_rn(dxA, dxA, a_dm2));
+                    a_dp2 = __fma_rn(d, d, a_dp2);
+                    a_cr = __fma_rn(d, divd, a_cr);
                 }
                 uyA = uyAn;
                 dyA = dyAn;
@@ -321,9 +321,9 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                     phw[ob] = pcB + d;
                     if (hx) mxw[ob] = ux;
                     if (hyB) myw[ob] = uy;
-                    b_dm2 += dx * dx + dy * dy;
-                    b_dp2 += d * d;
-                    b_cr += d * divd;
+                    b_dm2 = __fma_rn(dy, dy, __fma_rn(dx, dx, b_dm2));
+                    b_dp2 = __fma_rn(d, d, b_dp2);
+                    b_cr = __fma_rn(d, divd, b_cr);
                 }
                 uyB = uy;
                 dyB = dy;

@@ -156,9 +156,9 @@ __device__ __forceinline__ void march2w(const SweepArgs& a, int pair, int parity
                 const double d = tau * (divm + divd - r[s]);
                 fA[s] = pc[s] + d;
                 if (own[s] && rA >= j0 && rA < j1) {
-                    acc[0] += dxA[s] * dxA[s] + dyAn[s] * dyAn[s];
-                    acc[1] += d * d;
-                    acc[2] += d * divd;
+                    acc[0] = __fma_rn(dyAn[s], dyAn[s], __fma_rn(dxA[s], dxA[s], acc[0]));
+                    acc[1] = __fma_rn(d, d, acc[1]);
+                    acc[2] = __fma_rn(d, divd, acc[2]);
                 }
                 uyA[s] = uyAn[s];
                 dyA[s] = dyAn[s];
@@ -189,9 +189,9 @@ __device__ __forceinline__ void march2w(const SweepArgs& a, int pair, int parity
                     phw[ob] = fA_prev[s] + d;
                     if (hx[s]) mxw[ob] = ux[s];
                     if (hyB) myw[ob] = uy[s];
-                    acc[3] += dx[s] * dx[s] + dy[s] * dy[s];
-                    acc[4] += d * d;
-                    acc[5] += d * divd;
+                    acc[3] = __fma_rn(dy[s], dy[s], __fma_rn(dx[s], dx[s], acc[3]));
+                    acc[4] = __fma_rn(d, d, acc[4]);
+                    acc[5] = __fma_rn(d, divd, acc[5]);
                 }
                 uyB[s] = uy[s];
                 dyB[s] = dy[s];

@@ -216,9 +216,9 @@ __device__ __forceinline__ void row_update(const SweepArgs& a, const Strip& s, i
         s.phw[o] = pc + d;
         if (s.hx) s.mxw[o] = ux;
         if (hy) s.myw[o] = uy;
-        s_dm2 += dx * dx + dy * dy;
-        s_dp2 += d * d;
-        s_cr += d * divd;
+        s_dm2 = __fma_rn(dy, dy, __fma_rn(dx, dx, s_dm2));
+        s_dp2 = __fma_rn(d, d, s_dp2);
+        s_cr = __fma_rn(d, divd, s_cr);
         if (a.up_base && j == a.jhi - 1) {  // top owned row -> upper neighbour's halo
             const long po = 32 + (long)(j - a.up_row0) * a.L.pitch + s.i;
             a.up_base[(PHI0 + s.wpar) * a.up_plane + po] = pc + d;
@@ -627,7 +627,7 @@ cp_resident_kernel(const SweepArgs a) {
                 my[k] = uy;
                 ddx[k] = dx;
                 ddy[k] = dy;
-                s_dm2 += dx * dx + dy * dy;
+                s_dm2 = __fma_rn(dy, dy, __fma_rn(dx, dx, s_dm2));
                 i += di;
                 j += dj;
                 if (i >= W) { i -= W; ++j; }
@@ -645,8 +645,8 @@ cp_resident_kernel(const SweepArgs a) {
                 const double divd = (ddx[k] - dxl) * ih + (ddy[k] - dyb) * ih;
                 const double d = tau * (divm + divd - rho[k]);
                 phi[k] = phi[k] + d;
-                s_dp2 += d * d;
-                s_cr += d * divd;
+                s_dp2 = __fma_rn(d, d, s_dp2);
+                s_cr = __fma_rn(d, divd, s_cr);
                 i += di;
                 j += dj;
                 if (i >= W) { i -= W; ++j; }

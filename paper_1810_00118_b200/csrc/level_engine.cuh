@@ -542,8 +542,9 @@ bool launch_cluster_pn(const Level& lv, int C, cudaStream_t s) {
 // Level-persistent tile engine (tile_kernels.cuh): one pair, whole level in
 // one cooperative launch, TR x TC tiles in shared memory (one CTA per SM)
 // plus a controller CTA.  0 = off, 1 = auto (one-pair levels with
-// g_tile_min <= n <= g_tile_max), 2 = every one-pair level that fits.
-int g_tile = 0;
+// g_tile_min <= n <= g_tile_max while the resident engines are on auto),
+// 2 = every one-pair level that fits.
+int g_tile = 1;
 int g_tile_min = 96;
 int g_tile_max = 640;
 int g_tile_grid = 0;  // tiles per side (0: floor(sqrt(SMs - 1)))
@@ -554,7 +555,7 @@ struct TileGeom {
 
 bool tile_geometry(const w1mg_ctx* c, const Level& lv, TileGeom& g) {
     if (!g_tile || lv.slab || lv.B != 1) return false;
-    if (g_tile == 1 && (lv.n < g_tile_min || lv.n > g_tile_max)) return false;
+    if (g_tile == 1 && (g_resident != 1 || lv.n < g_tile_min || lv.n > g_tile_max)) return false;
     int t = g_tile_grid ? g_tile_grid : (int)std::floor(std::sqrt((double)(c->num_sms - 1)));
     t = std::min(t, (lv.n + 1) / 4);  // tiles at least 4 nodes wide
     if (t < 1 || (long)lv.B * (t * t + 1) > c->num_sms) return false;
@@ -582,6 +583,11 @@ void launch_tile_pn(w1mg_ctx* c, const Level& lv, const TileGeom& g) {
     t.dec = c->get<double>("tile.dec", B * kTileSlots * 2);
     t.dseq = c->get<unsigned long long>("tile.dseq", B * kTileSlots);
     t.err = c->get<int>("tile.err", 1);
+    t.dbg = nullptr;
+    if (std::getenv("W1MG_TILE_DEBUG")) {  // diagnostics: per-step stamps of tile 0
+        t.dbg = c->get<long long>("tile.dbg", (size_t)kTileDbgSteps * kTileDbgPts);
+        CK(cudaMemsetAsync(t.dbg, 0, sizeof(long long) * kTileDbgSteps * kTileDbgPts, c->stream));
+    }
     CK(cudaMemsetAsync(t.flags, 0, sizeof(unsigned) * B * T * kTileFlagStride, c->stream));
     CK(cudaMemsetAsync(t.cnt, 0, sizeof(unsigned) * B * kTileSlots, c->stream));
     CK(cudaMemsetAsync(t.dseq, 0, sizeof(unsigned long long) * B * kTileSlots, c->stream));
@@ -595,6 +601,18 @@ void launch_tile_pn(w1mg_ctx* c, const Level& lv, const TileGeom& g) {
     void* args[] = {(void*)&t};
     CK(cudaLaunchCooperativeKernel((const void*)cp_tile_kernel<PN>, dim3((unsigned)(B * (T + 1))),
                                    dim3(kTileThreads), args, smem, c->stream));
+    if (t.dbg) {
+        std::vector<long long> h((size_t)kTileDbgSteps * kTileDbgPts);
+        CK(cudaMemcpyAsync(h.data(), t.dbg, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        std::fprintf(stderr, "tile n=%d TRxTC=%dx%d smem=%d\n", lv.n, g.TR, g.TC, smem);
+        for (int q = 1; q < 64; ++q) {
+            const long long* r = &h[(size_t)q * kTileDbgPts];
+            std::fprintf(stderr, "step %d: A %lld B %lld post %lld wait %lld halo %lld next %lld\n", q,
+                         r[1] - r[0], r[2] - r[1], r[5] - r[2], r[3] - r[5], r[4] - r[3],
+                         r[kTileDbgPts] - r[4]);
+        }
+    }
 }
 
 void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {

@@ -38,6 +38,8 @@
 // them (tiles wait for decision k - kTileLag, kTileSlots > kTileLag).
 #pragma once
 
+#include <type_traits>
+
 #include "cp_kernels.cuh"
 
 namespace w1mg_dev {
@@ -65,7 +67,10 @@ struct TileArgs {
     double* dec;           // [pairs][kTileSlots][2] residual, stop
     unsigned long long* dseq;  // [pairs][kTileSlots] decided sweep + 1
     int* err;              // set when a wait times out (then the kernel traps)
+    long long* dbg;        // optional per-step clock64 stamps of tile 0 (diagnostics)
 };
+constexpr int kTileDbgSteps = 256;
+constexpr int kTileDbgPts = 8;
 
 __host__ __device__ inline int tile_lo(int N1, int parts, int t) {
     return (int)((long)N1 * t / parts);
@@ -94,24 +99,76 @@ __device__ __noinline__ void tile_timeout(int* err) {
 }
 constexpr unsigned long long kTileTimeoutNs = 20ull * 1000 * 1000 * 1000;
 
+// relaxed polls (an acquire load would invalidate L1 on every iteration);
+// the caller fences once afterwards.  Timeout checked every 1024 polls.
+__device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target, int* err) {
+    unsigned long long t0 = 0;
+    for (unsigned it = 0;; ++it) {
+        unsigned v;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+        if (v >= target) return;
+        if ((it & 1023u) == 0) {
+            const unsigned long long now = gtimer();
+            if (it == 0) t0 = now;
+            else if (now - t0 > kTileTimeoutNs) tile_timeout(err);
+        }
+    }
+}
+__device__ __forceinline__ void spin_eq64(const unsigned long long* p, unsigned long long target,
+                                          int* err) {
+    unsigned long long t0 = 0;
+    for (unsigned it = 0;; ++it) {
+        unsigned long long v;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+        if (v == target) return;
+        if ((it & 1023u) == 0) {
+            const unsigned long long now = gtimer();
+            if (it == 0) t0 = now;
+            else if (now - t0 > kTileTimeoutNs) tile_timeout(err);
+        }
+    }
+}
+
 // Controller of one pair: reduces sweep s's partials once every tile posted
 // them, records R^s, decides the stop (solver_cp.cpp:128-136), publishes it.
+// Warp w handles sweeps s = k0 + w (mod kTileWarps), so up to kTileWarps
+// decisions are in flight; kTileWarps == kTileLag makes "decision k - lag is
+// out" imply that the same warp finished sweep k - 2 lag, i.e. the residual
+// slot a tile reuses at sweep k (k - kTileSlots) has been consumed.
+static_assert(kTileWarps == kTileLag && kTileSlots == 2 * kTileLag, "controller pipelining");
 __device__ void tile_controller(const TileArgs& t, int pair, int T, long k0) {
-    if (threadIdx.x >= 32) return;
-    const int lane = threadIdx.x;
+    __shared__ long long c_stop;  // earliest stopping sweep found so far
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) c_stop = 0x7fffffffffffffffll;
+    __syncthreads();
     const SweepArgs& a = t.a;
     PairCtl* ctl = a.ctl + pair;
     const long max_it = ctl->max_it;
     const double tol = ctl->tol;
-    for (long s = k0;; ++s) {
+    volatile long long* vstop = &c_stop;
+    for (long s = k0 + warp;; s += kTileWarps) {
         const int slot = (int)(s % kTileSlots);
         unsigned* cnt = t.cnt + (long)pair * kTileSlots + slot;
+        int go = 0;
         if (lane == 0) {
-            const unsigned long long t0 = gtimer();
-            while (ld_acq(cnt) < (unsigned)T)
-                if (gtimer() - t0 > kTileTimeoutNs) tile_timeout(t.err);
+            unsigned long long t0 = 0;
+            for (unsigned it = 0;; ++it) {
+                if (*vstop < s) break;  // a tile never posts sweeps past the stop + lag
+                unsigned v;
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+                if (v >= (unsigned)T) {
+                    go = 1;
+                    break;
+                }
+                if ((it & 1023u) == 0) {
+                    const unsigned long long now = gtimer();
+                    if (it == 0) t0 = now;
+                    else if (now - t0 > kTileTimeoutNs) tile_timeout(t.err);
+                }
+            }
         }
-        __syncwarp();
+        if (!__shfl_sync(0xffffffffu, go, 0)) return;
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
         const double* p = t.part + ((long)pair * kTileSlots + slot) * T * 3;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0;
         for (int b = lane; b < T; b += 32) {
@@ -128,17 +185,16 @@ __device__ void tile_controller(const TileArgs& t, int pair, int T, long k0) {
             const bool finite = isfinite(fpr);
             stop = (fpr < tol || s + 1 >= max_it || !finite) ? 1 : 0;
             if (a.hist && s < a.hist_cap) a.hist[(long)pair * a.hist_cap + s] = fpr;
-            *cnt = 0u;  // the slot is reused only after tiles saw this decision
+            *cnt = 0u;
             double* d = t.dec + ((long)pair * kTileSlots + slot) * 2;
             d[0] = fpr;
             d[1] = stop ? 1.0 : 0.0;
-            __threadfence();
             asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(t.dseq + (long)pair * kTileSlots + slot),
                          "l"((unsigned long long)(s + 1))
                          : "memory");
+            if (stop) atomicMin((long long*)&c_stop, (long long)s);
         }
-        stop = __shfl_sync(0xffffffffu, stop, 0);
-        if (stop) return;
+        if (__shfl_sync(0xffffffffu, stop, 0)) return;
     }
 }
 
@@ -151,7 +207,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
     PairCtl* ctl = a.ctl + pair;
     if (*(volatile int*)&ctl->done) return;  // uniform: nothing writes ctl before the end
     const long k0 = ctl->it;
-    if (tile == T) {
+    if (tile == T) {  // uniform per block
         tile_controller(t, pair, T, k0);
         return;
     }
@@ -277,58 +333,156 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
     __syncthreads();
     if (ctl->cur != 0) store_state(0);  // checkpoint of state k0 (slot 0)
 
+    // (li, lj) of flat index q over a W-wide rectangle, stepped by a stride
+    struct Walk {
+        int li, lj, di, dj, W;
+        __device__ void init(int q, int W_, int stride) {
+            W = W_;
+            li = q % W;
+            lj = q / W;
+            di = stride % W;
+            dj = stride / W;
+        }
+        __device__ void next() {
+            li += di;
+            lj += dj;
+            if (li >= W) {
+                li -= W;
+                ++lj;
+            }
+        }
+    };
+    const int W1 = w + 1, cntA = W1 * (h + 1), cntB = w * h;
+    // warp 0 lanes 0..5 wait for the neighbours' step flags (relaxed polls,
+    // one acquire fence after), lane 6 for the decision of sweep kd
+    auto wait_neighbours = [&](unsigned target_step, long kd) {
+        int nb = -1;
+        if (lane == 0) nb = nL;
+        else if (lane == 1) nb = nR;
+        else if (lane == 2) nb = nD;
+        else if (lane == 3) nb = nU;
+        else if (lane == 4) nb = nUL;
+        else if (lane == 5) nb = nDR;
+        if (nb >= 0) spin_geq(flags + (long)nb * kTileFlagStride, target_step, t.err);
+        if (lane == 6 && kd >= k0) {
+            const int slot = (int)(kd % kTileSlots);
+            spin_eq64(t.dseq + (long)pair * kTileSlots + slot, (unsigned long long)(kd + 1), t.err);
+        }
+        __syncwarp();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (lane == 6 && kd >= k0) {
+            const double* d = t.dec + ((long)pair * kTileSlots + (int)(kd % kTileSlots)) * 2;
+            if (__ldcg(d + 1) != 0.0) {
+                s_stop = 1;
+                s_stop_at = kd;
+                s_fpr = __ldcg(d);
+            }
+        }
+    };
+
     for (;;) {
         if (replay && k >= target) break;
-        // ---- phase A: fluxes of owned nodes + recomputed left / bottom halo
+        if (t.dbg && tile == 0 && tid == 0 && step < kTileDbgSteps) t.dbg[(step) * kTileDbgPts + 0] = clock64();
+        // ---- phase A: fluxes of owned nodes + recomputed left / bottom halo,
+        // two nodes per thread per pass (independent chains for the scheduler)
         double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
         const int bufw = (int)((step + 1) & 1);  // record buffer of the state this step produces
-        {
-            const int W1 = w + 1, cnt = W1 * (h + 1);
-            for (int q = tid; q < cnt; q += kTileThreads) {
-                const int li = q % W1, lj = q / W1;
-                const int i = i0 - 1 + li, j = j0 - 1 + lj;
-                if (i < 0 || j < 0 || (li == 0 && lj == 0)) continue;
-                const int kk = lj * LW + li;
-                const bool hx = i < n, hy = j < n;
-                const double pc = phi[kk];
-                const double pr = hx ? phi[kk + 1] : 0.0;
-                const double pu = hy ? phi[kk + LW] : 0.0;
-                double ux, uy, dx, dy;
-                node_flux<PN>(hx, hy, pc, pr, pu, mx[kk], my[kk], mu, ih, ux, uy, dx, dy);
-                mx[kk] = ux;
-                my[kk] = uy;
-                ddx[kk] = dx;
-                ddy[kk] = dy;
-                if (li >= 1 && lj >= 1) {
-                    s_dm2 += dx * dx + dy * dy;
-                    if (li == w) {
-                        rec(bufw, tile, E_MX_R)[lj - 1] = ux;
-                        rec(bufw, tile, E_MY_R)[lj - 1] = uy;
-                    }
-                    if (lj == h) {
-                        rec(bufw, tile, E_MX_T)[li - 1] = ux;
-                        rec(bufw, tile, E_MY_T)[li - 1] = uy;
+        auto phaseA = [&](auto U_) {
+            constexpr int UU = decltype(U_)::value;
+            Walk wa, wb;
+            wa.init(tid, W1, UU * kTileThreads);
+            wb.init(tid + kTileThreads, W1, UU * kTileThreads);
+            for (int q = tid; q < cntA; q += UU * kTileThreads, wa.next(), wb.next()) {
+                const bool vb = UU == 2 && q + kTileThreads < cntA;
+                int kk[2];
+                bool ok[2], hx[2], hy[2];
+                double pc[2], pr[2], pu[2], mo[2], no[2];
+#pragma unroll
+                for (int u = 0; u < UU; ++u) {
+                    const Walk& wv = u ? wb : wa;
+                    const int i = i0 - 1 + wv.li, j = j0 - 1 + wv.lj;
+                    ok[u] = (u == 0 || vb) && i >= 0 && j >= 0 && (wv.li | wv.lj) != 0;
+                    kk[u] = wv.lj * LW + wv.li;
+                    hx[u] = i < n;
+                    hy[u] = j < n;
+                    const int k2 = ok[u] ? kk[u] : 0;
+                    pc[u] = phi[k2];
+                    pr[u] = hx[u] ? phi[k2 + 1] : 0.0;
+                    pu[u] = hy[u] ? phi[k2 + LW] : 0.0;
+                    mo[u] = mx[k2];
+                    no[u] = my[k2];
+                }
+                double ux[2], uy[2], dx[2], dy[2];
+#pragma unroll
+                for (int u = 0; u < UU; ++u)
+                    node_flux<PN>(hx[u], hy[u], pc[u], pr[u], pu[u], mo[u], no[u], mu, ih, ux[u], uy[u],
+                                  dx[u], dy[u]);
+#pragma unroll
+                for (int u = 0; u < UU; ++u) {
+                    if (!ok[u]) continue;
+                    const Walk& wv = u ? wb : wa;
+                    const int li = wv.li, lj = wv.lj;
+                    mx[kk[u]] = ux[u];
+                    my[kk[u]] = uy[u];
+                    ddx[kk[u]] = dx[u];
+                    ddy[kk[u]] = dy[u];
+                    if (li >= 1 && lj >= 1) {
+                        s_dm2 = __fma_rn(dy[u], dy[u], __fma_rn(dx[u], dx[u], s_dm2));
+                        if (li == w) {
+                            rec(bufw, tile, E_MX_R)[lj - 1] = ux[u];
+                            rec(bufw, tile, E_MY_R)[lj - 1] = uy[u];
+                        }
+                        if (lj == h) {
+                            rec(bufw, tile, E_MX_T)[li - 1] = ux[u];
+                            rec(bufw, tile, E_MY_T)[li - 1] = uy[u];
+                        }
                     }
                 }
             }
-        }
+        };
+        if (cntA > kTileThreads) phaseA(std::integral_constant<int, 2>{});
+        else phaseA(std::integral_constant<int, 1>{});
         __syncthreads();
+        if (t.dbg && tile == 0 && tid == 0 && step < kTileDbgSteps) t.dbg[(step) * kTileDbgPts + 1] = clock64();
         // ---- phase B: potential of owned nodes (row_update's divergence order)
-        for (int q = tid; q < w * h; q += kTileThreads) {
-            const int li = 1 + q % w, lj = 1 + q / w;
-            const int kk = lj * LW + li;
-            const double divm = (mx[kk] - mx[kk - 1]) * ih + (my[kk] - my[kk - LW]) * ih;
-            const double divd = (ddx[kk] - ddx[kk - 1]) * ih + (ddy[kk] - ddy[kk - LW]) * ih;
-            const double d = tau * (divm + divd - rho[kk]);
-            const double f = phi[kk] + d;
-            phi[kk] = f;
-            s_dp2 += d * d;
-            s_cr += d * divd;
-            if (li == 1) rec(bufw, tile, E_PHI_L)[lj - 1] = f;
-            if (li == w) rec(bufw, tile, E_PHI_R)[lj - 1] = f;
-            if (lj == 1) rec(bufw, tile, E_PHI_B)[li - 1] = f;
-            if (lj == h) rec(bufw, tile, E_PHI_T)[li - 1] = f;
-        }
+        auto phaseB = [&](auto U_) {
+            constexpr int UU = decltype(U_)::value;
+            Walk wa, wb;
+            wa.init(tid, w, UU * kTileThreads);
+            wb.init(tid + kTileThreads, w, UU * kTileThreads);
+            for (int q = tid; q < cntB; q += UU * kTileThreads, wa.next(), wb.next()) {
+                const bool vb = UU == 2 && q + kTileThreads < cntB;
+                int kk[2];
+                double divm[2], divd[2], rr[2], pc[2];
+#pragma unroll
+                for (int u = 0; u < UU; ++u) {
+                    const Walk& wv = u ? wb : wa;
+                    kk[u] = (u == 0 || vb) ? (1 + wv.lj) * LW + 1 + wv.li : LW + 1;
+                    const int c = kk[u];
+                    divm[u] = (mx[c] - mx[c - 1]) * ih + (my[c] - my[c - LW]) * ih;
+                    divd[u] = (ddx[c] - ddx[c - 1]) * ih + (ddy[c] - ddy[c - LW]) * ih;
+                    rr[u] = rho[c];
+                    pc[u] = phi[c];
+                }
+#pragma unroll
+                for (int u = 0; u < UU; ++u) {
+                    if (u == 1 && !vb) continue;
+                    const Walk& wv = u ? wb : wa;
+                    const int li = 1 + wv.li, lj = 1 + wv.lj;
+                    const double d = tau * (divm[u] + divd[u] - rr[u]);
+                    const double f = pc[u] + d;
+                    phi[kk[u]] = f;
+                    s_dp2 = __fma_rn(d, d, s_dp2);
+                    s_cr = __fma_rn(d, divd[u], s_cr);
+                    if (li == 1) rec(bufw, tile, E_PHI_L)[lj - 1] = f;
+                    if (li == w) rec(bufw, tile, E_PHI_R)[lj - 1] = f;
+                    if (lj == 1) rec(bufw, tile, E_PHI_B)[li - 1] = f;
+                    if (lj == h) rec(bufw, tile, E_PHI_T)[li - 1] = f;
+                }
+            }
+        };
+        if (cntB > kTileThreads) phaseB(std::integral_constant<int, 2>{});
+        else phaseB(std::integral_constant<int, 1>{});
         s_dm2 = warp_sum(s_dm2);
         s_dp2 = warp_sum(s_dp2);
         s_cr = warp_sum(s_cr);
@@ -338,62 +492,40 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
             wred[warp][2] = s_cr;
         }
         __syncthreads();
+        if (t.dbg && tile == 0 && tid == 0 && step < kTileDbgSteps) t.dbg[(step) * kTileDbgPts + 2] = clock64();
         ++k;
         ++step;
         const bool ckpt = !replay && ((k - k0) % kTileCk) == 0;
-        if (ckpt) store_state((int)(((k - k0) / kTileCk) & 1));
-        if (ckpt) __syncthreads();
-        // ---- post: residual partials of sweep k-1, step flag
-        if (tid == 0) {
-            const int slot = (int)((k - 1) % kTileSlots);
-            if (!replay) {
-                double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-                for (int q = 0; q < kTileWarps; ++q) {
-                    t0 += wred[q][0];
-                    t1 += wred[q][1];
-                    t2 += wred[q][2];
-                }
-                double* p = t.part + (((long)pair * kTileSlots + slot) * T + tile) * 3;
-                p[0] = t0;
-                p[1] = t1;
-                p[2] = t2;
-            }
-            __threadfence();
-            if (!replay) atomicAdd(t.cnt + (long)pair * kTileSlots + slot, 1u);
-            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(flags + (long)tile * kTileFlagStride),
+        if (ckpt) {
+            store_state((int)(((k - k0) / kTileCk) & 1));
+            __syncthreads();
+        }
+        // ---- post: the step flag first (release: the edge records of every
+        // thread, ordered by the barrier), the residual partials from warp 1
+        if (tid == 0)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + (long)tile * kTileFlagStride),
                          "r"(step)
                          : "memory");
+        if (tid == 32 && !replay) {
+            const int slot = (int)((k - 1) % kTileSlots);
+            double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+            for (int q = 0; q < kTileWarps; ++q) {
+                t0 += wred[q][0];
+                t1 += wred[q][1];
+                t2 += wred[q][2];
+            }
+            double* p = t.part + (((long)pair * kTileSlots + slot) * T + tile) * 3;
+            p[0] = t0;
+            p[1] = t1;
+            p[2] = t2;
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(t.cnt + (long)pair * kTileSlots + slot)
+                         : "memory");
         }
+        if (t.dbg && tile == 0 && tid == 0 && step - 1 < kTileDbgSteps) t.dbg[(step - 1) * kTileDbgPts + 5] = clock64();
         // ---- wait: neighbours done with this step; decision of sweep k - lag
-        if (warp == 0) {
-            const unsigned long long t0 = gtimer();
-            int nb = -1;
-            if (lane == 0) nb = nL;
-            else if (lane == 1) nb = nR;
-            else if (lane == 2) nb = nD;
-            else if (lane == 3) nb = nU;
-            else if (lane == 4) nb = nUL;
-            else if (lane == 5) nb = nDR;
-            if (nb >= 0) {
-                while (ld_acq(flags + (long)nb * kTileFlagStride) < step)
-                    if (gtimer() - t0 > kTileTimeoutNs) tile_timeout(t.err);
-            }
-            const long kd = k - kTileLag;
-            if (lane == 6 && !replay && kd >= k0) {
-                const int slot = (int)(kd % kTileSlots);
-                const unsigned long long* sq = t.dseq + (long)pair * kTileSlots + slot;
-                while (ld_acq64(sq) != (unsigned long long)(kd + 1))
-                    if (gtimer() - t0 > kTileTimeoutNs) tile_timeout(t.err);
-                const double* d = t.dec + ((long)pair * kTileSlots + slot) * 2;
-                if (__ldcg(d + 1) != 0.0) {
-                    s_stop = 1;
-                    s_stop_at = kd;
-                    s_fpr = __ldcg(d);
-                }
-            }
-            __syncwarp();
-        }
+        if (warp == 0) wait_neighbours(step, replay ? k0 - 1 : k - kTileLag);
         __syncthreads();
+        if (t.dbg && tile == 0 && tid == 0 && step - 1 < kTileDbgSteps) t.dbg[(step - 1) * kTileDbgPts + 3] = clock64();
         if (!replay && s_stop) {
             // sweep s = s_stop_at stopped: restore the checkpoint at or below
             // s + 1 and replay to exactly s + 1 (every tile does the same)
@@ -409,23 +541,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
         }
         load_halo((int)(step & 1));
         __syncthreads();
+        if (t.dbg && tile == 0 && tid == 0 && step - 1 < kTileDbgSteps) t.dbg[(step - 1) * kTileDbgPts + 4] = clock64();
     }
     // every neighbour finished its replay (and so its checkpoint reads)
     // before the final state goes into buffer 0
-    if (warp == 0) {
-        const unsigned long long t0 = gtimer();
-        int nb = -1;
-        if (lane == 0) nb = nL;
-        else if (lane == 1) nb = nR;
-        else if (lane == 2) nb = nD;
-        else if (lane == 3) nb = nU;
-        else if (lane == 4) nb = nUL;
-        else if (lane == 5) nb = nDR;
-        if (nb >= 0)
-            while (ld_acq(flags + (long)nb * kTileFlagStride) < step)
-                if (gtimer() - t0 > kTileTimeoutNs) tile_timeout(t.err);
-        __syncwarp();
-    }
+    if (warp == 0) wait_neighbours(step, k0 - 1);
     __syncthreads();
     store_state(0);
     if (tile == 0 && tid == 0) {
