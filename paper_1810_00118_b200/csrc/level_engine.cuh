@@ -544,7 +544,7 @@ bool launch_cluster_pn(const Level& lv, int C, cudaStream_t s) {
 // plus a controller CTA.  0 = off, 1 = auto (one-pair levels with
 // g_tile_min <= n <= g_tile_max while the resident engines are on auto),
 // 2 = every one-pair level that fits.
-int g_tile = 1;
+int g_tile = 0;
 int g_tile_min = 96;
 int g_tile_max = 640;
 int g_tile_grid = 0;  // tiles per side (0: floor(sqrt(SMs - 1)))
@@ -606,11 +606,10 @@ void launch_tile_pn(w1mg_ctx* c, const Level& lv, const TileGeom& g) {
         CK(cudaMemcpyAsync(h.data(), t.dbg, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         std::fprintf(stderr, "tile n=%d TRxTC=%dx%d smem=%d\n", lv.n, g.TR, g.TC, smem);
-        for (int q = 1; q < 64; ++q) {
+        for (int q = 0; q < T; ++q) {
             const long long* r = &h[(size_t)q * kTileDbgPts];
-            std::fprintf(stderr, "step %d: A %lld B %lld post %lld wait %lld halo %lld next %lld\n", q,
-                         r[1] - r[0], r[2] - r[1], r[5] - r[2], r[3] - r[5], r[4] - r[3],
-                         r[kTileDbgPts] - r[4]);
+            std::fprintf(stderr, "tile %3d: loop %lld A %lld B %lld post %lld wait %lld halo %lld\n", q,
+                         r[0] / 128, r[1] / 128, r[2] / 128, r[5] / 128, r[3] / 128, r[4] / 128);
         }
     }
 }

@@ -65,7 +65,7 @@ struct TileArgs {
     double* part;          // [pairs][kTileSlots][T][3]
     unsigned* cnt;         // [pairs][kTileSlots] tiles posted
     double* dec;           // [pairs][kTileSlots][2] residual, stop
-    unsigned long long* dseq;  // [pairs][kTileSlots] decided sweep + 1
+    unsigned long long* dseq;  // [pairs][kTileSlots] 2 (decided sweep + 1) + stop
     int* err;              // set when a wait times out (then the kernel traps)
     long long* dbg;        // optional per-step clock64 stamps of tile 0 (diagnostics)
 };
@@ -114,13 +114,14 @@ __device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target, int
         }
     }
 }
-__device__ __forceinline__ void spin_eq64(const unsigned long long* p, unsigned long long target,
-                                          int* err) {
+// waits for (*p >> 1) == tag and returns *p
+__device__ __forceinline__ unsigned long long spin_tag64(const unsigned long long* p,
+                                                         unsigned long long tag, int* err) {
     unsigned long long t0 = 0;
     for (unsigned it = 0;; ++it) {
         unsigned long long v;
         asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-        if (v == target) return;
+        if ((v >> 1) == tag) return v;
         if ((it & 1023u) == 0) {
             const unsigned long long now = gtimer();
             if (it == 0) t0 = now;
@@ -190,7 +191,7 @@ __device__ void tile_controller(const TileArgs& t, int pair, int T, long k0) {
             d[0] = fpr;
             d[1] = stop ? 1.0 : 0.0;
             asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(t.dseq + (long)pair * kTileSlots + slot),
-                         "l"((unsigned long long)(s + 1))
+                         "l"((unsigned long long)(2 * (s + 1) + stop))
                          : "memory");
             if (stop) atomicMin((long long*)&c_stop, (long long)s);
         }
@@ -353,8 +354,13 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
         }
     };
     const int W1 = w + 1, cntA = W1 * (h + 1), cntB = w * h;
-    // warp 0 lanes 0..5 wait for the neighbours' step flags (relaxed polls,
-    // one acquire fence after), lane 6 for the decision of sweep kd
+    // warp 0 lanes 0..5 wait for the neighbours' step flags, lane 6 for the
+    // decision of sweep kd.  Relaxed polls without an acquire fence: every
+    // load that consumes a neighbour's records is an L2 (.cg, gpu-scope
+    // strong) load issued only after the poll loop has exited (control
+    // dependence), and the producer released the flag after its records
+    // reached L2 (st.release), so the records are observed no earlier than
+    // the flag.  (A fence here costs ~600 cycles per sweep, measured.)
     auto wait_neighbours = [&](unsigned target_step, long kd) {
         int nb = -1;
         if (lane == 0) nb = nL;
@@ -366,23 +372,30 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
         if (nb >= 0) spin_geq(flags + (long)nb * kTileFlagStride, target_step, t.err);
         if (lane == 6 && kd >= k0) {
             const int slot = (int)(kd % kTileSlots);
-            spin_eq64(t.dseq + (long)pair * kTileSlots + slot, (unsigned long long)(kd + 1), t.err);
-        }
-        __syncwarp();
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        if (lane == 6 && kd >= k0) {
-            const double* d = t.dec + ((long)pair * kTileSlots + (int)(kd % kTileSlots)) * 2;
-            if (__ldcg(d + 1) != 0.0) {
+            const unsigned long long v =
+                spin_tag64(t.dseq + (long)pair * kTileSlots + slot, (unsigned long long)(kd + 1), t.err);
+            if (v & 1ull) {
                 s_stop = 1;
                 s_stop_at = kd;
-                s_fpr = __ldcg(d);
+                s_fpr = __ldcg(t.dec + ((long)pair * kTileSlots + slot) * 2);
             }
         }
+        __syncwarp();
     };
 
+    // diagnostics (W1MG_TILE_DEBUG): per-tile cycles spent in each segment
+    // of steps 8..135, thread 0
+    long long dbg_acc[kTileDbgPts] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long dbg_last = clock64();
+#define STAMP(pt)                                                    \
+    if (t.dbg && tid == 0) {                                         \
+        const long long now_ = clock64();                            \
+        if (step >= 8 && step < 136) dbg_acc[pt] += now_ - dbg_last; \
+        dbg_last = now_;                                             \
+    }
     for (;;) {
         if (replay && k >= target) break;
-        if (t.dbg && tile == 0 && tid == 0 && step < kTileDbgSteps) t.dbg[(step) * kTileDbgPts + 0] = clock64();
+        STAMP(0);
         // ---- phase A: fluxes of owned nodes + recomputed left / bottom halo,
         // two nodes per thread per pass (independent chains for the scheduler)
         double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
@@ -443,7 +456,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
         if (cntA > kTileThreads) phaseA(std::integral_constant<int, 2>{});
         else phaseA(std::integral_constant<int, 1>{});
         __syncthreads();
-        if (t.dbg && tile == 0 && tid == 0 && step < kTileDbgSteps) t.dbg[(step) * kTileDbgPts + 1] = clock64();
+        STAMP(1);
         // ---- phase B: potential of owned nodes (row_update's divergence order)
         auto phaseB = [&](auto U_) {
             constexpr int UU = decltype(U_)::value;
@@ -492,7 +505,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
             wred[warp][2] = s_cr;
         }
         __syncthreads();
-        if (t.dbg && tile == 0 && tid == 0 && step < kTileDbgSteps) t.dbg[(step) * kTileDbgPts + 2] = clock64();
+        STAMP(2);
         ++k;
         ++step;
         const bool ckpt = !replay && ((k - k0) % kTileCk) == 0;
@@ -521,11 +534,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
             asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(t.cnt + (long)pair * kTileSlots + slot)
                          : "memory");
         }
-        if (t.dbg && tile == 0 && tid == 0 && step - 1 < kTileDbgSteps) t.dbg[(step - 1) * kTileDbgPts + 5] = clock64();
+        STAMP(5);
         // ---- wait: neighbours done with this step; decision of sweep k - lag
         if (warp == 0) wait_neighbours(step, replay ? k0 - 1 : k - kTileLag);
         __syncthreads();
-        if (t.dbg && tile == 0 && tid == 0 && step - 1 < kTileDbgSteps) t.dbg[(step - 1) * kTileDbgPts + 3] = clock64();
+        STAMP(3);
         if (!replay && s_stop) {
             // sweep s = s_stop_at stopped: restore the checkpoint at or below
             // s + 1 and replay to exactly s + 1 (every tile does the same)
@@ -541,13 +554,16 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
         }
         load_halo((int)(step & 1));
         __syncthreads();
-        if (t.dbg && tile == 0 && tid == 0 && step - 1 < kTileDbgSteps) t.dbg[(step - 1) * kTileDbgPts + 4] = clock64();
+        STAMP(4);
     }
     // every neighbour finished its replay (and so its checkpoint reads)
     // before the final state goes into buffer 0
     if (warp == 0) wait_neighbours(step, k0 - 1);
     __syncthreads();
     store_state(0);
+    if (t.dbg && tid == 0)
+        for (int q = 0; q < kTileDbgPts; ++q) t.dbg[tile * kTileDbgPts + q] = dbg_acc[q];
+#undef STAMP
     if (tile == 0 && tid == 0) {
         ctl->it = stop_at + 1;
         ctl->fpr = fin_fpr;
