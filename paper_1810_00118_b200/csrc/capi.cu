@@ -590,7 +590,8 @@ int w1mg_rn_selftest(w1mg_ctx* c, long count, unsigned long long seed, double mu
         if (count < 0 || !(mu > 0.0)) fail(W1MG_EINVAL, "rn_selftest: bad arguments");
         auto* d = c->get<unsigned long long>("selftest.bad", 3);
         CK(cudaMemsetAsync(d, 0, 3 * sizeof(unsigned long long), c->stream));
-        rn_selftest_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(count, seed, mu, d);
+        rn_selftest_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(count, seed, mu,
+                                                                  shrink_zero_threshold(mu), d);
         ++c->launches;
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(bad, d, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));

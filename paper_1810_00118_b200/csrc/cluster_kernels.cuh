@@ -98,7 +98,7 @@ cp_cluster_kernel(const SweepArgs a, const int C) {
         }
     }
     __shared__ double wred[kClusterThreads / 32][3];
-    const double mu = a.mu, tau = a.tau, ih = a.ih;
+    const double mu = a.mu, zt = a.zt, tau = a.tau, ih = a.ih;
     long it = ctl->it;
     const long max_it = ctl->max_it;
     const double tol = ctl->tol;
@@ -118,7 +118,7 @@ cp_cluster_kernel(const SweepArgs a, const int C) {
                 double pu = 0.0;
                 if (hy) pu = (jl + 1 < nr) ? phi[k + W] : up_phi[i];
                 double ux, uy, dx, dy;
-                node_flux<PN>(hx, hy, pc, pr, pu, mx[k], my[k], mu, ih, ux, uy, dx, dy);
+                node_flux<PN>(hx, hy, pc, pr, pu, mx[k], my[k], mu, zt, ih, ux, uy, dx, dy);
                 mx[k] = ux;
                 my[k] = uy;
                 ddx[k] = dx;

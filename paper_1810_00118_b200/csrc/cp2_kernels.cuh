@@ -190,7 +190,7 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
         const bool in = kInt || ((i >= 0) && (i <= n));
         const bool hx = kInt || ((i >= 0) && (i < n));
         const bool own = (lane >= 2) && (lane <= 30) && in;
-        const double mu = a.mu, tau = a.tau, ih = a.ih;
+        const double mu = a.mu, zt = a.zt, tau = a.tau, ih = a.ih;
 
         const int ilo = cx * kOwn2 - 2;  // column of lane 0 (warp-uniform)
         const int a0 = ilo & ~1;  // 16-B aligned box / chunk start (TMA requirement)
@@ -235,7 +235,7 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
             double mxo = hx ? __ldg(mxr + o) : 0.0;
             double myo = in ? __ldg(myr + o) : 0.0;
             double ux, uy, dx, dy;
-            node_flux<PN>(hx, in, pc, pr, pu, mxo, myo, mu, ih, ux, uy, dx, dy);
+            node_flux<PN>(hx, in, pc, pr, pu, mxo, myo, mu, zt, ih, ux, uy, dx, dy);
             uyA = uy;
             dyA = dy;
         }
@@ -287,7 +287,7 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                     issue(st, rA + kStages);
                 }
                 // ---- sweep A at row rA
-                node_flux<PN>(hx, hy, pc, pr, pu, mxo, myo, mu, ih, uxA, uyAn, dxA, dyAn);
+                node_flux<PN>(hx, hy, pc, pr, pu, mxo, myo, mu, zt, ih, uxA, uyAn, dxA, dyAn);
                 const double uxl = __shfl_up_sync(0xffffffffu, uxA, 1);
                 const double dxl = __shfl_up_sync(0xffffffffu, dxA, 1);
                 const double divm = (uxA - uxl) * ih + (uyAn - uyA) * ih;
@@ -309,7 +309,7 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                 const double prB = __shfl_down_sync(0xffffffffu, fA_prev, 1);
                 const double puB = hyB ? fA : 0.0;
                 double ux, uy, dx, dy;
-                node_flux<PN>(hx, hyB, pcB, hx ? prB : 0.0, puB, mxA_prev, myA_prev, mu, ih,
+                node_flux<PN>(hx, hyB, pcB, hx ? prB : 0.0, puB, mxA_prev, myA_prev, mu, zt, ih,
                                    ux, uy, dx, dy);
                 const double uxl = __shfl_up_sync(0xffffffffu, ux, 1);
                 const double dxl = __shfl_up_sync(0xffffffffu, dx, 1);

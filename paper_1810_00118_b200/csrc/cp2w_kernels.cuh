@@ -61,7 +61,7 @@ __device__ __forceinline__ void march2w(const SweepArgs& a, int pair, int parity
     }
     own[0] = (lane >= 2) && in[0];
     own[1] = (lane <= 30) && in[1];
-    const double mu = a.mu, tau = a.tau, ih = a.ih;
+    const double mu = a.mu, zt = a.zt, tau = a.tau, ih = a.ih;
 
     const int a0 = ilo & ~1;
     const int sh = ilo - a0;
@@ -100,7 +100,7 @@ __device__ __forceinline__ void march2w(const SweepArgs& a, int pair, int parity
             double mx_ = hx[s] ? __ldg(mxr + o) : 0.0;
             double my_ = in[s] ? __ldg(myr + o) : 0.0;
             double ux, uy, dx, dy;
-            node_flux<PN>(hx[s], in[s], c_, r_, u_, mx_, my_, mu, ih, ux, uy, dx, dy);
+            node_flux<PN>(hx[s], in[s], c_, r_, u_, mx_, my_, mu, zt, ih, ux, uy, dx, dy);
             uyA[s] = uy;
             dyA[s] = dy;
         }
@@ -143,7 +143,7 @@ __device__ __forceinline__ void march2w(const SweepArgs& a, int pair, int parity
 #pragma unroll
             for (int s = 0; s < 2; ++s) {
                 const bool hy = kInt || (in[s] && (rA < n));
-                node_flux<PN>(hx[s], hy, pc[s], pr[s], pu[s], mxo[s], myo[s], mu, ih, uxA[s],
+                node_flux<PN>(hx[s], hy, pc[s], pr[s], pu[s], mxo[s], myo[s], mu, zt, ih, uxA[s],
                               uyAn[s], dxA[s], dyAn[s]);
             }
             double uxl[2], dxl[2];
@@ -173,7 +173,7 @@ __device__ __forceinline__ void march2w(const SweepArgs& a, int pair, int parity
             for (int s = 0; s < 2; ++s) {
                 const bool hyB = kInt || (in[s] && (rB < n));
                 node_flux<PN>(hx[s], hyB, fA_prev[s], hx[s] ? prB[s] : 0.0, hyB ? fA[s] : 0.0,
-                              mxA_prev[s], myA_prev[s], mu, ih, ux[s], uy[s], dx[s], dy[s]);
+                              mxA_prev[s], myA_prev[s], mu, zt, ih, ux[s], uy[s], dx[s], dy[s]);
             }
             double uxl[2], dxl[2];
             shfl_left2(ux[0], ux[1], lane, uxl[0], uxl[1]);

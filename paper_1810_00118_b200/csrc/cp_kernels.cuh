@@ -68,6 +68,7 @@ struct SweepArgs {
     double* red_out;    // slab mode: last block writes its pair's 3 local sums here
     int ntiles;         // ncx * nsy
     double mu, tau, ih, h2;
+    double zt;          // largest s with sqrt_rn(s) <= mu: the p = 2 shrink's zero test (host, exact)
     PairCtl* ctl;       // [pairs]
     double* partial;    // [pairs][gridDim.x][3]
     unsigned* ticket;   // [pairs]
@@ -122,12 +123,12 @@ constexpr int kTmaSmem = kSweepWarps * (kStages * kStageBytes + kStages * 8);
 // divergent region per node, so the scheduler can interleave nodes.
 template <int PN, bool kNB = true>
 __device__ __forceinline__ void node_flux(bool hx, bool hy, double pc, double pr, double pu,
-                                          double mxo, double myo, double mu, double ih,
+                                          double mxo, double myo, double mu, double zt, double ih,
                                           double& ux, double& uy, double& dx, double& dy) {
     double vx = hx ? mxo - mu * ((pc - pr) * ih) : 0.0;
     double vy = hy ? myo - mu * ((pc - pu) * ih) : 0.0;
     if constexpr (kNB && PN == 1) {
-        shrink2_nb(vx, vy, mu, ux, uy);
+        shrink2_nb(vx, vy, mu, zt, ux, uy);
     } else {
         shrink<PN>(vx, vy, mu, ux, uy);
     }
@@ -191,7 +192,7 @@ __device__ __forceinline__ void below_row(const SweepArgs& a, const Strip& s, in
     double mxo = s.hx ? __ldg(s.mxr + o) : 0.0;
     double myo = s.in ? __ldg(s.myr + o) : 0.0;
     double ux, uy, dx, dy;
-    node_flux<PN>(s.hx, s.in, pc, pr, pu, mxo, myo, a.mu, a.ih, ux, uy, dx, dy);
+    node_flux<PN>(s.hx, s.in, pc, pr, pu, mxo, myo, a.mu, a.zt, a.ih, ux, uy, dx, dy);
     uyb = uy;
     dyb = dy;
 }
@@ -206,7 +207,7 @@ __device__ __forceinline__ void row_update(const SweepArgs& a, const Strip& s, i
     const bool hy = s.in && (j < a.L.n);
     const double ih = a.ih;
     double ux, uy, dx, dy;
-    node_flux<PN>(s.hx, hy, pc, pr, pu, mxo, myo, a.mu, ih, ux, uy, dx, dy);
+    node_flux<PN>(s.hx, hy, pc, pr, pu, mxo, myo, a.mu, a.zt, ih, ux, uy, dx, dy);
     double uxl = __shfl_up_sync(0xffffffffu, ux, 1);
     double dxl = __shfl_up_sync(0xffffffffu, dx, 1);
     double divm = (ux - uxl) * ih + (uy - uyb) * ih;
@@ -606,7 +607,7 @@ cp_resident_kernel(const SweepArgs a) {
     }
     __shared__ double red[kResidentThreads / 32][3];
     __shared__ int stop;
-    const double mu = a.mu, tau = a.tau, ih = a.ih;
+    const double mu = a.mu, zt = a.zt, tau = a.tau, ih = a.ih;
     long it = ctl->it;
     const long max_it = ctl->max_it;
     const double tol = ctl->tol;
@@ -622,7 +623,7 @@ cp_resident_kernel(const SweepArgs a) {
                 const double pr = hx ? phi[k + 1] : 0.0;
                 const double pu = hy ? phi[k + W] : 0.0;
                 double ux, uy, dx, dy;
-                node_flux<PN>(hx, hy, pc, pr, pu, mx[k], my[k], mu, ih, ux, uy, dx, dy);
+                node_flux<PN>(hx, hy, pc, pr, pu, mx[k], my[k], mu, zt, ih, ux, uy, dx, dy);
                 mx[k] = ux;
                 my[k] = uy;
                 ddx[k] = dx;

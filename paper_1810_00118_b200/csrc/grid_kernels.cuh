@@ -47,7 +47,7 @@ __device__ __forceinline__ void below_row_cg(const SweepArgs& a, const Strip& s,
     double mxo = s.hx ? __ldcg(s.mxr + o) : 0.0;
     double myo = s.in ? __ldcg(s.myr + o) : 0.0;
     double ux, uy, dx, dy;
-    node_flux<PN>(s.hx, s.in, pc, pr, pu, mxo, myo, a.mu, a.ih, ux, uy, dx, dy);
+    node_flux<PN>(s.hx, s.in, pc, pr, pu, mxo, myo, a.mu, a.zt, a.ih, ux, uy, dx, dy);
     uyb = uy;
     dyb = dy;
 }

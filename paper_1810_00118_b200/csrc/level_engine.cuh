@@ -133,6 +133,7 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     a.jhi = jhi;
     a.red_out = nullptr;
     a.mu = mu;
+    a.zt = shrink_zero_threshold(mu);
     a.tau = tau;
     const double h = 1.0 / n;
     a.ih = 1.0 / h;  // inv_h, grid.cpp:48/79

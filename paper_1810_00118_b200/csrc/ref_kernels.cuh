@@ -82,7 +82,7 @@ __device__ double rn_operand(unsigned long long& st, double scale) {
     return (((r >> 40) & 1) ? -1.0 : 1.0) * scale * ldexp(u, e);
 }
 
-__global__ void rn_selftest_kernel(long count, unsigned long long seed, double mu,
+__global__ void rn_selftest_kernel(long count, unsigned long long seed, double mu, double zt,
                                    unsigned long long* bad) {
     unsigned long long nb_sqrt = 0, nb_div = 0, nb_shr = 0;
     for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < count;
@@ -97,7 +97,7 @@ __global__ void rn_selftest_kernel(long count, unsigned long long seed, double m
         const double fq = div_rn_fast(mu, s, ok);
         if (ok && !same_bits(fq, mu / s)) ++nb_div;
         double ux, uy, vx, vy;
-        shrink2_nb(a, b, mu, ux, uy);
+        shrink2_nb(a, b, mu, zt, ux, uy);
         shrink<1>(a, b, mu, vx, vy);
         if (!same_bits(ux, vx) || !same_bits(uy, vy)) ++nb_shr;
     }

@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
     double* rho = sm + 5 * S;
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
-    const double mu = a.mu, tau = a.tau, ih = a.ih;
+    const double mu = a.mu, zt = a.zt, tau = a.tau, ih = a.ih;
 
     // neighbours (tile index within the pair, -1 = none)
     const int nL = tc > 0 ? tile - 1 : -1;
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
                 double ux[2], uy[2], dx[2], dy[2];
 #pragma unroll
                 for (int u = 0; u < UU; ++u)
-                    node_flux<PN>(hx[u], hy[u], pc[u], pr[u], pu[u], mo[u], no[u], mu, ih, ux[u], uy[u],
+                    node_flux<PN>(hx[u], hy[u], pc[u], pr[u], pu[u], mo[u], no[u], mu, zt, ih, ux[u], uy[u],
                                   dx[u], dy[u]);
 #pragma unroll
                 for (int u = 0; u < UU; ++u) {
