@@ -25,7 +25,7 @@ rows = {
 p = os.path.join(ROOT, "profiles", "r1_summary.md")
 out, latest = [], True
 for line in open(p).read().split("\n"):
-    if line.startswith("## First capture"):
+    if line.startswith("## First capture") or line.startswith("## Earlier captures"):
         latest = False  # historical sections keep their numbers
     if latest:
         for k, v in rows.items():
