@@ -294,7 +294,8 @@ int w1mg_set_pdhg_small(int mode);
  * in PDHG iterations: 1 = odd m >= 400 (default), 2 = every odd m, 0 = off),
  * "pdhg_small" (0-2),
  * "cluster_pick" (0/1), "compact" (0/1), "compact_step" (>= 1),
- * "warps_per_sm" (strip target, default 32), "tmap_nw" (2/4/8).
+ * "warps_per_sm" (strip target, default 32), "tmap_nw" (2/4/8, 0 = auto),
+ * "tile" (0-2), "tile_min", "tile_max", "tile_grid".
  * W1MG_EINVAL for an unknown name or value. */
 int w1mg_set_option(const char* name, long value);
 /* Times the fused sweep kernel alone: `iters` sweeps over B pairs of an

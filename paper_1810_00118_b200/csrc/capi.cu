@@ -79,7 +79,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
             const int w = std::atoi(v);
-            g_tmap_nw = (w == 2 || w == 8) ? w : kWarpsT;
+            g_tmap_nw = (w == 2 || w == 4 || w == 8) ? w : 0;
         }
         auto* c = new w1mg_ctx();
         c->device = device;
@@ -564,7 +564,7 @@ int w1mg_set_option(const char* name, long value) {
     else if (k == "compact_step" && v >= 1) g_compact_step = v;
     else if (k == "warps_per_sm" && v >= 1) g_warps_per_sm = v;
     else if (k == "pdl" && (v == 0 || v == 1)) g_pdl = v;
-    else if (k == "tmap_nw" && (v == 2 || v == 4 || v == 8)) g_tmap_nw = v;
+    else if (k == "tmap_nw" && (v == 0 || v == 2 || v == 4 || v == 8)) g_tmap_nw = v;
     else if (k == "tile" && v >= 0 && v <= 2) g_tile = v;
     else if (k == "tile_min" && v >= 1) g_tile_min = v;
     else if (k == "tile_max" && v >= 1) g_tile_max = v;

@@ -25,7 +25,8 @@ struct Level {
     dim3 grid2;
     SweepArgs args2w{};  // two-sweep engine, two column sets per lane
     dim3 grid2w;
-    dim3 grid2t;  // two-sweep tensor-map engine (args2 geometry, kWarpsT-warp blocks)
+    dim3 grid2t;  // two-sweep tensor-map engine (args2 geometry, tmap_nw-warp blocks)
+    int tmap_nw = kWarpsT;
     bool slab = false;  // row slab of a decomposed grid (one-sweep engine only)
     int* act = nullptr;   // [B] running pairs of a compacted launch (null: B == 1 or slab)
     int* nact = nullptr;  // their count
@@ -74,8 +75,11 @@ void mirror_rho(w1mg_ctx* c, const Level& lv) {
 // strip-height target: enough strips for this many warps per SM (W1MG_WARPS_PER_SM)
 int g_warps_per_sm = 32;
 
-// warps per block of the tensor-map two-sweep kernel (W1MG_TMAP_NW = 2|4|8)
-int g_tmap_nw = kWarpsT;
+// warps per block of the tensor-map two-sweep kernel (W1MG_TMAP_NW = 2|4|8;
+// 0 = auto: 8 for a launch over ONE pair of a 384..640 level -- one-pair
+// 512^2 level 33.4 -> 30.9 ms, while the 256^2 one is 4 % slower and batches
+// prefer 4, measured with tools/gpu/sp_engines.sh and nw.sh -- else 4)
+int g_tmap_nw = 0;
 
 // Strip geometry of the three streaming engines for a launch over `pairs`
 // pairs: the tallest strips (<= 64 rows) that still give about 32 warps per
@@ -102,7 +106,8 @@ void set_geometry(Level& lv, int pairs, int num_sms) {
     lv.grid = dim3((lv.args.ntiles + kSweepWarps - 1) / kSweepWarps, pairs, 1);
     lv.grid2 = dim3((lv.args2.ntiles + kSweepWarps - 1) / kSweepWarps, pairs, 1);
     lv.grid2w = dim3((lv.args2w.ntiles + kWarpsW - 1) / kWarpsW, pairs, 1);
-    lv.grid2t = dim3((lv.args2.ntiles + g_tmap_nw - 1) / g_tmap_nw, pairs, 1);
+    lv.tmap_nw = g_tmap_nw ? g_tmap_nw : ((pairs == 1 && lv.n >= 384 && lv.n <= 640) ? 8 : kWarpsT);
+    lv.grid2t = dim3((lv.args2.ntiles + lv.tmap_nw - 1) / lv.tmap_nw, pairs, 1);
 }
 
 // jhi < 0: whole grid.  Otherwise a row slab owning global rows [jlo, jhi),
@@ -313,7 +318,7 @@ bool two_sweep(const Level& lv) {
 void launch_sweep2(const Level& lv, int pn, int parity, cudaStream_t s) {
     if (g_sweep_variant == kTma2T || g_sweep_variant == kAuto) {
         if (!lv.has_tmap) fail(W1MG_ELOGIC, "tensor-map sweep on a level without a map");
-        switch (g_tmap_nw) {
+        switch (lv.tmap_nw) {
             case 2: launch_tmap<2>(lv, pn, parity, s); break;
             case 8: launch_tmap<8>(lv, pn, parity, s); break;
             default: launch_tmap<4>(lv, pn, parity, s); break;

@@ -1,0 +1,4 @@
+set -x
+timeout 300 python tools/single_pair_profile.py > gpurun_out/single_pair.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_cp.py -x -q -p no:cacheprovider > gpurun_out/pytest_cl.log 2>&1; echo pytest $? >> gpurun_out/pytest_cl.log
+true
