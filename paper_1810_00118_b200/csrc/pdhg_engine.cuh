@@ -301,12 +301,17 @@ void launch_pdhg_small(w1mg_ctx* c, const PLevel& lv) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     if (!(attr >> (dev & 63) & 1ull)) {
-        CK(cudaFuncSetAttribute(pdhg_small_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)pdhg_small_smem(kPdhgSmallMaxM)));
+        const int mx = (int)std::max(pdhg_small_smem(kPdhgSmallMaxM), pdhg_small_smem(kPdhgStateM));
+        CK(cudaFuncSetAttribute(pdhg_small_kernel<Q, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        CK(cudaFuncSetAttribute(pdhg_small_kernel<Q, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         attr |= 1ull << (dev & 63);
     }
-    pdhg_small_kernel<Q><<<lv.B, kPdhgSmallThreads, pdhg_small_smem(lv.n + 1), c->stream>>>(
-        lv.args, lv.C, lv.S, lv.lam);
+    if (lv.n + 1 <= kPdhgStateM)
+        pdhg_small_kernel<Q, true><<<lv.B, kPdhgSmallThreads, pdhg_small_smem(lv.n + 1), c->stream>>>(
+            lv.args, lv.C, lv.S, lv.lam);
+    else
+        pdhg_small_kernel<Q, false><<<lv.B, kPdhgSmallThreads, pdhg_small_smem(lv.n + 1), c->stream>>>(
+            lv.args, lv.C, lv.S, lv.lam);
     CK(cudaGetLastError());
     ++c->launches;
 }

@@ -28,42 +28,50 @@ constexpr int kPdhgSmallMaxM = 65;  // shared-memory capacity of the kernel
 // the engine is used up to m = kPdhgSmallAutoM.
 constexpr int kPdhgSmallAutoM = 33;
 
-__host__ __device__ inline long pdhg_small_smem(int m) { return 4L * m * m * 8; }
-
-// Out(k, j) = alpha * sum_l A(k, l) * Bop(l, j); m x m column-major in shared
-// memory; Bop = B (BT = false) or B^T (BT = true).  2 x 4 output tile per
-// thread: 6 shared loads (4 of them warp broadcasts) per 8 FMAs.
-template <bool BT>
-__device__ __forceinline__ void smem_gemm(double* __restrict__ Out, const double* __restrict__ A,
-                                          const double* __restrict__ B, int m, double alpha) {
-    const int kt = (m + 1) / 2, jt = (m + 3) / 4;
-    for (int t = threadIdx.x; t < kt * jt; t += blockDim.x) {
-        const int k0 = (t % kt) * 2, j0 = (t / kt) * 4;
-        const bool k1ok = k0 + 1 < m;
-        double acc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
-        for (int l = 0; l < m; ++l) {
-            const double a0 = A[k0 + l * m];
-            const double a1 = k1ok ? A[k0 + 1 + l * m] : 0.0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int j = j0 + q;
-                const double bq = (j < m) ? (BT ? B[j + l * m] : B[l + j * m]) : 0.0;
-                acc[0][q] = fma(a0, bq, acc[0][q]);
-                acc[1][q] = fma(a1, bq, acc[1][q]);
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int j = j0 + q;
-            if (j < m) {
-                Out[k0 + j * m] = alpha * acc[0][q];
-                if (k1ok) Out[k0 + 1 + j * m] = alpha * acc[1][q];
-            }
-        }
-    }
+// levels up to kPdhgStateM also keep the pair's state (m, varphi, varphi_bar,
+// rho: 7 arrays) in shared memory for the whole level
+constexpr int kPdhgStateM = 33;
+__host__ __device__ inline long pdhg_small_smem(int m) {
+    return (m <= kPdhgStateM ? 11L : 4L) * m * m * 8;
 }
 
-template <int Q>
+// Out(k, j) = alpha * sum_l A(k, l) * Bop(l, j); m x m column-major in shared
+// memory; Bop = B (BT = false) or B^T (BT = true).  One row k and J columns
+// per thread (so m * ceil(m / J) <= blockDim threads cover the output in one
+// pass): consecutive threads take consecutive rows (conflict-free A loads),
+// the B operand is a warp broadcast.  Each output is the fma chain over
+// l = 0..m-1 from 0, the same order for every J.
+template <bool BT, int J>
+__device__ __forceinline__ void smem_gemm(double* __restrict__ Out, const double* __restrict__ A,
+                                          const double* __restrict__ B, int m, double alpha) {
+    const int jt = (m + J - 1) / J;
+    for (int t = threadIdx.x; t < m * jt; t += blockDim.x) {
+        const int k = t % m, j0 = (t / m) * J;
+        double acc[J];
+#pragma unroll
+        for (int q = 0; q < J; ++q) acc[q] = 0.0;
+        for (int l = 0; l < m; ++l) {
+            const double a0 = A[k + l * m];
+#pragma unroll
+            for (int q = 0; q < J; ++q) {
+                const int j = j0 + q;
+                const double bq = (j < m) ? (BT ? B[j + l * m] : B[l + j * m]) : 0.0;
+                acc[q] = fma(a0, bq, acc[q]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < J; ++q)
+            if (j0 + q < m) Out[k + (j0 + q) * m] = alpha * acc[q];
+    }
+}
+template <bool BT>
+__device__ __forceinline__ void smem_gemm_auto(double* Out, const double* A, const double* B, int m,
+                                               double alpha) {
+    if (m <= 45) smem_gemm<BT, 2>(Out, A, B, m, alpha);
+    else smem_gemm<BT, 5>(Out, A, B, m, alpha);
+}
+
+template <int Q, bool kS>
 __global__ void __launch_bounds__(kPdhgSmallThreads, 1)
 pdhg_small_kernel(const SweepArgs a, const double* __restrict__ Cg, const double* __restrict__ Sg,
                   const double* __restrict__ lam_g) {
@@ -86,13 +94,36 @@ pdhg_small_kernel(const SweepArgs a, const double* __restrict__ Cg, const double
         sS[k] = Sg[k];
     }
     if (tid < m) lam[tid] = lam_g[tid];
-    double* mx = pslot_w(a, b, P_MX);
-    double* my = pslot_w(a, b, P_MY);
-    double* px = pslot_w(a, b, P_PX);
-    double* py = pslot_w(a, b, P_PY);
-    double* bx = pslot_w(a, b, P_BX);
-    double* by = pslot_w(a, b, P_BY);
-    const double* rho = pslot(a, b, P_RHO);
+    double* gmx = pslot_w(a, b, P_MX);
+    double* gmy = pslot_w(a, b, P_MY);
+    double* gpx = pslot_w(a, b, P_PX);
+    double* gpy = pslot_w(a, b, P_PY);
+    double* gbx = pslot_w(a, b, P_BX);
+    double* gby = pslot_w(a, b, P_BY);
+    const double* grho = pslot(a, b, P_RHO);
+    // kS: the state lives in shared memory (dense, index k = j m + i, row
+    // stride m) for the whole level; else in the level buffer (L2-resident)
+    double* mx = kS ? sm + 4 * M2 : gmx;
+    double* my = kS ? sm + 5 * M2 : gmy;
+    double* px = kS ? sm + 6 * M2 : gpx;
+    double* py = kS ? sm + 7 * M2 : gpy;
+    double* bx = kS ? sm + 8 * M2 : gbx;
+    double* by = kS ? sm + 9 * M2 : gby;
+    double* srho = sm + 10 * M2;
+    const double* rho = kS ? srho : grho;
+    const int RS = kS ? m : P;  // row stride of the state arrays
+    if constexpr (kS) {
+        for (int k = tid; k < M2; k += blockDim.x) {
+            const long o = L.at(k % m, k / m);
+            mx[k] = gmx[o];
+            my[k] = gmy[o];
+            px[k] = gpx[o];
+            py[k] = gpy[o];
+            bx[k] = gbx[o];
+            by[k] = gby[o];
+            srho[k] = grho[o];
+        }
+    }
     const double mu = a.mu, tau = a.tau, ih = a.ih;
     const double scale = 1.0 / (4.0 * double(m) * double(m));  // poisson.cpp:93
     long it = ctl->it;
@@ -104,34 +135,34 @@ pdhg_small_kernel(const SweepArgs a, const double* __restrict__ Cg, const double
         // ---- pre: X = A v - rho, v = m - mu varphi_bar (pdhg_pre_kernel)
         for (int k = tid; k < M2; k += blockDim.x) {
             const int i = k % m, j = k / m;
-            const long o = L.at(i, j);
+            const long o = kS ? (long)k : L.at(i, j);
             const double r_ = (i < n) ? mx[o] - mu * bx[o] : 0.0;
             const double l_ = (i > 0) ? mx[o - 1] - mu * bx[o - 1] : 0.0;
             const double a_ = (j < n) ? my[o] - mu * by[o] : 0.0;
-            const double b_ = (j > 0) ? my[o - P] - mu * by[o - P] : 0.0;
+            const double b_ = (j > 0) ? my[o - RS] - mu * by[o - RS] : 0.0;
             const double div = (r_ - l_) * ih + (a_ - b_) * ih;
             X[k] = div - rho[o];
         }
         __syncthreads();
         // ---- Neumann Poisson solve (poisson.cpp:72-95)
-        smem_gemm<false>(T, sC, X, m, 1.0);
+        smem_gemm_auto<false>(T, sC, X, m, 1.0);
         __syncthreads();
-        smem_gemm<true>(X, T, sC, m, 1.0);
+        smem_gemm_auto<true>(X, T, sC, m, 1.0);
         __syncthreads();
         for (int k = tid; k < M2; k += blockDim.x) {
             const int k1 = k % m, k2 = k / m;
             X[k] = (k == 0) ? 0.0 : X[k] / (lam[k1] + lam[k2]);
         }
         __syncthreads();
-        smem_gemm<false>(T, sS, X, m, 1.0);
+        smem_gemm_auto<false>(T, sS, X, m, 1.0);
         __syncthreads();
-        smem_gemm<true>(X, T, sS, m, scale);
+        smem_gemm_auto<true>(X, T, sS, m, scale);
         __syncthreads();
         // ---- post: m, varphi, varphi_bar + Eq. 12 partials (pdhg_post_kernel)
         double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
         for (int k = tid; k < M2; k += blockDim.x) {
             const int i = k % m, j = k / m;
-            const long o = L.at(i, j);
+            const long o = kS ? (long)k : L.at(i, j);
             const bool hx = i < n, hy = j < n;
             const double pc = X[k];
             double mnx = 0.0, mny = 0.0, dmx = 0.0, dmy = 0.0, pox = 0.0, poy = 0.0;
@@ -197,6 +228,17 @@ pdhg_small_kernel(const SweepArgs a, const double* __restrict__ Cg, const double
         if (stop_s) break;
         // the node phase of the next iteration rewrites state read above only
         // after these barriers; global writes of this CTA are visible to it
+    }
+    if constexpr (kS) {
+        for (int k = tid; k < M2; k += blockDim.x) {
+            const long o = L.at(k % m, k / m);
+            gmx[o] = mx[k];
+            gmy[o] = my[k];
+            gpx[o] = px[k];
+            gpy[o] = py[k];
+            gbx[o] = bx[k];
+            gby[o] = by[k];
+        }
     }
     if (tid == 0) {
         ctl->it = it;
