@@ -307,10 +307,10 @@ void launch_pdhg_small(w1mg_ctx* c, const PLevel& lv) {
         attr |= 1ull << (dev & 63);
     }
     if (lv.n + 1 <= kPdhgStateM)
-        pdhg_small_kernel<Q, true><<<lv.B, kPdhgSmallThreads, pdhg_small_smem(lv.n + 1), c->stream>>>(
+        pdhg_small_kernel<Q, true><<<lv.B, pdhg_small_threads(lv.n + 1), pdhg_small_smem(lv.n + 1), c->stream>>>(
             lv.args, lv.C, lv.S, lv.lam);
     else
-        pdhg_small_kernel<Q, false><<<lv.B, kPdhgSmallThreads, pdhg_small_smem(lv.n + 1), c->stream>>>(
+        pdhg_small_kernel<Q, false><<<lv.B, pdhg_small_threads(lv.n + 1), pdhg_small_smem(lv.n + 1), c->stream>>>(
             lv.args, lv.C, lv.S, lv.lam);
     CK(cudaGetLastError());
     ++c->launches;

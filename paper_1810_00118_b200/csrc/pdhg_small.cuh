@@ -20,7 +20,10 @@
 
 namespace w1mg_dev {
 
-constexpr int kPdhgSmallThreads = 1024;
+constexpr int kPdhgSmallThreads = 1024;  // launch bound; the launch uses pdhg_small_threads(m)
+// threads per CTA: at m = 33, 576 (18 warps) balance the 1089-node phases (two
+// passes) and the 561 DCT GEMM tiles (ncu: barrier stalls dominated with 1024)
+__host__ __device__ inline int pdhg_small_threads(int m) { return m <= 33 ? 576 : 1024; }
 constexpr int kPdhgSmallMaxM = 65;  // shared-memory capacity of the kernel
 // Measured on one B200 (config 3 levels, tools/configs.py 3): 33^2 level
 // 13.7 us per iteration vs 19 us streaming; 65^2 level 50 us vs 21 us (the
@@ -214,7 +217,7 @@ pdhg_small_kernel(const SweepArgs a, const double* __restrict__ Cg, const double
         __syncthreads();
         if (tid == 0) {
             double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-            for (int w = 0; w < kPdhgSmallThreads / 32; ++w) {
+            for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
                 t0 += wred[w][0];
                 t1 += wred[w][1];
                 t2 += wred[w][2];
