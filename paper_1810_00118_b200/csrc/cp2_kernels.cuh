@@ -257,14 +257,17 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
 
         // One step of the march: sweep A at row rA0 + t, sweep B one row behind.
         // mode: 0 = decide at run time whether sweep B has a row (rB >= rA0),
-        // 1 = first step (no B row yet), 2 = a later step (B always runs).
+        // 1 = first step (no B row yet), 2 = a later step (B always runs),
+        // 3 = a middle step (2 <= t < j1 - rA0: A's and B's rows are owned
+        // rows of the grid, so the residual sums accumulate without row
+        // tests or selects; lanes that own no column are zeroed at the end).
         auto step = [&](const int t, auto mode) {
             constexpr int kMode = decltype(mode)::value;
             const int rA = rA0 + t;  // A row of this step (rA == n+1: virtual)
             const int rB = rA - 1;   // B row of this step
             double fA = 0.0, uxA = 0.0, uyAn = 0.0, dxA = 0.0, dyAn = 0.0, r = 0.0;
             double pu = 0.0, pur = 0.0;
-            if (kInt || rA <= rA1) {
+            if (kMode == 3 || kInt || rA <= rA1) {
                 const int st = t % kStages;
                 const double* c = ring + st * kStreams * kChunk + sh + lane;
                 const double* cph = c;  // phi^k(row rA+1)
@@ -294,7 +297,7 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                 const double divd = (dxA - dxl) * ih + (dyAn - dyA) * ih;
                 const double d = tau * (divm + divd - r);
                 fA = pc + d;
-                if (own && rA >= j0 && rA < j1) {
+                if (kMode == 3 || (own && rA >= j0 && rA < j1)) {
                     a_dm2 = __fma_rn(dyAn, dyAn, __fma_rn(dxA, dxA, a_dm2));
                     a_dp2 = __fma_rn(d, d, a_dp2);
                     a_cr = __fma_rn(d, divd, a_cr);
@@ -303,7 +306,7 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                 dyA = dyAn;
             }
             // ---- sweep B at row rB (inputs: A's rows rB and rB+1)
-            if (kMode == 2 || (kMode == 0 && rB >= rA0)) {
+            if (kMode >= 2 || (kMode == 0 && rB >= rA0)) {
                 const bool hyB = kInt || (in && (rB < n));
                 const double pcB = fA_prev;
                 const double prB = __shfl_down_sync(0xffffffffu, fA_prev, 1);
@@ -316,11 +319,13 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                 const double divm = (ux - uxl) * ih + (uy - uyB) * ih;
                 const double divd = (dx - dxl) * ih + (dy - dyB) * ih;
                 const double d = tau * (divm + divd - r_prev);
-                if (own && rB >= j0) {  // rB < j1 always
+                if (own && (kMode == 3 || rB >= j0)) {  // rB < j1 always
                     const long ob = o - P;
                     phw[ob] = pcB + d;
                     if (hx) mxw[ob] = ux;
                     if (hyB) myw[ob] = uy;
+                }
+                if (kMode == 3 || (own && rB >= j0)) {
                     b_dm2 = __fma_rn(dy, dy, __fma_rn(dx, dx, b_dm2));
                     b_dp2 = __fma_rn(d, d, b_dp2);
                     b_cr = __fma_rn(d, divd, b_cr);
@@ -341,14 +346,26 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
         // (80-register cap -> 3 spilled doubles), so it is a variant.
         // (peeling the first step helps the rolled loop; the unrolled one
         //  allocates registers better with the run-time test, measured)
+        // steps 0, 1 and the last one test rows at run time; the middle ones
+        // (mode 3) are row-test free
+        const int T = j1 - rA0;
+        step(0, std::integral_constant<int, 1>{});
+        o += P;
+        if (T >= 1) {
+            step(1, std::integral_constant<int, 0>{});
+            o += P;
+        }
         if constexpr (kUnroll) {
 #pragma unroll 2
-            for (int t = 0; t <= j1 - rA0; ++t, o += P) step(t, std::integral_constant<int, 0>{});
+            for (int t = 2; t < T; ++t, o += P) step(t, std::integral_constant<int, 3>{});
         } else {
-            step(0, std::integral_constant<int, 1>{});
-            o += P;
 #pragma unroll 1
-            for (int t = 1; t <= j1 - rA0; ++t, o += P) step(t, std::integral_constant<int, 2>{});
+            for (int t = 2; t < T; ++t, o += P) step(t, std::integral_constant<int, 3>{});
+        }
+        if (T >= 2) step(T, std::integral_constant<int, 0>{});
+        if (!own) {  // mode-3 steps accumulated every lane
+            a_dm2 = a_dp2 = a_cr = 0.0;
+            b_dm2 = b_dp2 = b_cr = 0.0;
         }
     }
 }
