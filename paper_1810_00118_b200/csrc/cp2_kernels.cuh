@@ -240,6 +240,11 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
             dyA = dy;
         }
         long o = L.at(i, rA0);
+        // B's stores go one row below A: running pointers, advanced one row
+        // per step (64-bit address math once, not per store)
+        double* __restrict__ wph = phw + (o - P);
+        double* __restrict__ wmx = mxw + (o - P);
+        double* __restrict__ wmy = myw + (o - P);
         double pc, pr;  // phi^k(i, r), phi^k(i+1, r)
         if constexpr (kTM) {
             mbar_wait(&bars[0], 0u);
@@ -320,10 +325,9 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                 const double divd = (dx - dxl) * ih + (dy - dyB) * ih;
                 const double d = tau * (divm + divd - r_prev);
                 if (own && (kMode == 3 || rB >= j0)) {  // rB < j1 always
-                    const long ob = o - P;
-                    phw[ob] = pcB + d;
-                    if (hx) mxw[ob] = ux;
-                    if (hyB) myw[ob] = uy;
+                    *wph = pcB + d;
+                    if (hx) *wmx = ux;
+                    if (hyB) *wmy = uy;
                 }
                 if (kMode == 3 || (own && rB >= j0)) {
                     b_dm2 = __fma_rn(dy, dy, __fma_rn(dx, dx, b_dm2));
@@ -349,18 +353,23 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
         // steps 0, 1 and the last one test rows at run time; the middle ones
         // (mode 3) are row-test free
         const int T = j1 - rA0;
+        auto next_row = [&] {
+            wph += P;
+            wmx += P;
+            wmy += P;
+        };
         step(0, std::integral_constant<int, 1>{});
-        o += P;
+        next_row();
         if (T >= 1) {
             step(1, std::integral_constant<int, 0>{});
-            o += P;
+            next_row();
         }
         if constexpr (kUnroll) {
 #pragma unroll 2
-            for (int t = 2; t < T; ++t, o += P) step(t, std::integral_constant<int, 3>{});
+            for (int t = 2; t < T; ++t, next_row()) step(t, std::integral_constant<int, 3>{});
         } else {
 #pragma unroll 1
-            for (int t = 2; t < T; ++t, o += P) step(t, std::integral_constant<int, 3>{});
+            for (int t = 2; t < T; ++t, next_row()) step(t, std::integral_constant<int, 3>{});
         }
         if (T >= 2) step(T, std::integral_constant<int, 0>{});
         if (!own) {  // mode-3 steps accumulated every lane
