@@ -30,6 +30,10 @@
 namespace w1mg_dev {
 
 constexpr int kOwn2 = 29;  // owned columns per warp in the two-sweep march
+// tensor-map ring: boxes of kBoxRows rows, kStagesT boxes in flight (6 rows
+// of look-ahead); one wait and one refill per two rows
+constexpr int kBoxRows = 2;
+constexpr int kStagesT = 3;
 
 // Block-wide sum of `count` 6-vectors at src (fixed order: thread-strided,
 // warp butterfly, then warps in order); the result is valid in thread 0.
@@ -197,15 +201,21 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
         const int sh = ilo - a0;
         const int zb = pair * NSLOT + PHI0 + parity;  // box planes zb, zb+2, zb+4, zb+6
         const long c0 = L.at(a0, 0);
+        // ring geometry: kTM boxes carry kBoxRows rows (box = rows
+        // rA0 + kBoxRows b ...), smem layout [plane][row][kChunk]
+        constexpr int NR = kTM ? kBoxRows : 1;  // rows per box
+        constexpr int NS = kTM ? kStagesT : kStages;  // boxes in the ring
+        constexpr int PS = NR * kChunk;          // plane stride in a stage
+        constexpr int STG = kStreams * PS;       // stage size (doubles)
         if (lane == 0) {
 #pragma unroll
-            for (int t = 0; t < kStages; ++t) mbar_init(&bars[t], 1);
+            for (int t = 0; t < NS; ++t) mbar_init(&bars[t], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncwarp();
         auto issue = [&](int st, int row) {
-            double* dst = ring + st * kStreams * kChunk;
-            mbar_expect_tx(&bars[st], kStageBytes);
+            double* dst = ring + st * STG;
+            mbar_expect_tx(&bars[st], NR * kStageBytes);
             if constexpr (kTM) {
                 tmap_g2s_3d(dst, tm, a0, row, zb, &bars[st]);
             } else {
@@ -220,9 +230,9 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
         const int rA0 = max(j0 - 1, 0);
         const int rA1 = min(j1, n);
         const int nA = rA1 - rA0 + 1;
-        const int nbox = kTM ? nA + 1 : nA;  // kTM: rows rA0 .. rA1+1
+        const int nbox = kTM ? (nA + NR) / NR : nA;  // kTM: rows rA0 .. rA1+1
         if (lane == 0) {
-            for (int t = 0; t < kStages && t < nbox; ++t) issue(t, rA0 + t);
+            for (int t = 0; t < NS && t < nbox; ++t) issue(t, rA0 + t * NR);
         }
 
         // A's y-flux below row rA0 (m-only warm-up, direct loads)
@@ -266,33 +276,45 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
         // 3 = a middle step (2 <= t < j1 - rA0: A's and B's rows are owned
         // rows of the grid, so the residual sums accumulate without row
         // tests or selects; lanes that own no column are zeroed at the end).
-        auto step = [&](const int t, auto mode) {
+        auto step = [&](const int t, auto mode, auto par) {
             constexpr int kMode = decltype(mode)::value;
+            constexpr int kPar = decltype(par)::value;  // 0 even t, 1 odd t, 2 run time
             const int rA = rA0 + t;  // A row of this step (rA == n+1: virtual)
             const int rB = rA - 1;   // B row of this step
             double fA = 0.0, uxA = 0.0, uyAn = 0.0, dxA = 0.0, dyAn = 0.0, r = 0.0;
             double pu = 0.0, pur = 0.0;
             if (kMode == 3 || kInt || rA <= rA1) {
-                const int st = t % kStages;
-                const double* c = ring + st * kStreams * kChunk + sh + lane;
+                // row t: m, rho (box t / NR, sub-row t % NR); phi^k of row t+1
+                const bool odd = (kPar == 0) ? false : (kPar == 1) ? true : ((t & 1) != 0);
+                const int bt = (NR == 2) ? (t >> 1) : t;
+                const int st = bt % NS;
+                const double* c = ring + st * STG + ((NR == 2 && odd) ? kChunk : 0) + sh + lane;
                 const double* cph = c;  // phi^k(row rA+1)
                 if constexpr (kTM) {
-                    const int su = (t + 1) % kStages;
-                    mbar_wait(&bars[su], (uint32_t)(((t + 1) / kStages) & 1));
-                    cph = ring + su * kStreams * kChunk + sh + lane;
+                    if (NR == 1 || odd) {  // row t+1 opens the next box
+                        const int bu = (NR == 2) ? ((t + 1) >> 1) : t + 1;
+                        const int su = bu % NS;
+                        mbar_wait(&bars[su], (uint32_t)((bu / NS) & 1));
+                        cph = ring + su * STG + sh + lane;
+                    } else {  // row t+1 is the second row of this box
+                        cph = c + kChunk;
+                    }
                 } else {
                     mbar_wait(&bars[st], (uint32_t)((t / kStages) & 1));
                 }
                 const bool hy = kInt || (in && (rA < n));
                 pu = hy ? cph[0] : 0.0;
                 pur = (kInt || (hx && rA < n)) ? cph[1] : 0.0;
-                const double mxo = hx ? c[kChunk] : 0.0;
-                const double myo = hy ? c[2 * kChunk] : 0.0;
-                r = in ? c[3 * kChunk] : 0.0;
-                __syncwarp();
-                if (lane == 0 && t + kStages < nbox) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    issue(st, rA + kStages);
+                const double mxo = hx ? c[PS] : 0.0;
+                const double myo = hy ? c[2 * PS] : 0.0;
+                r = in ? c[3 * PS] : 0.0;
+                // the box of row t is consumed after its last row: refill it
+                if (NR == 1 || odd) {
+                    __syncwarp();
+                    if (lane == 0 && bt + NS < nbox) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue(st, rA0 + (bt + NS) * NR);
+                    }
                 }
                 // ---- sweep A at row rA
                 node_flux<PN>(hx, hy, pc, pr, pu, mxo, myo, mu, zt, ih, uxA, uyAn, dxA, dyAn);
@@ -358,20 +380,43 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
             wmx += P;
             wmy += P;
         };
-        step(0, std::integral_constant<int, 1>{});
+        using M0 = std::integral_constant<int, 0>;
+        using M1 = std::integral_constant<int, 1>;
+        using M3 = std::integral_constant<int, 3>;
+        using PE = std::integral_constant<int, 0>;
+        using PO = std::integral_constant<int, 1>;
+        using PR = std::integral_constant<int, 2>;
+        step(0, M1{}, PE{});
         next_row();
         if (T >= 1) {
-            step(1, std::integral_constant<int, 0>{});
+            step(1, M0{}, PO{});
             next_row();
         }
+        // middle steps in (even, odd) pairs: the box position of each row is
+        // known at compile time
+        int t = 2;
         if constexpr (kUnroll) {
-#pragma unroll 2
-            for (int t = 2; t < T; ++t, next_row()) step(t, std::integral_constant<int, 3>{});
+#pragma unroll 1
+            for (; t + 1 < T; t += 2) {
+                step(t, M3{}, PE{});
+                next_row();
+                step(t + 1, M3{}, PO{});
+                next_row();
+            }
         } else {
 #pragma unroll 1
-            for (int t = 2; t < T; ++t, next_row()) step(t, std::integral_constant<int, 3>{});
+            for (; t + 1 < T; t += 2) {
+                step(t, M3{}, PE{});
+                next_row();
+                step(t + 1, M3{}, PO{});
+                next_row();
+            }
         }
-        if (T >= 2) step(T, std::integral_constant<int, 0>{});
+        if (t < T) {
+            step(t, M3{}, PE{});
+            next_row();
+        }
+        if (T >= 2) step(T, M0{}, PR{});
         if (!own) {  // mode-3 steps accumulated every lane
             a_dm2 = a_dp2 = a_cr = 0.0;
             b_dm2 = b_dp2 = b_cr = 0.0;
@@ -418,7 +463,7 @@ cp_sweep2_tma_kernel(const SweepArgs a, const int parity) {
 // {kChunk, 1, 8} at plane stride 2 (level_engine.cuh: make_level_tmap).  NW warps per
 // block: small blocks let an SM refill as soon as a few strips finish.
 constexpr int kWarpsT = 4;
-constexpr int tmap_smem(int nw) { return nw * (kStages * kStageBytes + kStages * 8); }
+constexpr int tmap_smem(int nw) { return nw * (kStagesT * kBoxRows * kStageBytes + kStagesT * 8); }
 
 template <int PN, int NW, bool kUnroll>
 __global__ void __launch_bounds__(NW * 32, 24 / NW)
@@ -435,9 +480,10 @@ cp_sweep2_tmap_kernel(const SweepArgs a, const int parity, const __grid_constant
     const int lane = threadIdx.x & 31;
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
     const int tile = blockIdx.x * NW + warp;
-    double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * kStages * kStreams * kChunk;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + NW * kStages * kStageBytes) +
-                     warp * kStages;
+    double* ring = reinterpret_cast<double*>(smem_raw) +
+                   (size_t)warp * kStagesT * kBoxRows * kStreams * kChunk;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + NW * kStagesT * kBoxRows * kStageBytes) +
+                     warp * kStagesT;
     double a_dm2 = 0.0, a_dp2 = 0.0, a_cr = 0.0;
     double b_dm2 = 0.0, b_dp2 = 0.0, b_cr = 0.0;
     if (tile < a.ntiles) {

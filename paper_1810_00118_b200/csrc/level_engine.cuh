@@ -35,8 +35,8 @@ struct Level {
 };
 
 // Tensor map over a whole-grid level: x = column (pitch), y = row (n+1 rows,
-// rows beyond are zero-filled), z = pair * NSLOT + slot; box {kChunk, 1, 8} at
-// plane stride 2 = one row of PHI_p, MX_p, MY_p, RHO_p for parity p.
+// rows beyond are zero-filled), z = pair * NSLOT + slot; box {kChunk, kBoxRows, 8}
+// at plane stride 2 = kBoxRows rows of PHI_p, MX_p, MY_p, RHO_p for parity p.
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -54,7 +54,7 @@ void make_level_tmap(Level& lv) {
     const Layout& L = lv.L;
     cuuint64_t dims[3] = {(cuuint64_t)L.pitch, (cuuint64_t)L.n + 1, (cuuint64_t)lv.B * NSLOT};
     cuuint64_t strides[2] = {(cuuint64_t)L.pitch * 8, (cuuint64_t)L.plane * 8};
-    cuuint32_t box[3] = {(cuuint32_t)kChunk, 1, 8};
+    cuuint32_t box[3] = {(cuuint32_t)kChunk, (cuuint32_t)kBoxRows, 8};
     cuuint32_t estr[3] = {1, 1, 2};
     CUresult r = tmap_encoder()(&lv.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
                                 lv.base + L.at(0, 0), dims, strides, box, estr,
@@ -281,6 +281,15 @@ void launch_pdl(K kernel, dim3 grid, dim3 blk, int smem, cudaStream_t s, const S
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = g_pdl ? 1 : 0;
+    if (smem > 48 * 1024) {  // opt in once per (kernel, device)
+        static std::set<std::pair<const void*, int>> done;
+        static std::mutex mu;
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(mu);
+        if (done.insert({(const void*)kernel, dev}).second)
+            CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
     CK(cudaLaunchKernelEx(&cfg, kernel, a, parity, tm, early));
 }
 
