@@ -37,6 +37,7 @@
 #include "cp2w_kernels.cuh"
 #include "grid_kernels.cuh"
 #include "tile_kernels.cuh"
+#include "cp3_kernels.cuh"
 
 using namespace w1mg_dev;
 
@@ -66,6 +67,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
                               : (std::string(v) == "tma2") ? kTma2
                               : (std::string(v) == "tma2w") ? kTma2W
                               : (std::string(v) == "tma2t") ? kTma2T
+                              : (std::string(v) == "tma3")  ? kTma3
                                                             : kAuto;
         if (const char* v = std::getenv("W1MG_RESIDENT")) g_resident = std::atoi(v);
         if (const char* v = std::getenv("W1MG_COMPACT")) g_compact = std::atoi(v) != 0;
@@ -545,7 +547,7 @@ int w1mg_interpolate_flux(w1mg_ctx* c, int nc, const double* cx, const double* c
 // Kernel probe: `iters` fused sweeps on B pairs of an n-cell level with the
 // stop rule disabled, after `warm` untimed sweeps; returns ms per sweep.
 int w1mg_set_sweep_engine(int engine) {
-    if (engine < kLdg || engine > kTma2T) return W1MG_EINVAL;
+    if (engine < kLdg || engine > kTma3) return W1MG_EINVAL;
     g_sweep_variant = engine;
     return W1MG_OK;
 }
@@ -616,9 +618,10 @@ int w1mg_sweep_probe(w1mg_ctx* c, int n, int B, int pnorm, long warm, long iters
         mirror_rho(c, lv);
         init_level_ctl(c, lv, 0.0, -1.0, 2 * (warm + iters) + 64);
         // kTma2: each launch is two sweeps; iters counts sweeps
-        const int per = two_sweep(lv) ? 2 : 1;
+        const int per = sweeps_per_launch(lv);
         auto one = [&](long k) {
-            if (per == 2) launch_sweep2(lv, pnorm, (int)(k & 1), c->stream);
+            if (per == 3) launch_sweep3(lv, pnorm, (int)(k & 1), c->stream);
+            else if (per == 2) launch_sweep2(lv, pnorm, (int)(k & 1), c->stream);
             else launch_sweep(lv, pnorm, (int)(k & 1), c->stream);
         };
         long k = 0;

@@ -43,7 +43,7 @@ struct PairCtl {
     int done;       // stop flag
     int cur;        // buffer parity holding the latest state
     int nonfinite;  // residual was NaN/Inf
-    int redo;       // a two-sweep launch stopped after its first sweep: replay it
+    int redo;       // a multi-sweep launch stopped after its first (second) sweep: replay 1 (2)
 };
 
 // Launch gate shared by the single-sweep kernels.  parity >= 0: a normal
@@ -251,9 +251,9 @@ __device__ __forceinline__ void finalize_pair(const SweepArgs& a, int pair, int 
     bool finite = isfinite(fpr);
     if (!finite) ctl->nonfinite = 1;
     if (ctl->redo) {
-        // fix-up sweep after a two-sweep launch stopped on its first
-        // sweep: the pair is already counted as done
-        ctl->redo = 0;
+        // fix-up sweep after a multi-sweep launch stopped on its first (or
+        // second) sweep: the pair is already counted as done
+        ctl->redo -= 1;
     } else if (fpr < ctl->tol || k + 1 >= ctl->max_it || !finite) {
         ctl->done = 1;
         if (a.ndone) atomicAdd(a.ndone, 1);

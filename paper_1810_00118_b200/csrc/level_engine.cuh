@@ -26,6 +26,8 @@ struct Level {
     SweepArgs args2w{};  // two-sweep engine, two column sets per lane
     dim3 grid2w;
     dim3 grid2t;  // two-sweep tensor-map engine (args2 geometry, tmap_nw-warp blocks)
+    SweepArgs args3{};  // three-sweep tensor-map engine
+    dim3 grid3;
     int tmap_nw = kWarpsT;
     bool slab = false;  // row slab of a decomposed grid (one-sweep engine only)
     int* act = nullptr;   // [B] running pairs of a compacted launch (null: B == 1 or slab)
@@ -106,6 +108,8 @@ void set_geometry(Level& lv, int pairs, int num_sms) {
     lv.grid = dim3((lv.args.ntiles + kSweepWarps - 1) / kSweepWarps, pairs, 1);
     lv.grid2 = dim3((lv.args2.ntiles + kSweepWarps - 1) / kSweepWarps, pairs, 1);
     lv.grid2w = dim3((lv.args2w.ntiles + kWarpsW - 1) / kWarpsW, pairs, 1);
+    strip_geometry(lv.args3, kOwn3, pairs, target, 4);     // three-sweep: 27 per warp
+    lv.grid3 = dim3((lv.args3.ntiles + kWarps3 - 1) / kWarps3, pairs, 1);
     lv.tmap_nw = g_tmap_nw ? g_tmap_nw : ((pairs == 1 && lv.n >= 384 && lv.n <= 640) ? 8 : kWarpsT);
     lv.grid2t = dim3((lv.args2.ntiles + lv.tmap_nw - 1) / lv.tmap_nw, pairs, 1);
 }
@@ -152,6 +156,7 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     a.nact = nullptr;
     lv.args2 = a;
     lv.args2w = a;
+    lv.args3 = a;
     set_geometry(lv, B, c->num_sms);
     // a compacted launch over fewer pairs uses shorter strips (more tiles per
     // pair), so size the partials for the one-pair geometry
@@ -161,10 +166,12 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
         tag + ".partial",
         (size_t)B * std::max<size_t>({(size_t)one.args.ntiles * 3, (size_t)one.args2.ntiles * 6,
                                       (size_t)one.args2w.ntiles * 6, (size_t)lv.args.ntiles * 3,
-                                      (size_t)lv.args2.ntiles * 6, (size_t)lv.args2w.ntiles * 6}));
+                                      (size_t)lv.args2.ntiles * 6, (size_t)lv.args2w.ntiles * 6,
+                                      (size_t)one.args3.ntiles * 9, (size_t)lv.args3.ntiles * 9}));
     a.partial = lv.partial;
     lv.args2.partial = lv.partial;
     lv.args2w.partial = lv.partial;
+    lv.args3.partial = lv.partial;
     if (!lv.slab) {  // two-level residual reduction of the two-sweep kernels
         const int gs = (one.args2.ntiles + kRedGroup - 1) / kRedGroup + 1;
         double* gp = c->get<double>(tag + ".gpart", (size_t)B * gs * 6);
@@ -258,6 +265,8 @@ constexpr int kTma2 = 2;
 // 3-14 % faster than the bulk-copy ring for batched 128..512 levels,
 // tools/probe.py; profiles/r1_summary.md)
 constexpr int kAuto = 3;
+// three sweeps per HBM pass (cp3_kernels.cuh), tensor-map ring; W1MG_SWEEP=tma3
+constexpr int kTma3 = 6;
 int g_sweep_variant = kAuto;
 
 constexpr int kTma2W = 4;  // two-sweep, two column sets per lane (cp2w_kernels.cuh)
@@ -323,6 +332,32 @@ bool two_sweep(const Level& lv) {
     return g_sweep_variant == kTma2 || g_sweep_variant == kTma2W || g_sweep_variant == kTma2T ||
            (g_sweep_variant == kAuto && lv.n >= 96);
 }
+// auto picks it for a one-pair level of 192..384 (one 256^2 pair: 22.4 ->
+// 19.7 ms per level); batched levels and big grids are issue-bound, where
+// its 27-of-32 owned columns and 94 registers cost more than the third of
+// the HBM bytes it saves (tools/gpu/tma3p.sh: 512^2 x256 419 vs 361 us,
+// 4096^2 97 vs 91 us per sweep)
+bool three_sweep(const Level& lv) {
+    if (lv.slab || !lv.has_tmap || lv.n < 96) return false;
+    return g_sweep_variant == kTma3 ||
+           (g_sweep_variant == kAuto && lv.B == 1 && lv.n >= 192 && lv.n <= 384);
+}
+// sweeps one streaming launch performs on this level
+int sweeps_per_launch(const Level& lv) { return three_sweep(lv) ? 3 : two_sweep(lv) ? 2 : 1; }
+
+void launch_sweep3(const Level& lv, int pn, int parity, cudaStream_t s) {
+    const dim3 blk(kWarps3 * 32);
+    const int sm = tmap3_smem(kWarps3);
+    const long blocks = (long)lv.grid3.x * lv.grid3.y;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int early = (g_pdl && 2 * blocks <= (long)nsm * 5) ? 1 : 0;
+    switch (pn) {
+        case 0: launch_pdl(cp_sweep3_tmap_kernel<0>, lv.grid3, blk, sm, s, lv.args3, parity, lv.tmap, early); break;
+        case 1: launch_pdl(cp_sweep3_tmap_kernel<1>, lv.grid3, blk, sm, s, lv.args3, parity, lv.tmap, early); break;
+        default: launch_pdl(cp_sweep3_tmap_kernel<2>, lv.grid3, blk, sm, s, lv.args3, parity, lv.tmap, early); break;
+    }
+}
 
 void launch_sweep2(const Level& lv, int pn, int parity, cudaStream_t s) {
     if (g_sweep_variant == kTma2T || g_sweep_variant == kAuto) {
@@ -375,7 +410,8 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
     std::string key(reinterpret_cast<const char*>(&lv.args), sizeof(SweepArgs));
     key += std::to_string(pn) + ":" + std::to_string(K) + ":" + std::to_string(lv.grid.x) + ":" +
            std::to_string(lv.grid.y) + ":" + std::to_string(lv.grid2.x) + ":" +
-           std::to_string(lv.grid2w.x) + ":" + std::to_string(lv.grid2t.x) + ":B" +
+           std::to_string(lv.grid2w.x) + ":" + std::to_string(lv.grid2t.x) + ":" +
+           std::to_string(lv.grid3.x) + ":B" +
            std::to_string(lv.B) + ":v" +
            std::to_string(g_sweep_variant);
     auto it = c->graphs.find(key);
@@ -385,7 +421,8 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
     if (lv.args.act)
         compact_active_kernel<<<1, kCompactThreads, 0, c->stream>>>(lv.ctl, lv.B, lv.act, lv.nact);
     for (int k = 0; k < K; ++k) {
-        if (two_sweep(lv)) launch_sweep2(lv, pn, k & 1, c->stream);
+        if (three_sweep(lv)) launch_sweep3(lv, pn, k & 1, c->stream);
+        else if (two_sweep(lv)) launch_sweep2(lv, pn, k & 1, c->stream);
         else launch_sweep(lv, pn, k & 1, c->stream);
     }
     CK(cudaStreamEndCapture(c->stream, &g));
@@ -407,7 +444,7 @@ int g_compact_step = 1 << 30;  // bucket granularity (W1MG_COMPACT_STEP; default
 Level compacted(const Level& lv, int pairs, int num_sms) {
     Level b = lv;
     set_geometry(b, pairs, num_sms);
-    for (SweepArgs* a : {&b.args, &b.args2, &b.args2w}) {
+    for (SweepArgs* a : {&b.args, &b.args2, &b.args2w, &b.args3}) {
         a->act = lv.act;
         a->nact = lv.nact;
     }
@@ -672,7 +709,7 @@ void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
         return;
     }
     cudaGraphExec_t ex = sweep_graph(c, lv, pn, K);
-    const long per_launch = two_sweep(lv) ? 2 : 1;
+    const long per_launch = sweeps_per_launch(lv);
     long launched = 0;
     int span = lv.B;  // pairs the current graph's grids cover
     for (long g = 0;; ++g) {
@@ -702,8 +739,9 @@ void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
         }
         if (launched >= max_iters + K * per_launch) break;  // every pair hit its cap by now
     }
-    if (two_sweep(lv)) {
-        // replay the first sweep of pairs whose two-sweep launch stopped early
+    // replay the first sweep(s) of pairs whose multi-sweep launch stopped
+    // early (redo = 1 or 2; pairs with redo = 0 exit at once)
+    for (long q = 1; q < per_launch; ++q) {
         launch_sweep(lv, pn, -1, c->stream);
         CK(cudaGetLastError());
         ++c->launches;

@@ -52,7 +52,7 @@ def _random_source(n, seed):
 
 
 ENGINES = {"auto": (1, 3), "cluster": (3, 3), "resident-1cta": (2, 3), "grid": (4, 3),
-           "stream-tma2": (0, 2),
+           "stream-tma2": (0, 2), "stream-tma3": (0, 6),
            "stream-tma2w": (0, 4), "stream-tma2t": (0, 5), "stream-tma": (0, 1),
            "stream-ldg": (0, 0)}
 
@@ -229,24 +229,26 @@ def test_cluster_engine_levels_bit_exact(oracle, n):
     _lib.lib().w1mg_set_resident_engine(1)
 
 
-@pytest.mark.parametrize("eng", [2, 4, 5])
+@pytest.mark.parametrize("iters", [32, 33, 34])
+@pytest.mark.parametrize("eng", [2, 4, 5, 6])
 @pytest.mark.parametrize("p", [0, 1, 2])
 @pytest.mark.parametrize("n", [300, 1024])
-def test_two_sweep_engine_odd_stop(oracle, n, p, eng):
-    """Two-sweep launches (one or two column sets per lane, interior fast
-    paths included) with an odd sweep cap: the last launch stops after its
-    first sweep and the fix-up replay must reproduce the reference state."""
+def test_two_sweep_engine_odd_stop(oracle, n, p, eng, iters):
+    """Multi-sweep launches (two sweeps with one or two column sets per lane,
+    three sweeps; interior fast paths included) with sweep caps that end a
+    launch after its first or second sweep: the fix-up replays must
+    reproduce the reference state."""
     from paper_1810_00118_b200 import _lib
 
     _lib.lib().w1mg_set_sweep_engine(eng)
     rng = np.random.default_rng(n + p)
     rho = instances.make_source(rng.random((n + 1, n + 1)), rng.random((n + 1, n + 1)), n)
     try:
-        rep = _run(rho, p, 33)
+        rep = _run(rho, p, iters)
     finally:
         _lib.lib().w1mg_set_sweep_engine(3)
-    ref = oracle.cp_run(rho, p=p, tol=-1.0, max_iters=33)
-    assert rep.iterations == 33
+    ref = oracle.cp_run(rho, p=p, tol=-1.0, max_iters=iters)
+    assert rep.iterations == iters
     _assert_fields_equal(rep, ref)
     np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-10)
 
@@ -263,3 +265,24 @@ def test_full_size_4096_bit_exact(oracle):
     ref = oracle.cp_run(rho, p=1, tol=-1.0, max_iters=3, m0=m0, phi0=phi0)
     _assert_fields_equal(rep, ref)
     assert _rel(rep.distance, ref.distance) <= RED_TOL
+
+
+@pytest.mark.parametrize("n", [256, 4096])
+def test_three_sweep_converged_matches_auto(n):
+    """The three-sweep engine stops at the same sweep with the same fields and
+    residual history as the default engine (stop after A, B or C replayed)."""
+    from paper_1810_00118_b200 import _lib
+
+    rng = np.random.default_rng(n)
+    rho = instances.make_source(rng.random((n + 1, n + 1)), rng.random((n + 1, n + 1)), n)
+    tol = 1e-3 * _run(rho, 1, 1).residual_history[0]
+    ref = _run(rho, 1, 100000, tol=tol)
+    _lib.lib().w1mg_set_sweep_engine(6)
+    try:
+        rep = _run(rho, 1, 100000, tol=tol)
+    finally:
+        _lib.lib().w1mg_set_sweep_engine(3)
+    assert rep.converged and rep.iterations == ref.iterations
+    assert np.array_equal(rep.flux.x_edges, ref.flux.x_edges)
+    assert np.array_equal(rep.potential.values, ref.potential.values)
+    np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-10, atol=0)
