@@ -286,3 +286,16 @@ def test_three_sweep_converged_matches_auto(n):
     assert np.array_equal(rep.flux.x_edges, ref.flux.x_edges)
     assert np.array_equal(rep.potential.values, ref.potential.values)
     np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-10, atol=0)
+
+
+@pytest.mark.parametrize("n,iters", [(256, 40), (256, 41), (512, 41), (512, 42)])
+def test_one_pair_auto_engines_bit_exact(oracle, n, iters):
+    """One-pair levels take the auto engines' special cases: the three-sweep
+    march at 192..384 and 8-warp two-sweep blocks at 384..640."""
+    rng = np.random.default_rng(n + iters)
+    rho = instances.make_source(rng.random((n + 1, n + 1)), rng.random((n + 1, n + 1)), n)
+    rep = _run(rho, 1, iters)
+    ref = oracle.cp_run(rho, p=1, tol=-1.0, max_iters=iters)
+    assert rep.iterations == iters
+    _assert_fields_equal(rep, ref)
+    np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-10)
