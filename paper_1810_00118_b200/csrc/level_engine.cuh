@@ -628,6 +628,7 @@ void launch_tile_pn(w1mg_ctx* c, const Level& lv, const TileGeom& g) {
     t.LW = g.LW;
     t.LH = g.LH;
     t.ES = g.LW - 2;
+    t.LCAP = tile_list_cap(g.LW, g.LH);
     t.edges = c->get<double>("tile.edges", B * 2 * T * kTileSecs * t.ES);
     t.flags = c->get<unsigned>("tile.flags", B * T * kTileFlagStride);
     t.part = c->get<double>("tile.part", B * kTileSlots * T * 3);
@@ -660,8 +661,9 @@ void launch_tile_pn(w1mg_ctx* c, const Level& lv, const TileGeom& g) {
         std::fprintf(stderr, "tile n=%d TRxTC=%dx%d smem=%d\n", lv.n, g.TR, g.TC, smem);
         for (int q = 0; q < T; ++q) {
             const long long* r = &h[(size_t)q * kTileDbgPts];
-            std::fprintf(stderr, "tile %3d: loop %lld A %lld B %lld post %lld wait %lld halo %lld\n", q,
-                         r[0] / 128, r[1] / 128, r[2] / 128, r[5] / 128, r[3] / 128, r[4] / 128);
+            std::fprintf(stderr,
+                         "tile %3d: top %lld A-int %lld wait %lld halo %lld borders %lld B-int+post %lld\n",
+                         q, r[0] / 128, r[1] / 128, r[2] / 128, r[3] / 128, r[4] / 128, r[5] / 128);
         }
     }
 }

@@ -60,6 +60,7 @@ struct TileArgs {
     int TR, TC;            // tiles per pair (rows x columns of tiles)
     int LW, LH;            // shared-memory pitch / rows (largest tile + halo ring)
     int ES;                // edge section stride (largest tile side)
+    int LCAP;              // capacity of each border list (ints)
     double* edges;         // [pairs][2][T][kTileSecs][ES]
     unsigned* flags;       // [pairs][T][kTileFlagStride] steps completed
     double* part;          // [pairs][kTileSlots][T][3]
@@ -75,7 +76,10 @@ constexpr int kTileDbgPts = 8;
 __host__ __device__ inline int tile_lo(int N1, int parts, int t) {
     return (int)((long)N1 * t / parts);
 }
-__host__ inline long tile_smem_bytes(int LW, int LH) { return 6L * LW * LH * 8; }
+__host__ inline int tile_list_cap(int LW, int LH) { return 2 * LW + 2 * LH + 8; }
+__host__ inline long tile_smem_bytes(int LW, int LH) {
+    return 6L * LW * LH * 8 + 2L * tile_list_cap(LW, LH) * 4;
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -324,26 +328,77 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
     __syncthreads();
     if (ctl->cur != 0) store_state(0);  // checkpoint of state k0 (slot 0)
 
-    // (li, lj) of flat index q over a W-wide rectangle, stepped by a stride
-    struct Walk {
-        int li, lj, di, dj, W;
-        __device__ void init(int q, int W_, int stride) {
-            W = W_;
-            li = q % W;
-            lj = q / W;
-            di = stride % W;
-            dj = stride / W;
-        }
-        __device__ void next() {
-            li += di;
-            lj += dj;
-            if (li >= W) {
-                li -= W;
-                ++lj;
+    // Border lists (built once, in order, by thread 0): A-border = nodes of
+    // phase A that need the halo (right column, top row) or are the
+    // recomputed halo (left column, bottom row); B-border = owned nodes whose
+    // phi is published (first / last column and row).  The interior parts
+    // of both phases need no halo: A-interior runs before the wait for the
+    // neighbours, B-interior after this tile's step flag is released, so
+    // both overlap the inter-SM flag latency.
+    int* listA = reinterpret_cast<int*>(sm + 6 * S);
+    int* listB = listA + t.LCAP;
+    __shared__ int s_na, s_nb;
+    if (tid == 0) {
+        int na = 0, nb = 0;
+        for (int lj = 0; lj <= h; ++lj)
+            for (int li = 0; li <= w; ++li) {
+                if (li == 0 && lj == 0) continue;
+                const bool intA = li >= 1 && li <= w - 1 && lj >= 1 && lj <= h - 1;
+                if (!intA && i0 - 1 + li >= 0 && j0 - 1 + lj >= 0) listA[na++] = li | (lj << 16);
+                if (li >= 1 && lj >= 1) {
+                    const bool intB = li >= 2 && li <= w - 1 && lj >= 2 && lj <= h - 1;
+                    if (!intB) listB[nb++] = li | (lj << 16);
+                }
+            }
+        s_na = na;
+        s_nb = nb;
+    }
+    __syncthreads();
+    const int nAb = s_na, nBb = s_nb;
+    const int wA = w - 1, nAi = (w >= 2 && h >= 2) ? (w - 1) * (h - 1) : 0;
+    const int wB = w - 2, nBi = (w >= 3 && h >= 3) ? (w - 2) * (h - 2) : 0;
+
+    // phase A at local node (li, lj): m-update (node_flux), m records
+    auto nodeA = [&](int li, int lj, int bufw, double& s_dm2) {
+        const int i = i0 - 1 + li, j = j0 - 1 + lj;
+        const int kk = lj * LW + li;
+        const bool hx = i < n, hy = j < n;
+        const double pc = phi[kk];
+        const double pr = hx ? phi[kk + 1] : 0.0;
+        const double pu = hy ? phi[kk + LW] : 0.0;
+        double ux, uy, dx, dy;
+        node_flux<PN>(hx, hy, pc, pr, pu, mx[kk], my[kk], mu, zt, ih, ux, uy, dx, dy);
+        mx[kk] = ux;
+        my[kk] = uy;
+        ddx[kk] = dx;
+        ddy[kk] = dy;
+        if (li >= 1 && lj >= 1) {
+            s_dm2 = __fma_rn(dy, dy, __fma_rn(dx, dx, s_dm2));
+            if (li == w) {
+                rec(bufw, tile, E_MX_R)[lj - 1] = ux;
+                rec(bufw, tile, E_MY_R)[lj - 1] = uy;
+            }
+            if (lj == h) {
+                rec(bufw, tile, E_MX_T)[li - 1] = ux;
+                rec(bufw, tile, E_MY_T)[li - 1] = uy;
             }
         }
     };
-    const int W1 = w + 1, cntA = W1 * (h + 1), cntB = w * h;
+    // phase B at owned local node (li, lj): row_update's divergence order
+    auto nodeB = [&](int li, int lj, int bufw, double& s_dp2, double& s_cr) {
+        const int kk = lj * LW + li;
+        const double divm = (mx[kk] - mx[kk - 1]) * ih + (my[kk] - my[kk - LW]) * ih;
+        const double divd = (ddx[kk] - ddx[kk - 1]) * ih + (ddy[kk] - ddy[kk - LW]) * ih;
+        const double d = tau * (divm + divd - rho[kk]);
+        const double f = phi[kk] + d;
+        phi[kk] = f;
+        s_dp2 = __fma_rn(d, d, s_dp2);
+        s_cr = __fma_rn(d, divd, s_cr);
+        if (li == 1) rec(bufw, tile, E_PHI_L)[lj - 1] = f;
+        if (li == w) rec(bufw, tile, E_PHI_R)[lj - 1] = f;
+        if (lj == 1) rec(bufw, tile, E_PHI_B)[li - 1] = f;
+        if (lj == h) rec(bufw, tile, E_PHI_T)[li - 1] = f;
+    };
     // warp 0 lanes 0..5 wait for the neighbours' step flags, lane 6 for the
     // decision of sweep kd.  Relaxed polls without an acquire fence: every
     // load that consumes a neighbour's records is an L2 (.cg, gpu-scope
@@ -383,109 +438,55 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
         if (step >= 8 && step < 136) dbg_acc[pt] += now_ - dbg_last; \
         dbg_last = now_;                                             \
     }
+
+    bool have_halo = true;  // the halo of state k is in shared memory (after a load)
     for (;;) {
         if (replay && k >= target) break;
         STAMP(0);
-        // ---- phase A: fluxes of owned nodes + recomputed left / bottom halo,
-        // two nodes per thread per pass (independent chains for the scheduler)
-        double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
         const int bufw = (int)((step + 1) & 1);  // record buffer of the state this step produces
-        auto phaseA = [&](auto U_) {
-            constexpr int UU = decltype(U_)::value;
-            Walk wa, wb;
-            wa.init(tid, W1, UU * kTileThreads);
-            wb.init(tid + kTileThreads, W1, UU * kTileThreads);
-            for (int q = tid; q < cntA; q += UU * kTileThreads, wa.next(), wb.next()) {
-                const bool vb = UU == 2 && q + kTileThreads < cntA;
-                int kk[2];
-                bool ok[2], hx[2], hy[2];
-                double pc[2], pr[2], pu[2], mo[2], no[2];
-#pragma unroll
-                for (int u = 0; u < UU; ++u) {
-                    const Walk& wv = u ? wb : wa;
-                    const int i = i0 - 1 + wv.li, j = j0 - 1 + wv.lj;
-                    ok[u] = (u == 0 || vb) && i >= 0 && j >= 0 && (wv.li | wv.lj) != 0;
-                    kk[u] = wv.lj * LW + wv.li;
-                    hx[u] = i < n;
-                    hy[u] = j < n;
-                    const int k2 = ok[u] ? kk[u] : 0;
-                    pc[u] = phi[k2];
-                    pr[u] = hx[u] ? phi[k2 + 1] : 0.0;
-                    pu[u] = hy[u] ? phi[k2 + LW] : 0.0;
-                    mo[u] = mx[k2];
-                    no[u] = my[k2];
-                }
-                double ux[2], uy[2], dx[2], dy[2];
-#pragma unroll
-                for (int u = 0; u < UU; ++u)
-                    node_flux<PN>(hx[u], hy[u], pc[u], pr[u], pu[u], mo[u], no[u], mu, zt, ih, ux[u], uy[u],
-                                  dx[u], dy[u]);
-#pragma unroll
-                for (int u = 0; u < UU; ++u) {
-                    if (!ok[u]) continue;
-                    const Walk& wv = u ? wb : wa;
-                    const int li = wv.li, lj = wv.lj;
-                    mx[kk[u]] = ux[u];
-                    my[kk[u]] = uy[u];
-                    ddx[kk[u]] = dx[u];
-                    ddy[kk[u]] = dy[u];
-                    if (li >= 1 && lj >= 1) {
-                        s_dm2 = __fma_rn(dy[u], dy[u], __fma_rn(dx[u], dx[u], s_dm2));
-                        if (li == w) {
-                            rec(bufw, tile, E_MX_R)[lj - 1] = ux[u];
-                            rec(bufw, tile, E_MY_R)[lj - 1] = uy[u];
-                        }
-                        if (lj == h) {
-                            rec(bufw, tile, E_MX_T)[li - 1] = ux[u];
-                            rec(bufw, tile, E_MY_T)[li - 1] = uy[u];
-                        }
-                    }
-                }
-            }
-        };
-        if (cntA > kTileThreads) phaseA(std::integral_constant<int, 2>{});
-        else phaseA(std::integral_constant<int, 1>{});
-        __syncthreads();
+        double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
+        // ---- A-interior (no halo needed)
+        for (int q = tid; q < nAi; q += kTileThreads) nodeA(1 + q % wA, 1 + q / wA, bufw, s_dm2);
         STAMP(1);
-        // ---- phase B: potential of owned nodes (row_update's divergence order)
-        auto phaseB = [&](auto U_) {
-            constexpr int UU = decltype(U_)::value;
-            Walk wa, wb;
-            wa.init(tid, w, UU * kTileThreads);
-            wb.init(tid + kTileThreads, w, UU * kTileThreads);
-            for (int q = tid; q < cntB; q += UU * kTileThreads, wa.next(), wb.next()) {
-                const bool vb = UU == 2 && q + kTileThreads < cntB;
-                int kk[2];
-                double divm[2], divd[2], rr[2], pc[2];
-#pragma unroll
-                for (int u = 0; u < UU; ++u) {
-                    const Walk& wv = u ? wb : wa;
-                    kk[u] = (u == 0 || vb) ? (1 + wv.lj) * LW + 1 + wv.li : LW + 1;
-                    const int c = kk[u];
-                    divm[u] = (mx[c] - mx[c - 1]) * ih + (my[c] - my[c - LW]) * ih;
-                    divd[u] = (ddx[c] - ddx[c - 1]) * ih + (ddy[c] - ddy[c - LW]) * ih;
-                    rr[u] = rho[c];
-                    pc[u] = phi[c];
-                }
-#pragma unroll
-                for (int u = 0; u < UU; ++u) {
-                    if (u == 1 && !vb) continue;
-                    const Walk& wv = u ? wb : wa;
-                    const int li = 1 + wv.li, lj = 1 + wv.lj;
-                    const double d = tau * (divm[u] + divd[u] - rr[u]);
-                    const double f = pc[u] + d;
-                    phi[kk[u]] = f;
-                    s_dp2 = __fma_rn(d, d, s_dp2);
-                    s_cr = __fma_rn(d, divd[u], s_cr);
-                    if (li == 1) rec(bufw, tile, E_PHI_L)[lj - 1] = f;
-                    if (li == w) rec(bufw, tile, E_PHI_R)[lj - 1] = f;
-                    if (lj == 1) rec(bufw, tile, E_PHI_B)[li - 1] = f;
-                    if (lj == h) rec(bufw, tile, E_PHI_T)[li - 1] = f;
-                }
+        if (!have_halo) {
+            // ---- neighbours done with the previous step; decision of sweep k - lag
+            if (warp == 0) wait_neighbours(step, replay ? k0 - 1 : k - kTileLag);
+            __syncthreads();
+            STAMP(2);
+            if (!replay && s_stop) {
+                // sweep s = s_stop_at stopped: restore the checkpoint at or
+                // below s + 1 and replay to exactly s + 1 (every tile does
+                // the same); this step's A-interior is discarded
+                stop_at = s_stop_at;
+                fin_fpr = s_fpr;
+                target = stop_at + 1;
+                const long c = k0 + ((target - k0) / kTileCk) * kTileCk;
+                load_state((int)(((c - k0) / kTileCk) & 1));
+                k = c;
+                replay = true;
+                have_halo = true;
+                __syncthreads();
+                continue;
             }
-        };
-        if (cntB > kTileThreads) phaseB(std::integral_constant<int, 2>{});
-        else phaseB(std::integral_constant<int, 1>{});
+            load_halo((int)(step & 1));
+        }
+        __syncthreads();
+        STAMP(3);
+        // ---- A-border, then B-border (the published edges)
+        for (int q = tid; q < nAb; q += kTileThreads) nodeA(listA[q] & 0xffff, listA[q] >> 16, bufw, s_dm2);
+        __syncthreads();
+        for (int q = tid; q < nBb; q += kTileThreads)
+            nodeB(listB[q] & 0xffff, listB[q] >> 16, bufw, s_dp2, s_cr);
+        __syncthreads();
+        // ---- release: the edge records of this step (every thread's,
+        // ordered by the barrier) before the flag
+        if (tid == 0)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + (long)tile * kTileFlagStride),
+                         "r"(step + 1)
+                         : "memory");
+        STAMP(4);
+        // ---- B-interior, overlapping the flag's way to the neighbours
+        for (int q = tid; q < nBi; q += kTileThreads) nodeB(2 + q % wB, 2 + q / wB, bufw, s_dp2, s_cr);
         s_dm2 = warp_sum(s_dm2);
         s_dp2 = warp_sum(s_dp2);
         s_cr = warp_sum(s_cr);
@@ -495,20 +496,14 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
             wred[warp][2] = s_cr;
         }
         __syncthreads();
-        STAMP(2);
         ++k;
         ++step;
-        const bool ckpt = !replay && ((k - k0) % kTileCk) == 0;
-        if (ckpt) {
+        have_halo = false;
+        if (!replay && ((k - k0) % kTileCk) == 0) {
             store_state((int)(((k - k0) / kTileCk) & 1));
             __syncthreads();
         }
-        // ---- post: the step flag first (release: the edge records of every
-        // thread, ordered by the barrier), the residual partials from warp 1
-        if (tid == 0)
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + (long)tile * kTileFlagStride),
-                         "r"(step)
-                         : "memory");
+        // ---- residual partials of sweep k-1 (warp 1, off the critical path)
         if (tid == 32 && !replay) {
             const int slot = (int)((k - 1) % kTileSlots);
             double t0 = 0.0, t1 = 0.0, t2 = 0.0;
@@ -525,26 +520,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile_kernel(const TileArgs
                          : "memory");
         }
         STAMP(5);
-        // ---- wait: neighbours done with this step; decision of sweep k - lag
-        if (warp == 0) wait_neighbours(step, replay ? k0 - 1 : k - kTileLag);
-        __syncthreads();
-        STAMP(3);
-        if (!replay && s_stop) {
-            // sweep s = s_stop_at stopped: restore the checkpoint at or below
-            // s + 1 and replay to exactly s + 1 (every tile does the same)
-            stop_at = s_stop_at;
-            fin_fpr = s_fpr;
-            target = stop_at + 1;
-            const long c = k0 + ((target - k0) / kTileCk) * kTileCk;
-            load_state((int)(((c - k0) / kTileCk) & 1));
-            k = c;
-            replay = true;
-            __syncthreads();
-            continue;
-        }
-        load_halo((int)(step & 1));
-        __syncthreads();
-        STAMP(4);
     }
     // every neighbour finished its replay (and so its checkpoint reads)
     // before the final state goes into buffer 0
