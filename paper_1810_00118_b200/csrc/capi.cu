@@ -38,6 +38,7 @@
 #include "grid_kernels.cuh"
 #include "tile_kernels.cuh"
 #include "cp3_kernels.cuh"
+#include "tile2_kernels.cuh"
 
 using namespace w1mg_dev;
 
@@ -80,6 +81,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_TILE_MIN")) g_tile_min = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TILE_MAX")) g_tile_max = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TILE_GRID")) g_tile_grid = std::max(0, std::atoi(v));
+        if (const char* v = std::getenv("W1MG_TILE_DEPTH")) g_tile_depth = std::atoi(v) == 2 ? 2 : 1;
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
             const int w = std::atoi(v);
@@ -573,6 +575,7 @@ int w1mg_set_option(const char* name, long value) {
     else if (k == "tile_min" && v >= 1) g_tile_min = v;
     else if (k == "tile_max" && v >= 1) g_tile_max = v;
     else if (k == "tile_grid" && v >= 0) g_tile_grid = v;
+    else if (k == "tile_depth" && (v == 1 || v == 2)) g_tile_depth = v;
     else return W1MG_EINVAL;
     return W1MG_OK;
 }

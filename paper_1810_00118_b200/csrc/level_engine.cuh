@@ -600,6 +600,7 @@ int g_tile = 0;
 int g_tile_min = 96;
 int g_tile_max = 640;
 int g_tile_grid = 0;  // tiles per side (0: floor(sqrt(SMs - 1)))
+int g_tile_depth = 1;  // sweeps per halo exchange: 1 (tile_kernels.cuh) or 2 (tile2_kernels.cuh)
 
 struct TileGeom {
     int TR = 0, TC = 0, LW = 0, LH = 0;
@@ -612,9 +613,10 @@ bool tile_geometry(const w1mg_ctx* c, const Level& lv, TileGeom& g) {
     t = std::min(t, (lv.n + 1) / 4);  // tiles at least 4 nodes wide
     if (t < 1 || (long)lv.B * (t * t + 1) > c->num_sms) return false;
     g.TR = g.TC = t;
-    g.LW = (lv.n + 1 + t - 1) / t + 2;
+    const int ring = g_tile_depth == 2 ? 4 : 2;
+    g.LW = (lv.n + 1 + t - 1) / t + ring;
     g.LH = g.LW;
-    return tile_smem_bytes(g.LW, g.LH) <= 200 * 1024;
+    return (g_tile_depth == 2 ? tile2_smem_bytes(g.LW, g.LH) : tile_smem_bytes(g.LW, g.LH)) <= 200 * 1024;
 }
 
 template <int PN>
@@ -627,9 +629,10 @@ void launch_tile_pn(w1mg_ctx* c, const Level& lv, const TileGeom& g) {
     t.TC = g.TC;
     t.LW = g.LW;
     t.LH = g.LH;
-    t.ES = g.LW - 2;
-    t.LCAP = tile_list_cap(g.LW, g.LH);
-    t.edges = c->get<double>("tile.edges", B * 2 * T * kTileSecs * t.ES);
+    const bool two = g_tile_depth == 2;
+    t.ES = g.LW - (two ? 4 : 2);
+    t.LCAP = two ? tile2_list_cap(g.LW, g.LH) : tile_list_cap(g.LW, g.LH);
+    t.edges = c->get<double>("tile.edges", B * 2 * T * (two ? kT2Secs : kTileSecs) * t.ES);
     t.flags = c->get<unsigned>("tile.flags", B * T * kTileFlagStride);
     t.part = c->get<double>("tile.part", B * kTileSlots * T * 3);
     t.cnt = c->get<unsigned>("tile.cnt", B * kTileSlots);
@@ -645,15 +648,16 @@ void launch_tile_pn(w1mg_ctx* c, const Level& lv, const TileGeom& g) {
     CK(cudaMemsetAsync(t.cnt, 0, sizeof(unsigned) * B * kTileSlots, c->stream));
     CK(cudaMemsetAsync(t.dseq, 0, sizeof(unsigned long long) * B * kTileSlots, c->stream));
     CK(cudaMemsetAsync(t.err, 0, sizeof(int), c->stream));
-    const int smem = (int)tile_smem_bytes(g.LW, g.LH);
-    CK(cudaFuncSetAttribute(cp_tile_kernel<PN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int smem = (int)(two ? tile2_smem_bytes(g.LW, g.LH) : tile_smem_bytes(g.LW, g.LH));
+    const void* kfn = two ? (const void*)cp_tile2_kernel<PN> : (const void*)cp_tile_kernel<PN>;
+    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cp_tile_kernel<PN>, kTileThreads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTileThreads, smem));
     if ((long)occ * c->num_sms < (long)B * (T + 1))
         fail(W1MG_ECUDA, "tile engine: the tiles do not fit co-resident");
     void* args[] = {(void*)&t};
-    CK(cudaLaunchCooperativeKernel((const void*)cp_tile_kernel<PN>, dim3((unsigned)(B * (T + 1))),
-                                   dim3(kTileThreads), args, smem, c->stream));
+    CK(cudaLaunchCooperativeKernel(kfn, dim3((unsigned)(B * (T + 1))), dim3(kTileThreads), args, smem,
+                                   c->stream));
     if (t.dbg) {
         std::vector<long long> h((size_t)kTileDbgSteps * kTileDbgPts);
         CK(cudaMemcpyAsync(h.data(), t.dbg, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));

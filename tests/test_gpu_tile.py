@@ -12,12 +12,15 @@ from paper_1810_00118_b200 import _lib, instances, w1mg
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture
-def tile_engine():
+@pytest.fixture(params=[1, 2], ids=["depth1", "depth2"])
+def tile_engine(request):
+    """Both tile kernels: one sweep per halo exchange and two (tile2_kernels)."""
     L = _lib.lib()
     L.w1mg_set_option(b"tile", 2)
+    L.w1mg_set_option(b"tile_depth", request.param)
     yield
-    L.w1mg_set_option(b"tile", 1)
+    L.w1mg_set_option(b"tile", 0)
+    L.w1mg_set_option(b"tile_depth", 1)
 
 
 def _src(rho):
