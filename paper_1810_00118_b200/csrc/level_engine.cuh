@@ -665,9 +665,12 @@ void launch_tile_pn(w1mg_ctx* c, const Level& lv, const TileGeom& g) {
         std::fprintf(stderr, "tile n=%d TRxTC=%dx%d smem=%d\n", lv.n, g.TR, g.TC, smem);
         for (int q = 0; q < T; ++q) {
             const long long* r = &h[(size_t)q * kTileDbgPts];
-            std::fprintf(stderr,
-                         "tile %3d: top %lld A-int %lld wait %lld halo %lld borders %lld B-int+post %lld\n",
-                         q, r[0] / 128, r[1] / 128, r[2] / 128, r[3] / 128, r[4] / 128, r[5] / 128);
+            // per-step averages of the segments between the kernel's stamps
+            // (depth 1: top, A-int, wait, halo, borders, B-int+post; depth 2:
+            // -, wait, halo, sweep 1, sweep 2, sums+post), steps 8..135 / 4..67
+            const int ns = two ? 64 : 128;
+            std::fprintf(stderr, "tile %3d: seg %lld %lld %lld %lld %lld %lld\n", q, r[0] / ns,
+                         r[1] / ns, r[2] / ns, r[3] / ns, r[4] / ns, r[5] / ns);
         }
     }
 }

@@ -304,9 +304,18 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile2_kernel(const TileArg
     __syncthreads();
     if (ctl->cur != 0) store_state(0);
     bool have_halo = true;
+    long long dbg_acc[kTileDbgPts] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long dbg_last = clock64();
+#define STAMP2(pt)                                                   \
+    if (t.dbg && tid == 0) {                                         \
+        const long long now_ = clock64();                            \
+        if (step >= 4 && step < 68) dbg_acc[pt] += now_ - dbg_last;  \
+        dbg_last = now_;                                             \
+    }
 
     for (;;) {
         if (replay && k >= target) break;
+        STAMP2(0);
         if (!have_halo) {
             if (warp == 0) wait_neighbours(step, replay ? k0 - 1 : k - kTileLag);
             __syncthreads();
@@ -322,17 +331,21 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile2_kernel(const TileArg
                 __syncthreads();
                 continue;
             }
+            STAMP2(1);
             load_halo((int)(step & 1));
             __syncthreads();
         }
+        STAMP2(2);
         double s1a = 0.0, s1b = 0.0, s1c = 0.0, s2a = 0.0, s2b = 0.0, s2c = 0.0;
         sweep1(s1a, s1b, s1c);
+        STAMP2(3);
         if (replay && k + 1 == target) {  // half step: sweep 1's owned values are final
             ++k;
             break;
         }
         const int bufw = (int)((step + 1) & 1);
         sweep2(bufw, s2a, s2b, s2c);
+        STAMP2(4);
         double v[6] = {s1a, s1b, s1c, s2a, s2b, s2c};
 #pragma unroll
         for (int q = 0; q < 6; ++q) v[q] = warp_sum(v[q]);
@@ -344,7 +357,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile2_kernel(const TileArg
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + (long)tile * kTileFlagStride),
                          "r"(step + 1)
                          : "memory");
-        if (tid == 32 && !replay) {
+        if (tid == 32 && !replay) {  // off the critical path: no barrier waits for it
             for (int sw = 0; sw < 2; ++sw) {
                 const int slot = (int)((k + sw) % kTileSlots);
                 double t0 = 0.0, t1 = 0.0, t2 = 0.0;
@@ -357,18 +370,25 @@ __global__ void __launch_bounds__(kTileThreads, 1) cp_tile2_kernel(const TileArg
                 p[0] = t0;
                 p[1] = t1;
                 p[2] = t2;
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(t.cnt + (long)pair * kTileSlots + slot)
-                             : "memory");
             }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            for (int sw = 0; sw < 2; ++sw)
+                asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(
+                                 t.cnt + (long)pair * kTileSlots + (int)((k + sw) % kTileSlots))
+                             : "memory");
         }
         k += 2;
         ++step;
         have_halo = false;
         if (!replay && ((k - k0) % kTileCk) == 0) {
             store_state((int)(((k - k0) / kTileCk) & 1));
+            __syncthreads();  // the next sweep rewrites the owned nodes being stored
         }
-        __syncthreads();
+        STAMP2(5);
     }
+    if (t.dbg && tid == 0)
+        for (int q = 0; q < kTileDbgPts; ++q) t.dbg[tile * kTileDbgPts + q] = dbg_acc[q];
+#undef STAMP2
     // final barrier with the neighbours: every one of them has finished its
     // replay (including a checkpoint load after a rollback) before the final
     // state overwrites buffer 0
