@@ -141,6 +141,11 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     a.jlo = jlo;
     a.jhi = jhi;
     a.red_out = nullptr;
+    // the branch-free p = 2 shrink (device_common.cuh: shrink2_nb) relies on
+    // mu^2 lying inside the fast sqrt range and mu^2 < DBL_MAX: every step
+    // size of a grid with n < 2^400 does; refuse (loudly) the rest
+    if (!(mu >= 1e-140 && mu <= 1e140))
+        fail(W1MG_EINVAL, "shrink: mu outside the supported range [1e-140, 1e140]");
     a.mu = mu;
     a.zt = shrink_zero_threshold(mu);
     a.tau = tau;

@@ -99,3 +99,14 @@ def test_large_batch_many_levels_smoke():
     dist, dual, iters, conv = w1mg.ml_run_batch(img0, img1, 4, rel_tol=1e-5)
     assert conv.all() and np.isfinite(dist).all() and (dist > 0).all()
     assert (dual < 0).all()  # CP dual value ~ -W1
+
+
+def test_step_size_outside_supported_range_fails_loudly():
+    """The branch-free shrink needs mu^2 inside the fp64 fast-path range:
+    a custom mu outside [1e-140, 1e140] is refused with W1MG_EINVAL instead
+    of computing silently wrong fluxes (the reference accepts any mu > 0)."""
+    from paper_1810_00118_b200 import w1mg as W
+
+    rho = instances.config1_source(16)
+    with pytest.raises(Exception, match="supported range"):
+        W._cp_call(16, rho, None, None, None, 1, 1e-150, 1e-150, -1.0, 5, 0)
