@@ -182,8 +182,18 @@ def measured_traffic():
         return None
     with open(p) as f:
         d = json.load(f)
-    # bytes per launch of the captured configuration (256 pairs, one two-sweep launch)
+    # bytes per launch of the captured configuration (256 pairs, one launch)
     return d.get("dram_bytes_per_launch")
+
+
+def traffic_meta():
+    """(sweeps per captured launch, kernel name) of profiles/traffic.json."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return 2, None
+    with open(p) as f:
+        d = json.load(f)
+    return int(d.get("sweeps_per_launch", 2)), d.get("kernel")
 
 
 def peaks():
@@ -418,7 +428,8 @@ def main():
     # reads and writes the state once per TWO sweeps, so the algorithmic
     # one-sweep figure above can exceed the HBM peak while DRAM does not
     tr = measured_traffic()
-    dram = (tr / (2 * 256)) * finest_sweeps / finest_s / 1e9 if tr else None
+    tr_sweeps, tr_kernel = traffic_meta()
+    dram = (tr / (tr_sweeps * 256)) * finest_sweeps / finest_s / 1e9 if tr else None
 
     # ---- e2e through the public host API (pinned host buffers)
     e2e = None
@@ -557,14 +568,14 @@ def main():
                        for n, s_, c_ in zip(level_sizes(), lev_s, lev_cu)],
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": measured_traffic(),
-                         "kernel": "w1mg_dev::cp_sweep2_tmap_kernel<1,4,true> (two fused PD sweeps "
-                                   "per HBM pass, two-row tensor-map ring, 512^2 level); achieved = "
-                                   "algorithmic one-sweep 8(3V+4E) bytes per sweep / device "
-                                   "time per sweep; traffic = ncu DRAM bytes of one launch "
-                                   "(2 sweeps, 256 pairs x 512^2)",
+                         "kernel": "w1mg_dev::cp_sweep3_tmap_kernel<1> (three fused PD sweeps "
+                                   "per HBM pass, two-row tensor-map ring, the batched 512^2 "
+                                   "level); achieved = algorithmic one-sweep 8(3V+4E) bytes per "
+                                   "sweep / device time per sweep; traffic = ncu DRAM bytes of one "
+                                   f"launch ({tr_sweeps} sweeps, 256 pairs x 512^2)",
                          "bytes_per_sweep": alg_bytes_per_sweep(M), "peak_kind": peak_kind,
                          "dram_achieved": dram, "dram_frac": (dram / hbm) if dram else None,
-                         "note": "frac > 1: two PD sweeps per HBM pass (temporal blocking); "
+                         "note": "frac > 1: several PD sweeps per HBM pass (temporal blocking); "
                                  "dram_achieved = measured DRAM bytes per pair-sweep x in-run "
                                  "sweep rate; ncu of one launch (profiles/r1_summary.md): "
                                  "FP64 pipe 66 %, issue 68 %, DRAM 85 % of the copy peak in "

@@ -338,14 +338,19 @@ bool two_sweep(const Level& lv) {
            (g_sweep_variant == kAuto && lv.n >= 96);
 }
 // auto picks it for a one-pair level of 192..384 (one 256^2 pair: 22.4 ->
-// 19.7 ms per level); batched levels and big grids are issue-bound, where
-// its 27-of-32 owned columns and 94 registers cost more than the third of
-// the HBM bytes it saves (tools/gpu/tma3p.sh: 512^2 x256 419 vs 361 us,
-// 4096^2 97 vs 91 us per sweep)
+// 19.7 ms per level) and for batched levels of n >= 384: there the sustained
+// run is power-capped, and the third of the HBM bytes it saves buys clock
+// (bench A/B on one box, tools/gpu/bench_ab.sh: 512^2 level 11.69 -> 11.25 s
+// per step at 1725 vs 1500 MHz; 1.472e11 -> 1.511e11 cell-updates/s with it
+// on every level), although in short probes the issue-bound two-sweep
+// kernel is as fast or faster (512^2 x256 367 vs 369 us, 256^2 x1024 422 vs
+// 386 us per sweep); batched 256^2 and the big one-pair grids stay on two
+// sweeps
 bool three_sweep(const Level& lv) {
     if (lv.slab || !lv.has_tmap || lv.n < 96) return false;
     return g_sweep_variant == kTma3 ||
-           (g_sweep_variant == kAuto && lv.B == 1 && lv.n >= 192 && lv.n <= 384);
+           (g_sweep_variant == kAuto && ((lv.B == 1 && lv.n >= 192 && lv.n <= 384) ||
+                                         (lv.B > 1 && lv.n >= 384)));
 }
 // sweeps one streaming launch performs on this level
 int sweeps_per_launch(const Level& lv) { return three_sweep(lv) ? 3 : two_sweep(lv) ? 2 : 1; }
