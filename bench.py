@@ -7,10 +7,8 @@ configs[2] (seeded U[0,1] noise on 512x512, Gaussian blur sigma = 8 px with
 reflect boundary, exp(4x) + 1e-6, unit mass; pair i uses seeds 2i, 2i+1),
 each solved by a 5-level CP cascade 32 -> 512 (p = 2, practical steps,
 per-level tolerance 1e-5 * R_cold,l).  A step = one batch of
---pairs pairs per GPU (default 512, half of the 1024-pair config, so the
-default run ends in a few minutes; larger batches fill the GPU longer before
-the per-level tail of slow-converging pairs: measured 1.195e11 / 1.254e11 /
-1.285e11 cell-updates/s at 256 / 512 / 1024 pairs) solved to converged W1.
+--pairs pairs per GPU (default 1024, the config-4 batch) solved to converged
+W1.
 
 value  = cell-updates/s over the whole job: sum over pairs and levels of
          (n_l+1)^2 * sweeps_l, divided by the device time of the K timed steps
@@ -18,13 +16,18 @@ value  = cell-updates/s over the whole job: sum over pairs and levels of
          per-step working set (GBs) exceeds the 126 MB L2.
 e2e    = the same metric through the public C-ABI call w1mg_ml_cp_batch with
          pinned HOST images (H2D of both image stacks and D2H of every pair's
-         W1/dual/iterations inside the timed region).
-Extra: pairs_per_s, time_to_w1_512_s (one pair, device-resident), roofline of
-the fused sweep (dominant kernel), cpu_baseline (oracle port, 1 core).
+         W1/dual/iterations inside the timed region), over --e2e-steps steps.
+Extra: pairs_per_s, time_to_w1_512_s (one pair, device-resident, and e2e),
+config3_pdhg (the G-prox PDHG cascade's time to W1, device and e2e), the
+roofline of the dominant kernel (FP64 pipe against an in-run DFMA peak, plus
+DRAM and one-sweep-equivalent HBM rates), cpu_baseline (the reference build,
+1 core, bounded sample) and parity_sample (8 pairs of the timed batch vs the
+C oracle on the same sources).
 
-Multi-GPU (torchrun): every rank solves its own --pairs pairs (distinct seeds;
-weak scaling, no collective on the data path; one barrier and a max-reduce of
-the timings).
+Multi-GPU: `--gpus N` outside torchrun re-executes itself as N ranks
+(torch.distributed.run, 127.0.0.1); every rank solves its own --pairs pairs
+(distinct seeds; weak scaling, no collective on the data path; a barrier and
+max/sum reductions of the timings).
 --impl reference runs the reference C++ solver (oracle/_ref, compiled from
 /root/reference) on the host cores instead, rank 0 only.
 """
@@ -173,29 +176,6 @@ def dist_setup():
     return world, rank, local
 
 
-def measured_traffic():
-    """DRAM bytes (read + write) per launch of the dominant kernel from the
-    committed ncu --set full capture (profiles/traffic.json: 256 pairs x 512^2,
-    one two-sweep launch = 2 x 7.54 GB algorithmic one-sweep bytes), or None."""
-    p = os.path.join(ROOT, "profiles", "traffic.json")
-    if not os.path.exists(p):
-        return None
-    with open(p) as f:
-        d = json.load(f)
-    # bytes per launch of the captured configuration (256 pairs, one launch)
-    return d.get("dram_bytes_per_launch")
-
-
-def traffic_meta():
-    """(sweeps per captured launch, kernel name) of profiles/traffic.json."""
-    p = os.path.join(ROOT, "profiles", "traffic.json")
-    if not os.path.exists(p):
-        return 2, None
-    with open(p) as f:
-        d = json.load(f)
-    return int(d.get("sweeps_per_launch", 2)), d.get("kernel")
-
-
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -206,13 +186,6 @@ def peaks():
 
 
 # ------------------------------------------------------------------ CPU legs
-def cpu_cascade_oracle(pair, use_reference=False):
-    """One pair through the CPU cascade: the C oracle (port) or the reference
-    build (oracle/_ref cp_run per level with Eq. 14/15 warm starts restated in
-    the oracle).  Returns (W1, sweeps per level, seconds)."""
-    return solve_cascade_cpu(pair_sources(pair), use_reference)
-
-
 def pair_sources(pair):
     """Per-level sources of config-4 pair `pair` (host restriction rule)."""
     from oracle import Oracle
@@ -305,19 +278,189 @@ def workload_config(args, pairs):
             "parallelism": f"independent pairs per GPU ({args.gpus} GPU(s)), no collective"}
 
 
+# ------------------------------------------------------------------ launcher
+def free_port():
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def relaunch_cmd(args, argv):
+    """`--gpus N` (N > 1) outside torchrun: the command that re-executes this
+    script as N ranks, one process per GPU (torch.distributed.run on
+    127.0.0.1), or None when no relaunch is needed."""
+    if args.gpus <= 1 or os.environ.get("WORLD_SIZE"):
+        return None
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+            f"--master-port={free_port()}", os.path.abspath(__file__)] + list(argv)
+
+
+def shard(rank, pairs_per_rank):
+    """Weak scaling: rank r solves pairs [r*B, (r+1)*B) of config 4 (pair i
+    uses seeds 2i, 2i+1); no data crosses ranks."""
+    return rank * pairs_per_rank, pairs_per_rank
+
+
+class Ranks:
+    """Barrier and max / sum over ranks (NCCL on the GPUs, gloo in --dry-run)."""
+
+    def __init__(self, world, device):
+        self.world = world
+        self.device = device
+        self.pg = None
+        if world > 1:
+            import torch.distributed as dist
+
+            if device.type == "cuda":
+                dist.init_process_group("nccl", device_id=device)
+            else:
+                dist.init_process_group("gloo")
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def _reduce(self, x, op):
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device=self.device)
+        self.pg.all_reduce(t, op=op)
+        return float(t.item())
+
+    def max(self, x):
+        return self._reduce(x, self.pg.ReduceOp.MAX) if self.pg else x
+
+    def sum(self, x):
+        return self._reduce(x, self.pg.ReduceOp.SUM) if self.pg else x
+
+    def gather(self, obj):
+        if not self.pg:
+            return [obj]
+        out = [None] * self.world
+        self.pg.all_gather_object(out, obj)
+        return out
+
+    def close(self):
+        if self.pg:
+            self.pg.barrier()
+            self.pg.destroy_process_group()
+
+
+def dry_run(args, world, rank):
+    """--dry-run: the launcher, sharding and cross-rank aggregation of the
+    real bench on CPU ranks (gloo), with the solve replaced by a stub that
+    reports one sweep per level per pair (tests/test_bench_launcher.py)."""
+    import torch
+
+    R = Ranks(world, torch.device("cpu"))
+    first, B = shard(rank, args.pairs)
+    pairs = list(range(first, first + B))
+    R.barrier()
+    t0 = time.perf_counter()
+    cu = 0.0
+    for _ in range(args.steps):
+        cu += cell_updates(np.ones((B, LEVELS)))
+    t = time.perf_counter() - t0
+    T = R.max(t)
+    cu_all = R.sum(cu)
+    shards = R.gather(pairs)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "steps": args.steps,
+                          "cell_updates": cu_all, "max_seconds": T, "shards": shards,
+                          "config": workload_config(args, args.pairs * world)}), flush=True)
+    R.close()
+
+
+# ------------------------------------------------------------------ parity sample
+def parity_sample(img0, img1, dist, iters, k=8):
+    """Per-pair parity of the TIMED batch itself: k pairs spread over the
+    batch; their GPU-built images are copied back, restricted by the device
+    rule (w1mg.ml_sources: the same bits the batch built, reductions split by
+    row count only) and solved by the C oracle (restatement of
+    proj/src/solver_cp.cpp:113-147 + Eq. 14/15), one pair per host thread,
+    outside the timed region."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import Oracle
+    from paper_1810_00118_b200 import w1mg
+
+    B = dist.shape[0]
+    idx = sorted(set(np.linspace(0, B - 1, min(k, B)).round().astype(int).tolist()))
+    srcs = [w1mg.ml_sources(img0[i].cpu().numpy(), img1[i].cpu().numpy(), LEVELS) for i in idx]
+    O = Oracle()
+    t = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=min(len(idx), os.cpu_count() or 1)) as ex:
+        refs = list(ex.map(lambda s: O.ml_cp_run(s, p=1, rel_tol=REL_TOL), srcs))
+    secs = time.perf_counter() - t
+    rows = []
+    for i, r in zip(idx, refs):
+        g = [int(x) for x in iters[i]]
+        rows.append({"pair": i, "w1_gpu": float(dist[i]), "w1_cpu": r.distance,
+                     "rel_err": abs(float(dist[i]) - r.distance) / r.distance,
+                     "sweeps_gpu": g, "sweeps_cpu": r.level_iters,
+                     "same_sweeps": g == r.level_iters})
+    return {"source": "pairs of the last timed step (bench GPU images, device restriction) vs "
+                      "the C oracle cascade on the same sources",
+            "pairs": rows, "max_rel_err": max(x["rel_err"] for x in rows),
+            "all_within_1e-4": all(x["rel_err"] <= 1e-4 for x in rows),
+            "all_same_sweeps": all(x["same_sweeps"] for x in rows), "cpu_seconds": secs}
+
+
+# ------------------------------------------------------------------ config 3
+def config3_time_to_w1(reps=3):
+    """Config 3 (BASELINE.json configs[2]): G-prox PDHG cascade 32 -> 512 to
+    rel tol 1e-5 * G_cold,l.  Device = the cascade's device time (CUDA events
+    from resident per-level sources to W1); e2e = wall time of the public call
+    w1mg.ml_pdhg_run with host sources (H2D, solve, D2H of fields and W1)."""
+    from paper_1810_00118_b200 import instances, w1mg
+
+    rhos = instances.ml_sources(*instances.config3_images(m=M), LEVELS)
+    r = w1mg.ml_pdhg_run(rhos, rel_tol=REL_TOL)
+    dev, wall = [], []
+    for _ in range(reps):
+        t = time.perf_counter()
+        r = w1mg.ml_pdhg_run(rhos, rel_tol=REL_TOL)
+        wall.append(time.perf_counter() - t)
+        dev.append(r.total_seconds)
+    return {"workload": "config3: G-prox PDHG cascade 32->512, p=2, rel tol 1e-5 * G_cold,l",
+            "device_s": min(dev), "e2e_s": min(wall), "W1": r.distance,
+            "iters": [l.iters for l in r.levels],
+            "level_s": [l.seconds for l in r.levels],
+            "us_per_iter_finest": 1e6 * r.levels[-1].seconds / max(r.levels[-1].iters, 1)}
+
+
 # ------------------------------------------------------------------ our arm
-def main():
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pairs", type=int, default=512, help="pairs per GPU per step")
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--pairs", type=int, default=1024,
+                    help="pairs per GPU per step (config 4: 1024)")
+    ap.add_argument("--e2e-steps", type=int, default=5,
+                    help="steps of the e2e leg (at most --steps)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / parity legs")
     ap.add_argument("--no-e2e", action="store_true")
-    args = ap.parse_args()
+    ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
+    args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
+    cmd = relaunch_cmd(args, argv)
+    if cmd:
+        sys.exit(subprocess.call(cmd))
     world, rank, local = dist_setup()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        dry_run(args, world, rank)
+        return
 
     if args.impl == "reference":
         if rank == 0:
@@ -328,19 +471,13 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    pg = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
-        pg = dist
+    R = Ranks(world, dev)
 
     from paper_1810_00118_b200 import _lib
     from paper_1810_00118_b200._lib import MLParams, check
     import ctypes as C
 
-    B = args.pairs
-    first = rank * B
+    first, B = shard(rank, args.pairs)
     img0, img1 = make_images_gpu(first, B, dev)
 
     ctx = _lib.Context(local)
@@ -363,22 +500,7 @@ def main():
     def barrier():
         torch.cuda.synchronize(dev)
         ctx.synchronize()
-        if pg:
-            pg.barrier()
-
-    def max_over_ranks(x):
-        if not pg:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum_over_ranks(x):
-        if not pg:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        pg.all_reduce(t)
-        return float(t.item())
+        R.barrier()
 
     for _ in range(args.warmup):
         step_dev()
@@ -411,29 +533,65 @@ def main():
         ev1.record(cstream)
         barrier()
         torch.cuda.profiler.stop()
+        # FP64 peak under the same thermal / power state (roofline denominator)
+        fp64_peak = C.c_double()
+        check(L.w1mg_fp64_peak_probe(ctx.h, 1 << 17, C.byref(fp64_peak)))
     t_local = ev0.elapsed_time(ev1) * 1e-3
     launches = ctx.launches - launches0
-    T = max_over_ranks(t_local)
-    cu_all = sum_over_ranks(cu)
+    T = R.max(t_local)
+    cu_all = R.sum(cu)
     value = cu_all / T
     pairs_per_s = args.pairs * world * args.steps / T
+    last_dist = dist_d.cpu().numpy()
+    last_iters = iters_d.cpu().numpy()
+    conv_all = bool(conv_d.cpu().numpy().all())
 
-    # roofline of the fused sweep at the finest level, measured in the timed
-    # region: algorithmic bytes of every pair-sweep / device time of the
-    # finest level's sweep loop (includes early-exit launches of converged pairs)
+    # roofline of the dominant kernel (the three-sweep pass over the batched
+    # 512^2 level), from the finest level's device time inside the timed
+    # region.  It is FP64/issue-bound (ncu: FP64 pipe 65 %, issue 66 %), so
+    # the primary figure is the FP64 roofline against the in-run DFMA peak;
+    # DRAM and the one-sweep algorithmic-bytes rate explain the HBM side.
     hbm, peak_kind = peaks()
-    achieved = finest_sweeps * alg_bytes_per_sweep(M) / finest_s / 1e9
-    # bytes the kernel actually moves (ncu capture: one launch = 2 sweeps of
-    # 256 pairs), at the in-run sweep rate: the temporally blocked kernel
-    # reads and writes the state once per TWO sweeps, so the algorithmic
-    # one-sweep figure above can exceed the HBM peak while DRAM does not
-    tr = measured_traffic()
-    tr_sweeps, tr_kernel = traffic_meta()
-    dram = (tr / (tr_sweeps * 256)) * finest_sweeps / finest_s / 1e9 if tr else None
+    node_sweeps_s = finest_sweeps * (M + 1) ** 2 / finest_s
+    trj = {}
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            trj = json.load(f)
+    flops_ns = trj.get("fp64_flops_per_node_sweep")
+    inst_ns = trj.get("fp64_inst_per_node_sweep")
+    tr = trj.get("dram_bytes_per_launch")
+    tr_ns = trj.get("node_sweeps_per_launch")
+    eff = finest_sweeps * alg_bytes_per_sweep(M) / finest_s / 1e9
+    dram = tr / tr_ns * node_sweeps_s / 1e9 if tr and tr_ns else None
+    peak_tf = float(fp64_peak.value)
+    ach_tf = flops_ns * node_sweeps_s / 1e12 if flops_ns else None
+    roofline = {
+        "bound": "fp64", "unit": "TFLOP/s", "achieved": ach_tf, "peak": peak_tf,
+        "frac": (ach_tf / peak_tf) if ach_tf else None,
+        "pipe_frac": (inst_ns * node_sweeps_s / (peak_tf * 1e12 / 2)) if inst_ns else None,
+        "peak_kind": "measured in this run (w1mg_fp64_peak_probe: DFMA chains on every SM, "
+                     "right after the timed region)",
+        "traffic": tr,
+        "kernel": trj.get("kernel"),
+        "per_unit": {"fp64_flops_per_node_sweep": flops_ns, "fp64_inst_per_node_sweep": inst_ns,
+                     "source": "profiles/traffic.json (ncu --set full of one launch)"},
+        "dram": {"achieved": dram, "peak": hbm, "unit": "GB/s",
+                 "frac": (dram / hbm) if dram else None, "peak_kind": peak_kind,
+                 "note": "ncu DRAM bytes per node-sweep x in-run node-sweep rate"},
+        "effective_hbm": {"achieved": eff, "peak": hbm, "unit": "GB/s", "frac": eff / hbm,
+                          "bytes_per_sweep": alg_bytes_per_sweep(M),
+                          "note": "one-sweep algorithmic 8(3V+4E) bytes per sweep / time per "
+                                  "sweep; > 1 because three PD sweeps share one HBM pass"},
+        "note": "achieved = FP64 flops (DADD, DMUL 1, DFMA 2) per node-sweep x node-sweeps/s "
+                "of the 512^2 level in the timed region; pipe_frac = FP64 instructions / "
+                "DFMA issue peak (the pipe-occupancy reading)",
+    }
 
     # ---- e2e through the public host API (pinned host buffers)
     e2e = None
     if not args.no_e2e:
+        ks = max(1, min(args.e2e_steps, args.steps))
         h0 = torch.empty((B, M, M), dtype=torch.float64, pin_memory=True)
         h1 = torch.empty((B, M, M), dtype=torch.float64, pin_memory=True)
         h0.copy_(img0)
@@ -451,30 +609,29 @@ def main():
                                      C.cast(oi.data_ptr(), C.POINTER(C.c_long)),
                                      C.cast(oc.data_ptr(), C.POINTER(C.c_int))))
 
-        step_host()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         ecu = 0.0
         e0.record(cstream)
-        for _ in range(args.steps):
+        for _ in range(ks):
             step_host()
             ecu += cell_updates(oi.numpy())
         e1.record(cstream)
         barrier()
-        te = max_over_ranks(e0.elapsed_time(e1) * 1e-3)
-        e2e = {"value": sum_over_ranks(ecu) / te, "unit": UNIT,
+        te = R.max(e0.elapsed_time(e1) * 1e-3)
+        e2e = {"value": R.sum(ecu) / te, "unit": UNIT,
                "h2d_bytes_per_step": 2 * args.pairs * world * M * M * 8,
                "d2h_bytes_per_step": args.pairs * world * (8 + 8 + 8 * LEVELS + 4),
-               "pairs_per_s": args.pairs * world * args.steps / te}
+               "pairs_per_s": args.pairs * world * ks / te, "steps": ks,
+               "api": "w1mg_ml_cp_batch (C-ABI, pinned host images in, W1/dual/sweeps out)"}
         del h0, h1
 
     # ---- single-pair time-to-converged-W1 at 512^2 (device-resident input)
     t_single = None
     t_single_e2e = None
+    cfg3 = None
     if rank == 0:
-        one = [None]
-
         def single():
             check(L.w1mg_ml_cp_batch_dev(ctx.h, 1, M, C.c_void_p(img0.data_ptr()),
                                          C.c_void_p(img1.data_ptr()), C.byref(prm),
@@ -491,7 +648,6 @@ def main():
             single()
             ts.append(time.perf_counter() - t0)
         t_single = min(ts)
-        one[0] = float(dist_d[0].item())
         # the same through the host API: H2D of the two 512^2 images, the
         # cascade, D2H of W1 / dual / sweeps (SURVEY 8d "end-to-end time")
         ha = img0[:1].cpu().numpy()
@@ -515,6 +671,7 @@ def main():
             single_host()
             te2e.append(time.perf_counter() - t0)
         t_single_e2e = min(te2e)
+        cfg3 = config3_time_to_w1()
 
     # ---- CPU baseline + per-pair parity sample (rank 0, N = 1 only)
     cpu = None
@@ -524,36 +681,21 @@ def main():
 
         # the reference's own build (oracle/_ref) on a bounded sample: every
         # level of pair 0's cascade capped at REF_SWEEP_CAP sweeps (a full
-        # converged pair costs ~45 s there); the C oracle (bit-identical
-        # restatement, ~3.4x faster than the reference's 9-pass loop) runs the
-        # full converged cascade for the parity sample
+        # converged pair costs ~45 s there)
         use_ref = have_reference()
-        w1_cpu, its_cpu, secs_cpu = cpu_cascade_oracle(0)
-        if use_ref:
-            _, its_ref, secs_ref = solve_cascade_cpu(pair_sources(0), use_reference=True,
-                                                     max_iters=REF_SWEEP_CAP)
-        else:
-            its_ref, secs_ref = its_cpu, secs_cpu
+        srcs0 = pair_sources(0)
+        _, its_ref, secs_ref = solve_cascade_cpu(srcs0, use_reference=use_ref,
+                                                 max_iters=REF_SWEEP_CAP)
         cpu = {"value": cell_updates([its_ref]) / secs_ref, "unit": UNIT, "cores": 1,
                "kind": "reference" if use_ref else "port",
                "sample": ("config-4 pair 0 (seeds 0,1), 5-level CP cascade 32->512 with at most "
                           f"{REF_SWEEP_CAP} sweeps per level through the reference's cp_run "
                           "(oracle/_ref, unmodified sources) and the restated Eq. 14/15 warm "
                           "starts" if use_ref else
-                          "config-4 pair 0 (seeds 0,1): one converged 5-level CP cascade 32->512 "
-                          "through the C oracle (bit-identical restatement of the reference)")
-                         + ", 1 thread",
-               "oracle_port_value": cell_updates([its_cpu]) / secs_cpu,
-               "pairs_per_s": 1.0 / secs_cpu}
-        # the bench images come from GPU GEMM blur: re-solve pair 0 from the
-        # numpy images for an exact-input comparison
-        from paper_1810_00118_b200 import instances, w1mg
-
-        a, b = instances.config4_pair(0)
-        g = w1mg.ml_run_batch(a[None], b[None], LEVELS, rel_tol=REL_TOL)
-        parity = {"pair": 0, "w1_gpu": float(g[0][0]), "w1_cpu": w1_cpu,
-                  "rel_err": abs(float(g[0][0]) - w1_cpu) / w1_cpu,
-                  "sweeps_gpu": [int(x) for x in g[2][0]], "sweeps_cpu": list(its_cpu)}
+                          "config-4 pair 0 (seeds 0,1), 5-level CP cascade 32->512 with at most "
+                          f"{REF_SWEEP_CAP} sweeps per level through the C oracle")
+                         + ", 1 thread"}
+        parity = parity_sample(img0, img1, last_dist, last_iters)
 
     if rank == 0:
         line = {
@@ -561,32 +703,18 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(args, args.pairs * world),
-            "pairs_per_s": pairs_per_s, "time_to_w1_512_s": t_single,
-            "time_to_w1_512_e2e_s": t_single_e2e,
+            "pairs_per_s": pairs_per_s, "all_converged": conv_all,
+            "time_to_w1_512_s": t_single, "time_to_w1_512_e2e_s": t_single_e2e,
+            "config3_pdhg": cfg3,
             "levels": [{"n": n, "seconds_per_step": s_ / args.steps,
                         "cell_updates_per_s": c_ / s_}
                        for n, s_, c_ in zip(level_sizes(), lev_s, lev_cu)],
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": measured_traffic(),
-                         "kernel": "w1mg_dev::cp_sweep3_tmap_kernel<1> (three fused PD sweeps "
-                                   "per HBM pass, two-row tensor-map ring, the batched 512^2 "
-                                   "level); achieved = algorithmic one-sweep 8(3V+4E) bytes per "
-                                   "sweep / device time per sweep; traffic = ncu DRAM bytes of one "
-                                   f"launch ({tr_sweeps} sweeps, 256 pairs x 512^2)",
-                         "bytes_per_sweep": alg_bytes_per_sweep(M), "peak_kind": peak_kind,
-                         "dram_achieved": dram, "dram_frac": (dram / hbm) if dram else None,
-                         "note": "frac > 1: several PD sweeps per HBM pass (temporal blocking); "
-                                 "dram_achieved = measured DRAM bytes per pair-sweep x in-run "
-                                 "sweep rate; ncu of one launch (profiles/r1_summary.md): "
-                                 "FP64 pipe 66 %, issue 68 %, DRAM 85 % of the copy peak in "
-                                 "actual bytes -- balanced, power-capped in the sustained run"},
+            "roofline": roofline,
             "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
             "cpu_baseline": cpu, "parity_sample": parity,
         }
         print(json.dumps(line), flush=True)
-    if pg:
-        pg.barrier()
-        pg.destroy_process_group()
+    R.close()
 
 
 if __name__ == "__main__":

@@ -184,6 +184,14 @@ int w1mg_ml_cp_run(w1mg_ctx* ctx, int n_finest, const double* rho_levels,
 int w1mg_ml_cp_batch(w1mg_ctx* ctx, int npairs, int m, const double* img0s,
                      const double* img1s, const w1mg_ml_params* prm, double* distance,
                      double* dual, long* iters, int* converged);
+/* w1mg_ml_cp_batch plus every pair's finest-level fields from its latest
+ * buffer (pair-major: mx, my npairs*m*(m+1); phi npairs*(m+1)^2) and final
+ * residual (npairs); field pointers may be NULL.  For per-pair parity checks
+ * of the batched engines. */
+int w1mg_ml_cp_batch_fields(w1mg_ctx* ctx, int npairs, int m, const double* img0s,
+                            const double* img1s, const w1mg_ml_params* prm, double* distance,
+                            double* dual, long* iters, int* converged, double* mx, double* my,
+                            double* phi, double* fpr_final);
 int w1mg_ml_cp_batch_dev(w1mg_ctx* ctx, int npairs, int m, const double* img0s_dev,
                          const double* img1s_dev, const w1mg_ml_params* prm,
                          double* distance_dev, double* dual_dev, long* iters_dev,
@@ -303,6 +311,11 @@ int w1mg_set_option(const char* name, long value);
  * writes the mean milliseconds per sweep launch (CUDA events). */
 int w1mg_sweep_probe(w1mg_ctx* ctx, int n, int B, int pnorm, long warm, long iters,
                      double* ms_per_sweep);
+
+/* Measured FP64 peak of this device (TFLOP/s, DFMA = 2 flops): SMs x 4 blocks
+ * x 256 threads, 8 independent DFMA chains of `iters` steps each, CUDA events.
+ * The denominator of the sweep kernels' FP64-pipe roofline (bench.py). */
+int w1mg_fp64_peak_probe(w1mg_ctx* ctx, long iters, double* tflops);
 
 /* Diagnostics: compares the kernels' branch-free sqrt / division / p = 2
  * shrink (restated fast paths, device_common.cuh) with the library operators

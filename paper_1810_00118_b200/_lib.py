@@ -101,6 +101,10 @@ def lib():
                                      C.POINTER(LevelStatsC), _dp, C.c_long, C.POINTER(CPReport)]
         L.w1mg_ml_cp_batch.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp,
                                        C.POINTER(MLParams), _dp, _dp, _lp, _ip]
+        L.w1mg_fp64_peak_probe.argtypes = [C.c_void_p, C.c_long, _dp]
+        L.w1mg_ml_cp_batch_fields.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp,
+                                              C.POINTER(MLParams), _dp, _dp, _lp, _ip, _dp, _dp,
+                                              _dp, _dp]
         L.w1mg_ml_cp_batch_dev.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                            C.POINTER(MLParams), C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_void_p]

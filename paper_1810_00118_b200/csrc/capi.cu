@@ -507,6 +507,52 @@ int w1mg_ml_cp_batch(w1mg_ctx* c, int npairs, int m, const double* img0s, const 
     });
 }
 
+// Batched cascades with every pair's finest-level fields and residual copied
+// back (parity checks of the batched engines against per-pair oracle runs).
+int w1mg_ml_cp_batch_fields(w1mg_ctx* c, int npairs, int m, const double* img0s,
+                            const double* img1s, const w1mg_ml_params* prm, double* distance,
+                            double* dual, long* iters, int* converged, double* mx, double* my,
+                            double* phi, double* fpr_final) {
+    return guard([&] {
+        check_n(m);
+        check_ml(prm);
+        if (npairs < 1 || npairs > 65535) fail(W1MG_EINVAL, "npairs must be in [1, 65535]");
+        const size_t MM = (size_t)npairs * m * m;
+        double* d0 = c->get<double>("in.img0s", MM);
+        double* d1 = c->get<double>("in.img1s", MM);
+        CK(cudaMemcpyAsync(d0, img0s, MM * 8, cudaMemcpyDefault, c->stream));
+        CK(cudaMemcpyAsync(d1, img1s, MM * 8, cudaMemcpyDefault, c->stream));
+        std::vector<Level> lv =
+            make_levels(c, "mlb", m, prm->levels, npairs, prm->step_mode, nullptr, 0);
+        for (auto& L : lv) zero_level(c, L);
+        build_sources(c, lv, d0, d1, m);
+        long* oi = c->get<long>("out.iters", (size_t)npairs * prm->levels);
+        run_cascade(c, lv, *prm, oi, nullptr, nullptr, nullptr);
+        double* od = c->get<double>("out.dist", npairs);
+        double* ou = c->get<double>("out.dual", npairs);
+        level_values(c, lv.back(), prm->pnorm, od, ou);
+        const Level& F = lv.back();
+        std::vector<PairCtl> hc(npairs);
+        CK(cudaMemcpyAsync(hc.data(), F.ctl, npairs * sizeof(PairCtl), cudaMemcpyDeviceToHost,
+                           c->stream));
+        if (distance) CK(cudaMemcpyAsync(distance, od, npairs * 8, cudaMemcpyDefault, c->stream));
+        if (dual) CK(cudaMemcpyAsync(dual, ou, npairs * 8, cudaMemcpyDefault, c->stream));
+        if (iters)
+            CK(cudaMemcpyAsync(iters, oi, (size_t)npairs * prm->levels * sizeof(long),
+                               cudaMemcpyDefault, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const size_t E = (size_t)m * (m + 1), V = (size_t)(m + 1) * (m + 1);
+        for (int b = 0; b < npairs; ++b) {
+            if (converged) converged[b] = (hc[b].fpr < hc[b].tol) ? 1 : 0;
+            if (fpr_final) fpr_final[b] = hc[b].fpr;
+            if (mx) get_xedges(c, F, b, MX0 + hc[b].cur, mx + b * E);
+            if (my) get_yedges(c, F, b, MY0 + hc[b].cur, my + b * E);
+            if (phi) get_nodes(c, F, b, PHI0 + hc[b].cur, phi + b * V);
+        }
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
 // Eq. 14 / Eq. 15 on single reference-layout fields (value API).
 int w1mg_interpolate_scalar(w1mg_ctx* c, int nc, const double* coarse, double* fine) {
     return guard([&] {
@@ -640,6 +686,27 @@ int w1mg_sweep_probe(w1mg_ctx* c, int n, int B, int pnorm, long warm, long iters
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, c->t0, c->t1));
         *ms_per_sweep = ms / (double)iters;
+    });
+}
+
+// Measured FP64 pipe peak (the denominator of the sweep kernels' FP64
+// roofline): every thread of SMs x 4 blocks x 256 threads runs 8 independent
+// DFMA chains of `iters` steps; flops = 2 per DFMA.  Timed with CUDA events.
+int w1mg_fp64_peak_probe(w1mg_ctx* c, long iters, double* tflops) {
+    return guard([&] {
+        if (iters < 1 || !tflops) fail(W1MG_EINVAL, "fp64 probe: bad arguments");
+        double* sink = c->get<double>("probe.fp64", 1);
+        const int blocks = c->num_sms * 4;
+        fp64_peak_kernel<<<blocks, 256, 0, c->stream>>>(iters / 4, sink);  // warm-up
+        CK(cudaEventRecord(c->t0, c->stream));
+        fp64_peak_kernel<<<blocks, 256, 0, c->stream>>>(iters, sink);
+        CK(cudaEventRecord(c->t1, c->stream));
+        CK(cudaGetLastError());
+        c->launches += 2;
+        CK(cudaEventSynchronize(c->t1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->t0, c->t1));
+        *tflops = 2.0 * 8.0 * (double)iters * blocks * 256 / (ms * 1e-3) / 1e12;
     });
 }
 

@@ -146,6 +146,7 @@ __device__ __forceinline__ void finish_sweep2(const SweepArgs& a, int pair, int 
         // keep the input buffer as "latest" and replay A in the fix-up launch
         ctl->cur = parity;
         ctl->redo = 1;
+        ctl->rf[0] = fA;
         ctl->done = 1;
         atomicAdd(a.ndone, 1);
     } else {

@@ -96,6 +96,7 @@ __device__ __forceinline__ void finish_sweep3(const SweepArgs& a, int pair, int 
         // record their residuals
         ctl->cur = parity;
         ctl->redo = stop_at + 1;
+        for (int q = 0; q <= stop_at; ++q) ctl->rf[stop_at - q] = f[q];  // rf[redo - 1] = next
         ctl->done = 1;
         atomicAdd(a.ndone, 1);
     } else {

@@ -44,6 +44,9 @@ struct PairCtl {
     int cur;        // buffer parity holding the latest state
     int nonfinite;  // residual was NaN/Inf
     int redo;       // a multi-sweep launch stopped after its first (second) sweep: replay 1 (2)
+    double rf[2];   // residuals that launch computed for the replayed sweeps, rf[redo - 1] is
+                    // the next one: the replay records them instead of its own re-summation,
+                    // so history, fpr and `converged` are the values the stop was decided on
 };
 
 // Launch gate shared by the single-sweep kernels.  parity >= 0: a normal
@@ -244,6 +247,7 @@ __device__ __forceinline__ void finalize_pair(const SweepArgs& a, int pair, int 
     double fpr = kPlusCross ? a.h2 * (sdm2 / a.mu + sdp2 / a.tau + 2.0 * scr)
                             : a.h2 * (sdm2 / a.mu + sdp2 / a.tau - 2.0 * scr);
     long k = ctl->it;
+    if (ctl->redo) fpr = ctl->rf[ctl->redo - 1];
     if (a.hist && k < a.hist_cap) a.hist[(long)pair * a.hist_cap + k] = fpr;
     ctl->it = k + 1;
     ctl->fpr = fpr;

@@ -245,11 +245,13 @@ dim3 node_grid(int n, int B, dim3 blk) {
     return dim3((n + 1 + blk.x - 1) / blk.x, (n + 1 + blk.y - 1) / blk.y, B);
 }
 
-// compensated per-pair reduction, out[b] = (sum f * s1) * s2
+// compensated per-pair reduction, out[b] = (sum f * s1) * s2.  The split of
+// a pair's rows over G blocks depends on the row count only, never on the
+// batch size, so a pair's sources, W1 and dual value carry the same bits
+// whether it is solved alone or inside any batch.
 template <class F>
 void reduce_pairs(w1mg_ctx* c, F f, int w, int rows, int B, double s1, double s2, double* out) {
-    int G = (2 * c->num_sms + B - 1) / B;
-    if (G > 64) G = 64;
+    int G = 64;
     if (G > rows) G = rows;
     if (G < 1) G = 1;
     double2* part = c->get<double2>("reduce.partial", (size_t)G * B);
@@ -423,7 +425,8 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
            std::to_string(lv.grid2w.x) + ":" + std::to_string(lv.grid2t.x) + ":" +
            std::to_string(lv.grid3.x) + ":B" +
            std::to_string(lv.B) + ":v" +
-           std::to_string(g_sweep_variant);
+           std::to_string(g_sweep_variant) + ":nw" + std::to_string(lv.tmap_nw) + ":pdl" +
+           std::to_string(g_pdl);
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) return it->second;
     cudaGraph_t g;
@@ -445,9 +448,11 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
 
 // Tail compaction (W1MG_COMPACT, default on): once at most half of a batch
 // is still running, launch grids span only a power-of-two bucket >= the
-// running count, with strips re-split for that many pairs.  Pair results do
-// not depend on the launch geometry (each pair's sweep and residual order are
-// fixed), so this only removes the early-exit blocks of stopped pairs.
+// running count, with strips re-split for that many pairs.  Fields never
+// depend on the launch geometry (every node's arithmetic is fixed); the
+// residual sums are reassociated with the strip split, so a residual within a
+// few ulps of the tolerance could stop one sweep apart -- the residual that
+// decided a stop is the one recorded (PairCtl::rf), so `converged` is exact.
 bool g_compact = true;
 int g_compact_step = 1 << 30;  // bucket granularity (W1MG_COMPACT_STEP; default: powers of two)
 

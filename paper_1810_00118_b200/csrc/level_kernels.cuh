@@ -276,6 +276,23 @@ __global__ void harvest_kernel(const PairCtl* __restrict__ ctl, int npairs, int 
     if (tol) tol[(long)b * levels + level] = ctl[b].tol;
 }
 
+// FP64 peak probe: 8 independent DFMA chains per thread (latency hidden by
+// 8 chains x 32 warps per SM); the result is stored only if it is impossible,
+// so the chains cannot be optimised away.
+__global__ void __launch_bounds__(256) fp64_peak_kernel(long iters, double* sink) {
+    double x[8];
+    const double a = 1.0 + 1e-12 * threadIdx.x, b = -1e-13;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = q + blockIdx.x * 1e-9;
+    for (long k = 0; k < iters; ++k)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = fma(x[q], a, b);
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += x[q];
+    if (s == -1.2345e300) *sink = s;
+}
+
 __global__ void converged_kernel(const PairCtl* __restrict__ ctl, int npairs, int* conv) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= npairs) return;

@@ -451,6 +451,32 @@ def ml_run_batch(img0s: np.ndarray, img1s: np.ndarray, levels: int, p: PNorm = P
     return dist, dual, iters, conv.astype(bool)
 
 
+def ml_run_batch_fields(img0s: np.ndarray, img1s: np.ndarray, levels: int,
+                        p: PNorm = PNorm.p2, rel_tol: float = 1e-5, eps=None,
+                        max_iters: int = 5_000_000, step_mode: StepMode = StepMode.practical):
+    """ml_run_batch plus every pair's finest-level fields: returns
+    (distance, dual, iters, converged, mx[B], my[B], phi[B], fpr_final[B])."""
+    img0s = np.ascontiguousarray(img0s, dtype=np.float64)
+    img1s = np.ascontiguousarray(img1s, dtype=np.float64)
+    B, m = img0s.shape[0], img0s.shape[1]
+    prm, keep = _ml_params(levels, p, step_mode, rel_tol, eps, max_iters)
+    dist = np.zeros(B)
+    dual = np.zeros(B)
+    iters = np.zeros((B, levels), dtype=np.int64)
+    conv = np.zeros(B, dtype=np.int32)
+    mx = np.empty((B, m + 1, m))
+    my = np.empty((B, m, m + 1))
+    phi = np.empty((B, m + 1, m + 1))
+    fpr = np.empty(B)
+    check(_lib.lib().w1mg_ml_cp_batch_fields(_ctx(), B, m, ptr(img0s), ptr(img1s), C.byref(prm),
+                                             ptr(dist), ptr(dual),
+                                             iters.ctypes.data_as(_lib._lp),
+                                             conv.ctypes.data_as(_lib._ip), ptr(mx), ptr(my),
+                                             ptr(phi), ptr(fpr)))
+    del keep
+    return dist, dual, iters, conv.astype(bool), mx, my, phi, fpr
+
+
 def interpolate_scalar(coarse: ScalarField, fine: GridSpec) -> ScalarField:
     """Eq. 14 on the GPU."""
     if fine.n != 2 * coarse.grid.n:
