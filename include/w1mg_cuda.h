@@ -89,7 +89,7 @@ typedef struct w1mg_ml_params {
 
 /* ---------------------------------------------------------------- context */
 /* A context owns one stream, its device buffers, cached CUDA graphs and the
- * cuBLAS handle of one device.  It is not thread-safe: use one per host
+ * Poisson DCT plans of one device.  It is not thread-safe: use one per host
  * thread.  w1mg_ctx_create makes `device` current on the calling thread;
  * later calls on the context expect that device to be current (one process
  * or thread per GPU, the model of the multi-GPU paths).  The engine switches
@@ -298,9 +298,7 @@ int w1mg_set_tail_compaction(int on);
  * W1MG_PDHG_SMALL. */
 int w1mg_set_pdhg_small(int mode);
 /* Engine tuning switches by name (process-wide; each also has a W1MG_<NAME>
- * environment variable read at context creation): "pdhg_fold" (folded DCTs
- * in PDHG iterations: 1 = odd m >= 400 (default), 2 = every odd m, 0 = off),
- * "pdhg_small" (0-2),
+ * environment variable read at context creation): "pdhg_small" (0-2),
  * "cluster_pick" (0/1), "compact" (0/1), "compact_step" (>= 1),
  * "warps_per_sm" (strip target, default 32), "tmap_nw" (2/4/8, 0 = auto),
  * "tile" (0-2), "tile_min", "tile_max", "tile_grid".

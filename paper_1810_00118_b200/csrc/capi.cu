@@ -11,7 +11,6 @@
 //   cp_residual      proj/src/solver_cp.cpp:102-111
 //   grid operators   proj/src/grid.cpp:45-142
 //   ml_run (spec)
-#include <cublas_v2.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -39,6 +38,7 @@
 #include "tile_kernels.cuh"
 #include "cp3_kernels.cuh"
 #include "tile2_kernels.cuh"
+#include "dct_kernels.cuh"
 
 using namespace w1mg_dev;
 
@@ -74,7 +74,6 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_COMPACT")) g_compact = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_CLUSTER_PICK")) g_cluster_pick = std::atoi(v);
         if (const char* v = std::getenv("W1MG_PDHG_SMALL")) g_pdhg_small = std::atoi(v);
-        if (const char* v = std::getenv("W1MG_PDHG_FOLD")) g_pdhg_fold = std::atoi(v);
         if (const char* v = std::getenv("W1MG_WARPS_PER_SM")) g_warps_per_sm = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_PDL")) g_pdl = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_TILE")) g_tile = std::atoi(v);
@@ -110,7 +109,6 @@ void w1mg_ctx_destroy(w1mg_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->lev_ev) cudaEventDestroy(e);
-    if (c->blas) cublasDestroy(static_cast<cublasHandle_t>(c->blas));
     if (c->t0) cudaEventDestroy(c->t0);
     if (c->t1) cudaEventDestroy(c->t1);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -609,8 +607,7 @@ int w1mg_set_option(const char* name, long value) {
     if (!name) return W1MG_EINVAL;
     const std::string k(name);
     const int v = (int)value;
-    if (k == "pdhg_fold" && v >= 0 && v <= 2) g_pdhg_fold = v;
-    else if (k == "pdhg_small" && v >= 0 && v <= 2) g_pdhg_small = v;
+    if (k == "pdhg_small" && v >= 0 && v <= 2) g_pdhg_small = v;
     else if (k == "cluster_pick" && (v == 0 || v == 1)) g_cluster_pick = v;
     else if (k == "compact") g_compact = v != 0;
     else if (k == "compact_step" && v >= 1) g_compact_step = v;

@@ -1,0 +1,562 @@
+// dct_kernels.cuh -- hand-written fp64 DCT-II / DCT-III for the Neumann
+// Poisson solve of G-prox PDHG (sm_100a), replacing the reference's FFTW
+// REDFT10 / REDFT01 plans (proj/src/poisson.cpp:35-38, 82-98):
+//
+//   REDFT10 (DCT-II):  X_k = 2 sum_i x_i cos(pi k (2i+1) / 2m)
+//   REDFT01 (DCT-III): y_i = X_0 + 2 sum_{k>=1} X_k cos(pi k (2i+1) / 2m)
+//
+// on m = n+1 node rows / columns (odd at every config: 33 ... 4097).
+//
+// Algorithm (per 1-D vector of length m, all in shared memory):
+//   * Makhoul's reordering turns the DCT-II into one length-m DFT of the real
+//     sequence v[n] = x[2n] (n <= (m-1)/2), v[m-1-n] = x[2n+1], followed by
+//     X_k = 2 Re(e^{-i pi k/2m} V_k); the DCT-III runs the same steps
+//     backwards (W_k = e^{i pi k/2m}(X_k - i X_{m-k}), real inverse DFT,
+//     un-reorder).
+//   * The length-m DFT is a prime-factor (Good-Thomas) split m = N1 N2 with
+//     coprime N1 >= N2 (513 = 27 x 19, 257 prime, 129 = 43 x 3, 65 = 13 x 5):
+//     no twiddles between the stages, input map n = (N2 n1 + N1 n2) mod m,
+//     output map by the CRT.
+//   * Each stage is a direct DFT whose symmetric (cos) and antisymmetric (sin)
+//     halves are folded first (x_t +- x_{N-t}), so a stage is two small real
+//     GEMMs  [twiddles] x [folded vectors]; real input halves stage 1 and
+//     Hermitian symmetry halves stage 2.  The GEMMs run from shared memory
+//     with 4 x 4 register tiles (twiddle tables read through L1, broadcast
+//     across a warp).
+//   At m = 513 one vector costs ~16.5k fp64 FMA (the dense folded DCT matrix
+//   costs 132k), at m = 257 (prime) ~33k.
+//
+// Kernels of one Poisson solve / PDHG iteration (the 2-D transform is
+// separable: rows along i, columns along j):
+//   dct_rows_fwd_kernel<MODE>  rows: (MODE 1: r = A v - rho, the PDHG pre
+//                              step, formed on the fly) -> DCT-II along i -> T
+//   dct_cols_kernel            columns of T: DCT-II along j, divide by
+//                              lambda_k1 + lambda_k2 (constant mode -> 0),
+//                              DCT-III along j -> T
+//   dct_rows_inv_kernel<MODE>  rows of T: DCT-III along i, x 1/(4 m^2) = psi;
+//                              MODE 0 stores psi, MODE 1 runs the PDHG post
+//                              step (m, varphi, varphi_bar, Eq. 12 partials,
+//                              stop rule) on the rows with psi from shared
+//                              memory (one extra row transformed for the
+//                              y-difference).
+// A vector's transform depends only on its own data (fixed operation order),
+// so the extra row a CTA recomputes carries the same bits as its owner's.
+#pragma once
+
+#include "pdhg_kernels.cuh"
+
+namespace w1mg_dev {
+
+// H = N/2 + 1 outputs of a real length-N DFT, T = (N-1)/2 symmetric pairs
+// (t, N-t), E = 1 for even N: the Nyquist element N/2 enters once, as an
+// extra row T of the cosine GEMM.
+struct DctPlan {
+    int m, N1, N2, H1, T1, E1, H2, T2, E2, H1p, H2p;
+    const short* idxA;  // [N2][N1] row position of v[(N2 t + N1 n2) mod m]
+    const short* crt;   // [N2][H1] k with k mod N1 = k1 and k mod N2 = k2
+    const double* c1;   // [T1+E1][H1p]  cos(2 pi (t+1) k1 / N1); Nyquist row (-1)^k1
+    const double* s1;   // [T1][H1p]    -sin(2 pi (t+1) k1 / N1)
+    const double* c2;   // [T2+E2][H2p]  cos(2 pi (t+1) k2 / N2); Nyquist row (-1)^k2
+    const double* s2;   // [T2][H2p]     sin(2 pi (t+1) k2 / N2)
+    const double* cT;   // [T1+E1][H1p]  cos(2 pi n1 (k1+1) / N1); Nyquist row (-1)^n1 / 2
+    const double* sT;   // [T1][H1p]     sin(2 pi n1 (k1+1) / N1)
+    const double* mk;   // [2m] cos, sin of pi k / 2m
+};
+
+__host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
+
+// Shared-memory arenas (doubles) for NV vectors: P and Q (ping-pong scratch
+// of the stages), then X (NV x m).
+__host__ __device__ inline void dct_arena(const DctPlan& p, int NV, int& szP, int& szQ) {
+    const int NpA = round4(NV * p.N2);
+    szP = (2 * p.T1 + 1 + p.E1) * NpA;
+    szQ = 2 * p.H1p * NpA;
+    if (p.N2 > 1) {
+        const int W2 = 2 * round4(NV * p.H1);
+        const int b2 = (2 * p.T2 + 1 + p.E2) * W2;
+        szP = szP > b2 ? szP : b2;
+        szQ = szQ > 2 * p.H2p * W2 ? szQ : 2 * p.H2p * W2;
+    }
+    szP = round4(szP);
+    szQ = round4(szQ);
+}
+
+__host__ __device__ inline size_t dct_smem_bytes(const DctPlan& p, int NV) {
+    int a, b;
+    dct_arena(p, NV, a, b);
+    return sizeof(double) * ((size_t)a + b + (size_t)NV * p.m);
+}
+
+// C[i][j] = (C0 ? C0[j] : 0) + sum_k A[k*lda + i] * B[k*ldb + j] for
+// i < 4 Mt, j < 4 Nt.  A: twiddle table in global memory (read-only path);
+// B, C, C0: shared memory, rows 16-B aligned.  One 4 x 4 tile per thread.
+__device__ __forceinline__ void tgemm(const double* __restrict__ A, int lda, int Mt, int K,
+                                      const double* B, int ldb, int Nt, double* C, int ldc,
+                                      const double* C0) {
+    const int tiles = Mt * Nt;
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+        const int ti = t / Nt, tj = t - ti * Nt;
+        double acc[4][4];
+        double2 z01 = make_double2(0.0, 0.0), z23 = z01;
+        if (C0) {
+            z01 = *reinterpret_cast<const double2*>(C0 + 4 * tj);
+            z23 = *reinterpret_cast<const double2*>(C0 + 4 * tj + 2);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            acc[r][0] = z01.x;
+            acc[r][1] = z01.y;
+            acc[r][2] = z23.x;
+            acc[r][3] = z23.y;
+        }
+        const double* a = A + 4 * ti;
+        const double* b = B + 4 * tj;
+#pragma unroll 4
+        for (int k = 0; k < K; ++k) {
+            const double2 a01 = __ldg(reinterpret_cast<const double2*>(a + (long)k * lda));
+            const double2 a23 = __ldg(reinterpret_cast<const double2*>(a + (long)k * lda + 2));
+            const double2 b01 = *reinterpret_cast<const double2*>(b + k * ldb);
+            const double2 b23 = *reinterpret_cast<const double2*>(b + k * ldb + 2);
+            const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+            const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[r][q] = fma(av[r], bv[q], acc[r][q]);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double* cr = C + (4 * ti + r) * ldc + 4 * tj;
+            *reinterpret_cast<double2*>(cr) = make_double2(acc[r][0], acc[r][1]);
+            *reinterpret_cast<double2*>(cr + 2) = make_double2(acc[r][2], acc[r][3]);
+        }
+    }
+}
+
+// Forward DCT-II of NV vectors X[v*m + i] in place (P, Q scratch).
+__device__ void dct2_vectors(const DctPlan& p, int NV, double* X, double* P, double* Q) {
+    const int m = p.m, N1 = p.N1, N2 = p.N2, H1 = p.H1, T1 = p.T1, E1 = p.E1;
+    const int NA = NV * N2, NpA = round4(NA);
+    // stage 1 fold: X0 = x_0, S_t = x_t + x_{N1-t}, D_t = x_t - x_{N1-t}
+    // (S row T1 = x_{N1/2} for even N1)
+    double* SA = P;
+    double* DA = P + (T1 + E1) * NpA;
+    double* X0 = DA + T1 * NpA;
+    for (int e = threadIdx.x; e < (T1 + 1 + E1) * NpA; e += blockDim.x) {
+        const int t = e / NpA, j = e - t * NpA;
+        double s = 0.0, d = 0.0;
+        if (j < NA) {
+            const int n2 = j / NV, v = j - n2 * NV;
+            const short* ix = p.idxA + n2 * N1;
+            const double* xv = X + v * m;
+            if (t == 0 || t > T1) {
+                s = xv[ix[t]];
+            } else {
+                const double x0 = xv[ix[t]], x1 = xv[ix[N1 - t]];
+                s = x0 + x1;
+                d = x0 - x1;
+            }
+        }
+        if (t == 0) {
+            X0[j] = s;
+        } else {
+            SA[(t - 1) * NpA + j] = s;
+            if (t <= T1) DA[(t - 1) * NpA + j] = d;
+        }
+    }
+    __syncthreads();
+    // stage 1: A[k1][j] = X0 + sum cos S - i sum sin D, k1 < H1
+    double* ReA = Q;
+    double* ImA = Q + p.H1p * NpA;
+    tgemm(p.c1, p.H1p, p.H1p / 4, T1 + E1, SA, NpA, NpA / 4, ReA, NpA, X0);
+    tgemm(p.s1, p.H1p, p.H1p / 4, T1, DA, NpA, NpA / 4, ImA, NpA, nullptr);
+    __syncthreads();
+    const int NB = NV * H1, NpB = round4(NB), W2 = 2 * NpB, H2 = p.H2;
+    double* Cp = Q;
+    double* Sn = Q + p.H2p * W2;
+    if (N2 > 1) {
+        // stage 2 fold over n2 of the complex A[k1][n2 NV + v]; vector jb = k1 NV + v,
+        // real parts in columns [0, NpB), imaginary parts in [NpB, 2 NpB)
+        const int T2 = p.T2, E2 = p.E2;
+        double* SB = P;
+        double* DB = P + (T2 + E2) * W2;
+        double* A0 = DB + T2 * W2;
+        for (int e = threadIdx.x; e < (T2 + 1 + E2) * NpB; e += blockDim.x) {
+            const int t = e / NpB, jb = e - t * NpB;
+            double sr = 0.0, si = 0.0, dr = 0.0, di = 0.0;
+            if (jb < NB) {
+                const int k1 = jb / NV, v = jb - k1 * NV;
+                const double* re = ReA + k1 * NpA;
+                const double* im = ImA + k1 * NpA;
+                if (t == 0 || t > T2) {
+                    sr = re[t * NV + v];
+                    si = im[t * NV + v];
+                } else {
+                    const int ja = t * NV + v, jc = (N2 - t) * NV + v;
+                    sr = re[ja] + re[jc];
+                    si = im[ja] + im[jc];
+                    dr = re[ja] - re[jc];
+                    di = im[ja] - im[jc];
+                }
+            }
+            if (t == 0) {
+                A0[jb] = sr;
+                A0[NpB + jb] = si;
+            } else {
+                double* s = SB + (t - 1) * W2;
+                s[jb] = sr;
+                s[NpB + jb] = si;
+                if (t <= T2) {
+                    double* d = DB + (t - 1) * W2;
+                    d[jb] = dr;
+                    d[NpB + jb] = di;
+                }
+            }
+        }
+        __syncthreads();
+        tgemm(p.c2, p.H2p, p.H2p / 4, T2 + E2, SB, W2, W2 / 4, Cp, W2, A0);
+        tgemm(p.s2, p.H2p, p.H2p / 4, T2, DB, W2, W2 / 4, Sn, W2, nullptr);
+        __syncthreads();
+    }
+    // V[k1, k2] = Cp - i Sn (k2 < H2), V[k1, N2 - k2] = Cp + i Sn; V[m-k] = conj V[k];
+    // X_k = 2 (cos(pi k/2m) Re V_k + sin(pi k/2m) Im V_k)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int v = warp; v < NV; v += nw) {
+        for (int k = lane; k < m; k += 32) {
+            int kk = k;
+            int k1 = kk % N1;
+            const bool cj = k1 >= H1;
+            if (cj) {
+                kk = m - k;
+                k1 = kk % N1;
+            }
+            double vr, vi;
+            if (N2 == 1) {
+                vr = ReA[k1 * NpA + v];
+                vi = ImA[k1 * NpA + v];
+            } else {
+                const int k2 = kk % N2, jb = k1 * NV + v;
+                if (k2 < H2) {
+                    const double* cp = Cp + k2 * W2;
+                    const double* sn = Sn + k2 * W2;
+                    vr = cp[jb] + sn[NpB + jb];
+                    vi = cp[NpB + jb] - sn[jb];
+                } else {
+                    const double* cp = Cp + (N2 - k2) * W2;
+                    const double* sn = Sn + (N2 - k2) * W2;
+                    vr = cp[jb] - sn[NpB + jb];
+                    vi = cp[NpB + jb] + sn[jb];
+                }
+            }
+            if (cj) vi = -vi;
+            const double c = p.mk[2 * k], s = p.mk[2 * k + 1];
+            X[v * m + k] = 2.0 * (c * vr + s * vi);
+        }
+    }
+    __syncthreads();
+}
+
+// W_k = e^{i pi k/2m} (X_k - i X_{m-k}), X_m = 0
+__device__ __forceinline__ void dct3_w(const DctPlan& p, const double* x, int k, double& wr,
+                                       double& wi) {
+    const double a = x[k], b = k ? x[p.m - k] : 0.0;
+    const double c = p.mk[2 * k], s = p.mk[2 * k + 1];
+    wr = c * a + s * b;
+    wi = s * a - c * b;
+}
+
+// DCT-III of NV vectors X[v*m + k] in place (P, Q scratch).
+__device__ void dct3_vectors(const DctPlan& p, int NV, double* X, double* P, double* Q) {
+    const int m = p.m, N1 = p.N1, N2 = p.N2, H1 = p.H1, T1 = p.T1, E1 = p.E1;
+    const int NA = NV * N2, NpA = round4(NA);
+    // stage 1 inputs: BR / BI rows k1 = 1..T1 (BR row T1: Nyquist k1 = N1/2), B0 = Re b[0]
+    double* BR = P;
+    double* BI = P + (T1 + E1) * NpA;
+    double* B0 = BI + T1 * NpA;
+    if (N2 == 1) {
+        for (int e = threadIdx.x; e < H1 * NpA; e += blockDim.x) {
+            const int t = e / NpA, j = e - t * NpA;
+            double wr = 0.0, wi = 0.0;
+            if (j < NV) dct3_w(p, X + j * m, t, wr, wi);
+            if (t == 0) {
+                B0[j] = wr;
+            } else {
+                BR[(t - 1) * NpA + j] = wr;
+                if (t <= T1) BI[(t - 1) * NpA + j] = wi;
+            }
+        }
+        __syncthreads();
+    } else {
+        // stage 2 (inverse, over k2): fold W[k1, t] +- W[k1, N2-t] for k1 < H1
+        const int T2 = p.T2, E2 = p.E2, NB = NV * H1, NpB = round4(NB), W2 = 2 * NpB, H2 = p.H2;
+        double* SB = P;
+        double* DB = P + (T2 + E2) * W2;
+        double* A0 = DB + T2 * W2;
+        for (int e = threadIdx.x; e < (T2 + 1 + E2) * NpB; e += blockDim.x) {
+            const int t = e / NpB, jb = e - t * NpB;
+            double sr = 0.0, si = 0.0, dr = 0.0, di = 0.0;
+            if (jb < NB) {
+                const int k1 = jb / NV, v = jb - k1 * NV;
+                const double* x = X + v * m;
+                if (t == 0 || t > T2) {
+                    dct3_w(p, x, p.crt[t * H1 + k1], sr, si);
+                } else {
+                    double ar, ai, br, bi;
+                    dct3_w(p, x, p.crt[t * H1 + k1], ar, ai);
+                    dct3_w(p, x, p.crt[(N2 - t) * H1 + k1], br, bi);
+                    sr = ar + br;
+                    si = ai + bi;
+                    dr = ar - br;
+                    di = ai - bi;
+                }
+            }
+            if (t == 0) {
+                A0[jb] = sr;
+                A0[NpB + jb] = si;
+            } else {
+                double* s = SB + (t - 1) * W2;
+                s[jb] = sr;
+                s[NpB + jb] = si;
+                if (t <= T2) {
+                    double* d = DB + (t - 1) * W2;
+                    d[jb] = dr;
+                    d[NpB + jb] = di;
+                }
+            }
+        }
+        __syncthreads();
+        double* Cp = Q;
+        double* Sn = Q + p.H2p * W2;
+        tgemm(p.c2, p.H2p, p.H2p / 4, T2 + E2, SB, W2, W2 / 4, Cp, W2, A0);
+        tgemm(p.s2, p.H2p, p.H2p / 4, T2, DB, W2, W2 / 4, Sn, W2, nullptr);
+        __syncthreads();
+        // b[k1][n2] = Cp + i Sn (n2 < H2), b[k1][N2 - n2] = Cp - i Sn -> stage 1 inputs
+        // (vector j = n2 NV + v): BR / BI rows k1 = 1..H1-1, B0 = Re b[0]
+        for (int e = threadIdx.x; e < H1 * NpA; e += blockDim.x) {
+            const int t = e / NpA, j = e - t * NpA;
+            double br = 0.0, bi = 0.0;
+            if (j < NA) {
+                const int n2 = j / NV, v = j - n2 * NV, jb = t * NV + v;
+                if (n2 < H2) {
+                    const double* cp = Cp + n2 * W2;
+                    const double* sn = Sn + n2 * W2;
+                    br = cp[jb] - sn[NpB + jb];
+                    bi = cp[NpB + jb] + sn[jb];
+                } else {
+                    const double* cp = Cp + (N2 - n2) * W2;
+                    const double* sn = Sn + (N2 - n2) * W2;
+                    br = cp[jb] + sn[NpB + jb];
+                    bi = cp[NpB + jb] - sn[jb];
+                }
+            }
+            if (t == 0) {
+                B0[j] = br;
+            } else {
+                BR[(t - 1) * NpA + j] = br;
+                if (t <= T1) BI[(t - 1) * NpA + j] = bi;
+            }
+        }
+        __syncthreads();
+    }
+    // stage 1 (inverse, over k1): w[n1] = b0 + 2 (P - Q), w[N1 - n1] = b0 + 2 (P + Q)
+    double* PP = Q;
+    double* QQ = Q + p.H1p * NpA;
+    tgemm(p.cT, p.H1p, p.H1p / 4, T1 + E1, BR, NpA, NpA / 4, PP, NpA, nullptr);
+    tgemm(p.sT, p.H1p, p.H1p / 4, T1, BI, NpA, NpA / 4, QQ, NpA, nullptr);
+    __syncthreads();
+    // un-reorder: n = (N2 n1 + N1 n2) mod m -> y[2n] / y[2(m-1-n)+1]
+    for (int e = threadIdx.x; e < NA * N1; e += blockDim.x) {
+        const int r = e / NV, v = e - r * NV;
+        const int n2 = r / N1, n1 = r - n2 * N1;
+        const int j = n2 * NV + v;
+        double w;
+        if (n1 < H1) w = B0[j] + 2.0 * (PP[n1 * NpA + j] - QQ[n1 * NpA + j]);
+        else w = B0[j] + 2.0 * (PP[(N1 - n1) * NpA + j] + QQ[(N1 - n1) * NpA + j]);
+        const int n = (N2 * n1 + N1 * n2) % m;
+        const int pos = (n <= (m - 1) / 2) ? 2 * n : 2 * (m - 1 - n) + 1;
+        X[v * m + pos] = w;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void dct_smem(const DctPlan& p, int NV, double*& P, double*& Q,
+                                         double*& X) {
+    extern __shared__ __align__(16) double dct_sm[];
+    int a, b;
+    dct_arena(p, NV, a, b);
+    P = dct_sm;
+    Q = dct_sm + a;
+    X = Q + b;
+}
+
+// r = A v - rho with v = m - mu varphi_bar (pdhg_pre_kernel's expression)
+__device__ __forceinline__ double pdhg_rhs(const SweepArgs& a, int b, int i, int j) {
+    const Layout L = a.L;
+    const int n = L.n;
+    const double* mx = pslot(a, b, P_MX);
+    const double* my = pslot(a, b, P_MY);
+    const double* bx = pslot(a, b, P_BX);
+    const double* by = pslot(a, b, P_BY);
+    const double mu = a.mu, ih = a.ih;
+    const long o = L.at(i, j);
+    const double r_ = (i < n) ? mx[o] - mu * bx[o] : 0.0;
+    const double l_ = (i > 0) ? mx[o - 1] - mu * bx[o - 1] : 0.0;
+    const double a_ = (j < n) ? my[o] - mu * by[o] : 0.0;
+    const double b_ = (j > 0) ? my[o - L.pitch] - mu * by[o - L.pitch] : 0.0;
+    const double div = (r_ - l_) * ih + (a_ - b_) * ih;
+    return div - pslot(a, b, P_RHO)[o];
+}
+
+// Rows j0 .. j0+R-1: (MODE 0) slot `in` or (MODE 1) the PDHG right-hand side
+// -> DCT-II along i -> slot P_T.
+template <int MODE>
+__global__ void __launch_bounds__(256) dct_rows_fwd_kernel(const SweepArgs a, const DctPlan p, int in,
+                                                           int R, int check_done) {
+    const int b = blockIdx.y;
+    if (check_done && *(volatile int*)&a.ctl[b].done) return;
+    double *P, *Q, *X;
+    dct_smem(p, R, P, Q, X);
+    const int m = p.m, j0 = blockIdx.x * R;
+    const Layout L = a.L;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const double* src = pslot(a, b, in);
+    for (int v = warp; v < R; v += nw) {
+        const int j = j0 + v;
+        for (int i = lane; i < m; i += 32) {
+            double x = 0.0;
+            if (j < m) x = MODE ? pdhg_rhs(a, b, i, j) : src[L.at(i, j)];
+            X[v * m + i] = x;
+        }
+    }
+    __syncthreads();
+    dct2_vectors(p, R, X, P, Q);
+    double* T = pslot_w(a, b, P_T);
+    for (int v = warp; v < R; v += nw) {
+        const int j = j0 + v;
+        if (j >= m) break;
+        for (int i = lane; i < m; i += 32) T[L.at(i, j)] = X[v * m + i];
+    }
+}
+
+// Columns k1 = c0 .. c0+Wc-1 of P_T: DCT-II along j, spectral divide
+// (poisson.cpp:84-89), DCT-III along j, back to P_T.
+__global__ void __launch_bounds__(256) dct_cols_kernel(const SweepArgs a, const DctPlan p,
+                                                       const double* __restrict__ lambda, int Wc,
+                                                       int check_done) {
+    const int b = blockIdx.y;
+    if (check_done && *(volatile int*)&a.ctl[b].done) return;
+    double *P, *Q, *X;
+    dct_smem(p, Wc, P, Q, X);
+    const int m = p.m, c0 = blockIdx.x * Wc;
+    const Layout L = a.L;
+    double* T = pslot_w(a, b, P_T);
+    for (int e = threadIdx.x; e < Wc * m; e += blockDim.x) {
+        const int j = e / Wc, v = e - j * Wc;
+        X[v * m + j] = (c0 + v < m) ? T[L.at(c0 + v, j)] : 0.0;
+    }
+    __syncthreads();
+    dct2_vectors(p, Wc, X, P, Q);
+    for (int e = threadIdx.x; e < Wc * m; e += blockDim.x) {
+        const int v = e / m, k2 = e - v * m, k1 = c0 + v;
+        if (k1 < m) {
+            double& y = X[v * m + k2];
+            y = (k1 == 0 && k2 == 0) ? 0.0 : y / (lambda[k1] + lambda[k2]);
+        }
+    }
+    __syncthreads();
+    dct3_vectors(p, Wc, X, P, Q);
+    for (int e = threadIdx.x; e < Wc * m; e += blockDim.x) {
+        const int j = e / Wc, v = e - j * Wc;
+        if (c0 + v < m) T[L.at(c0 + v, j)] = X[v * m + j];
+    }
+}
+
+// Rows j0 .. j0+R-1 of P_T: DCT-III along i, psi = y / (4 m^2) (poisson.cpp:93).
+// MODE 0: psi -> P_PSI.  MODE 1 (Q = conjugate norm): the PDHG post step on
+// these rows (pdhg_post_kernel's arithmetic) with psi from shared memory.
+template <int MODE, int QN>
+__global__ void __launch_bounds__(256) dct_rows_inv_kernel(const SweepArgs a, const DctPlan p, int R,
+                                                           double scale, int check_done) {
+    const int b = blockIdx.y;
+    if (check_done && *(volatile int*)&a.ctl[b].done) return;
+    const int NV = MODE ? R + 1 : R;
+    double *P, *Q, *X;
+    dct_smem(p, NV, P, Q, X);
+    const int m = p.m, j0 = blockIdx.x * R;
+    const Layout L = a.L;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const double* T = pslot(a, b, P_T);
+    for (int v = warp; v < NV; v += nw) {
+        const int j = j0 + v;
+        for (int i = lane; i < m; i += 32) X[v * m + i] = (j < m) ? T[L.at(i, j)] : 0.0;
+    }
+    __syncthreads();
+    dct3_vectors(p, NV, X, P, Q);
+    if (MODE == 0) {
+        double* psi = pslot_w(a, b, P_PSI);
+        for (int v = warp; v < R; v += nw) {
+            const int j = j0 + v;
+            if (j >= m) break;
+            for (int i = lane; i < m; i += 32) psi[L.at(i, j)] = scale * X[v * m + i];
+        }
+        return;
+    }
+    const int n = L.n;
+    const double mu = a.mu, tau = a.tau, ih = a.ih;
+    double* mx = pslot_w(a, b, P_MX);
+    double* my = pslot_w(a, b, P_MY);
+    double* px = pslot_w(a, b, P_PX);
+    double* py = pslot_w(a, b, P_PY);
+    double* bx = pslot_w(a, b, P_BX);
+    double* by = pslot_w(a, b, P_BY);
+    double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
+    for (int v = warp; v < R; v += nw) {
+        const int j = j0 + v;
+        if (j > n) break;
+        for (int i = lane; i <= n; i += 32) {
+            const long o = L.at(i, j);
+            const bool hx = i < n, hy = j < n;
+            const double pc = scale * X[v * m + i];
+            double mnx = 0.0, mny = 0.0, dmx = 0.0, dmy = 0.0, pox = 0.0, poy = 0.0;
+            if (hx) {
+                const double mo = mx[o];
+                const double vv = mo - mu * bx[o];
+                mnx = vv - (pc - scale * X[v * m + i + 1]) * ih;  // poisson.cpp:124
+                dmx = mnx - mo;
+                pox = px[o];
+            }
+            if (hy) {
+                const double mo = my[o];
+                const double vv = mo - mu * by[o];
+                mny = vv - (pc - scale * X[(v + 1) * m + i]) * ih;  // poisson.cpp:130
+                dmy = mny - mo;
+                poy = py[o];
+            }
+            const double wx = hx ? pox + tau * mnx : 0.0;
+            const double wy = hy ? poy + tau * mny : 0.0;
+            double qx, qy;
+            proj_unit_ball<QN>(wx, wy, qx, qy);
+            if (hx) {
+                mx[o] = mnx;
+                px[o] = qx;
+                bx[o] = 2.0 * qx - pox;
+                const double dp = qx - pox;
+                s_dm2 += dmx * dmx;
+                s_dp2 += dp * dp;
+                s_cr += dp * dmx;
+            }
+            if (hy) {
+                my[o] = mny;
+                py[o] = qy;
+                by[o] = 2.0 * qy - poy;
+                const double dp = qy - poy;
+                s_dm2 += dmy * dmy;
+                s_dp2 += dp * dp;
+                s_cr += dp * dmy;
+            }
+        }
+    }
+    finish_sweep<true>(a, b, /*parity=*/1, blockIdx.x, gridDim.x, s_dm2, s_dp2, s_cr);
+}
+
+}  // namespace w1mg_dev

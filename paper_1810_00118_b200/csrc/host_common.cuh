@@ -65,7 +65,7 @@ struct w1mg_ctx {
     int lev_count = 0;
     long launches = 0;
     int num_sms = 148;
-    void* blas = nullptr;  // cublasHandle_t for the Poisson DCT GEMMs (lazy)
+    std::map<int, w1mg_dev::DctPlan> dct;  // Poisson DCT plans per m (dct_kernels.cuh)
 
     void* buf(const std::string& name, size_t bytes) {
         Buf& b = bufs[name];

@@ -532,9 +532,6 @@ bool resident_ok(const Level& lv) {
 // the cluster engine wherever it fits (tests).
 // PDHG levels with m = n+1 <= 65 run level-resident (pdhg_engine.cuh)
 int g_pdhg_small = 1;
-// PDHG iterations with symmetry-folded DCTs (pdhg_fold.cuh): 1 = auto (odd
-// m >= kFoldMinM), 2 = every odd m, 0 = dense sandwich only
-int g_pdhg_fold = 1;
 
 // cluster-size rule (W1MG_CLUSTER_PICK): 1 = fewest node passes per phase
 // (default), 0 = powers of two with >= 8 rows per CTA

@@ -11,30 +11,11 @@
 
 #include "pdhg_kernels.cuh"
 #include "pdhg_small.cuh"
-#include "pdhg_fold.cuh"
+#include "dct_kernels.cuh"
 
 namespace {
 
-void blas_check(cublasStatus_t s, const char* what) {
-    if (s != CUBLAS_STATUS_SUCCESS) fail(W1MG_ECUDA, std::string("cuBLAS ") + what + " failed");
-}
-
-cublasHandle_t blas(w1mg_ctx* c) {
-    if (!c->blas) {
-        cublasHandle_t h;
-        blas_check(cublasCreate(&h), "create");
-        // a fixed workspace keeps DGEMM capturable in CUDA graphs
-        void* ws = c->buf("blas.workspace", 8u << 20);
-        blas_check(cublasSetWorkspace(h, ws, 8u << 20), "workspace");
-        blas_check(cublasSetMathMode(h, CUBLAS_DEFAULT_MATH), "math mode");
-        c->blas = h;
-    }
-    cublasHandle_t h = static_cast<cublasHandle_t>(c->blas);
-    blas_check(cublasSetStream(h, c->stream), "stream");
-    return h;
-}
-
-// One PDHG level batch (B pairs, P_NSLOT planes each) + DCT operators.
+// One PDHG level batch (B pairs, P_NSLOT planes each) + its DCT plan.
 struct PLevel {
     int n = 0, B = 0;
     Layout L{};
@@ -44,64 +25,25 @@ struct PLevel {
     int* ndone = nullptr;
     SweepArgs args{};
     dim3 grid, blk;
-    const double* C = nullptr;    // DCT-II matrix, m x m column-major: C(k, j) = 2 cos(pi (2j+1) k / 2m)
-    const double* S = nullptr;    // DCT-III matrix: S(k, j) = j ? 2 cos(pi j (2k+1) / 2m) : 1
+    const double* C = nullptr;    // dense DCT-II matrix (level-resident small kernel only)
+    const double* S = nullptr;    // dense DCT-III matrix (level-resident small kernel only)
     const double* lam = nullptr;  // lambda_k, poisson.cpp:28-30
-    // symmetry-folded DCTs for the PDHG iteration (pdhg_fold.cuh), odd m >= kFoldMinM
-    bool fold = false;
-    FoldGeom fg{};
-    const double* const* gp = nullptr;  // device pointer arrays [4 stages][A,B,C][4B]
+    DctPlan dp{};                 // prime-factor DCT plan (dct_kernels.cuh)
+    int rows_f = 1, cols = 1, rows_i = 1;  // vectors per CTA of the three DCT launches
 };
 
-// folded DCT in the PDHG iteration from this m on (W1MG_PDHG_FOLD=0 disables).
-// Measured per level of config 3 (one pair): 513^2 176 vs 202 ms (folded vs
-// dense), 257^2 143 vs 128 ms, 129^2 157 vs 130 ms -- the batched half-size
-// GEMMs only win once the dense ones are large.
-constexpr int kFoldMinM = 400;
-
-// Folded DCT operators (h x h, ld h, zero padded): C_e, C_o, S_e, S_o.
-const double* fold_operators(w1mg_ctx* c, int n) {
-    const int m = n + 1, h = (m + 1) / 2, ho = h - 1;
-    const std::string key = "dctf." + std::to_string(m);
-    const bool fresh = c->bufs.find(key) == c->bufs.end();
-    double* d = c->get<double>(key, (size_t)4 * h * h);
-    if (fresh) {
-        std::vector<double> M((size_t)4 * h * h, 0.0);
-        const long double pi = 3.141592653589793238462643383279502884L;
-        auto Cf = [&](long k, long l) {  // C(k, l) = 2 cos(pi (2l+1) k / 2m)
-            return (double)(2.0L * cosl(pi * (((2 * l + 1) * k) % (4L * m)) / (2.0L * m)));
-        };
-        auto Sf = [&](long k, long j) {  // S(k, j) = j ? 2 cos(pi j (2k+1) / 2m) : 1
-            return j == 0 ? 1.0 : (double)(2.0L * cosl(pi * ((j * (2 * k + 1)) % (4L * m)) / (2.0L * m)));
-        };
-        double* Ce = M.data();
-        double* Co = Ce + (size_t)h * h;
-        double* Se = Co + (size_t)h * h;
-        double* So = Se + (size_t)h * h;
-        for (int col = 0; col < h; ++col)
-            for (int row = 0; row < h; ++row) {
-                const size_t e = (size_t)col * h + row;
-                Ce[e] = Cf(2L * row, col);
-                if (row < ho && col < ho) Co[e] = Cf(2L * row + 1, col);
-                Se[e] = Sf(row, 2L * col);
-                if (row < ho && col < ho) So[e] = Sf(row, 2L * col + 1);
-            }
-        CK(cudaMemcpy(d, M.data(), M.size() * 8, cudaMemcpyHostToDevice));
-    }
-    return d;
-}
-
-// DCT operators for m = n+1, built once per size on the host in long double
-// and cached on the device.
-void dct_operators(w1mg_ctx* c, int n, const double** C, const double** S, const double** lam) {
+// Dense DCT matrices for m = n+1, built once per size on the host in long
+// double and cached on the device -- only for the level-resident small
+// kernel (pdhg_small.cuh, m <= kPdhgSmallMaxM), which multiplies them in
+// shared memory.
+void dct_operators(w1mg_ctx* c, int n, const double** C, const double** S) {
     const int m = n + 1;
     const std::string key = std::to_string(m);
     const bool fresh = c->bufs.find("dct.C." + key) == c->bufs.end();
     double* dC = c->get<double>("dct.C." + key, (size_t)m * m);
     double* dS = c->get<double>("dct.S." + key, (size_t)m * m);
-    double* dl = c->get<double>("dct.lam." + key, m);
     if (fresh) {
-        std::vector<double> hC((size_t)m * m), hS((size_t)m * m), hl(m);
+        std::vector<double> hC((size_t)m * m), hS((size_t)m * m);
         const long double pi = 3.141592653589793238462643383279502884L;
         for (int j = 0; j < m; ++j)
             for (int k = 0; k < m; ++k) {
@@ -110,16 +52,171 @@ void dct_operators(w1mg_ctx* c, int n, const double** C, const double** S, const
                 hC[(size_t)j * m + k] = (double)(2.0L * cosl(pi * a / (2.0L * m)));
                 hS[(size_t)j * m + k] = j == 0 ? 1.0 : (double)(2.0L * cosl(pi * b / (2.0L * m)));
             }
-        const double h = 1.0 / n;
-        const double inv_h2 = 1.0 / (h * h);
-        for (int k = 0; k < m; ++k) hl[k] = (2.0 - 2.0 * std::cos(M_PI * k / m)) * inv_h2;
         CK(cudaMemcpy(dC, hC.data(), hC.size() * 8, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(dS, hS.data(), hS.size() * 8, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(dl, hl.data(), hl.size() * 8, cudaMemcpyHostToDevice));
     }
     *C = dC;
     *S = dS;
-    *lam = dl;
+}
+
+// lambda_k = (2 - 2 cos(pi k / m)) / h^2 exactly as poisson.cpp:28-30
+const double* dct_lambda(w1mg_ctx* c, int n) {
+    const int m = n + 1;
+    const std::string key = "dct.lam." + std::to_string(m);
+    const bool fresh = c->bufs.find(key) == c->bufs.end();
+    double* dl = c->get<double>(key, m);
+    if (fresh) {
+        std::vector<double> hl(m);
+        const double h = 1.0 / n;
+        const double inv_h2 = 1.0 / (h * h);
+        for (int k = 0; k < m; ++k) hl[k] = (2.0 - 2.0 * std::cos(M_PI * k / m)) * inv_h2;
+        CK(cudaMemcpy(dl, hl.data(), hl.size() * 8, cudaMemcpyHostToDevice));
+    }
+    return dl;
+}
+
+// Prime-factor split m = N1 N2: coprime, N1 >= N2, N1 + N2 minimal (prime
+// powers kept whole; a prime m gives N2 = 1).
+void dct_split(int m, int& N1, int& N2) {
+    std::vector<int> pp;
+    int x = m;
+    for (int q = 2; (long)q * q <= x; ++q)
+        if (x % q == 0) {
+            int pw = 1;
+            while (x % q == 0) {
+                x /= q;
+                pw *= q;
+            }
+            pp.push_back(pw);
+        }
+    if (x > 1) pp.push_back(x);
+    N1 = m;
+    N2 = 1;
+    const int np = (int)pp.size();
+    for (int mask = 0; mask < (1 << np); ++mask) {
+        int a = 1;
+        for (int t = 0; t < np; ++t)
+            if (mask >> t & 1) a *= pp[t];
+        const int b = m / a;
+        if (a >= b && a + b < N1 + N2) {
+            N1 = a;
+            N2 = b;
+        }
+    }
+}
+
+// DCT plan for m: index maps and twiddle tables (host long double, exact
+// angle reduction), cached on the device per context.
+DctPlan dct_plan(w1mg_ctx* c, int m) {
+    auto it = c->dct.find(m);
+    if (it != c->dct.end()) return it->second;
+    if (m > 32767) fail(W1MG_EINVAL, "Poisson solve: grid too large for the DCT plan");
+    DctPlan p{};
+    p.m = m;
+    dct_split(m, p.N1, p.N2);
+    const int N1 = p.N1, N2 = p.N2;
+    p.H1 = N1 / 2 + 1;
+    p.T1 = (N1 - 1) / 2;
+    p.E1 = 1 - (N1 & 1);
+    p.H2 = N2 / 2 + 1;
+    p.T2 = (N2 - 1) / 2;
+    p.E2 = 1 - (N2 & 1);
+    p.H1p = round4(p.H1);
+    p.H2p = round4(p.H2);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    auto cosN = [&](long a, long N) { return (double)cosl(2.0L * pi * (long double)(a % N) / N); };
+    auto sinN = [&](long a, long N) { return (double)sinl(2.0L * pi * (long double)(a % N) / N); };
+    auto pos = [&](int n) { return n <= (m - 1) / 2 ? 2 * n : 2 * (m - 1 - n) + 1; };
+    std::vector<short> idxA((size_t)N2 * N1), crt((size_t)N2 * p.H1);
+    for (int n2 = 0; n2 < N2; ++n2)
+        for (int t = 0; t < N1; ++t) idxA[(size_t)n2 * N1 + t] = (short)pos((int)(((long)N2 * t + (long)N1 * n2) % m));
+    for (int k = 0; k < m; ++k)
+        if (k % N1 < p.H1) crt[(size_t)(k % N2) * p.H1 + k % N1] = (short)k;
+    const int r1 = p.T1 + p.E1, r2 = p.T2 + p.E2;
+    std::vector<double> c1((size_t)std::max(r1, 1) * p.H1p, 0.0), s1((size_t)std::max(p.T1, 1) * p.H1p, 0.0);
+    std::vector<double> cT(c1.size(), 0.0), sT(s1.size(), 0.0);
+    std::vector<double> c2((size_t)std::max(r2, 1) * p.H2p, 0.0), s2((size_t)std::max(p.T2, 1) * p.H2p, 0.0);
+    for (int t = 0; t < r1; ++t)
+        for (int k = 0; k < p.H1; ++k) {
+            const size_t e = (size_t)t * p.H1p + k;
+            if (t < p.T1) {
+                c1[e] = cosN((long)(t + 1) * k, N1);
+                s1[e] = -sinN((long)(t + 1) * k, N1);
+                cT[e] = cosN((long)(t + 1) * k, N1);
+                sT[e] = sinN((long)(t + 1) * k, N1);
+            } else {  // Nyquist row (even N1)
+                c1[e] = (k & 1) ? -1.0 : 1.0;
+                cT[e] = (k & 1) ? -0.5 : 0.5;
+            }
+        }
+    for (int t = 0; t < r2; ++t)
+        for (int k = 0; k < p.H2; ++k) {
+            const size_t e = (size_t)t * p.H2p + k;
+            if (t < p.T2) {
+                c2[e] = cosN((long)(t + 1) * k, N2);
+                s2[e] = sinN((long)(t + 1) * k, N2);
+            } else {
+                c2[e] = (k & 1) ? -1.0 : 1.0;
+            }
+        }
+    std::vector<double> mk(2 * (size_t)m);
+    for (int k = 0; k < m; ++k) {  // pi k / 2m = 2 pi k / 4m
+        mk[2 * k] = cosN(k, 4L * m);
+        mk[2 * k + 1] = sinN(k, 4L * m);
+    }
+    const std::string key = "dctp." + std::to_string(m) + ".";
+    auto up_d = [&](const char* name, const std::vector<double>& v) {
+        double* d = c->get<double>(key + name, v.size());
+        CK(cudaMemcpy(d, v.data(), v.size() * 8, cudaMemcpyHostToDevice));
+        return (const double*)d;
+    };
+    auto up_s = [&](const char* name, const std::vector<short>& v) {
+        short* d = c->get<short>(key + name, v.size());
+        CK(cudaMemcpy(d, v.data(), v.size() * sizeof(short), cudaMemcpyHostToDevice));
+        return (const short*)d;
+    };
+    p.idxA = up_s("idxA", idxA);
+    p.crt = up_s("crt", crt);
+    p.c1 = up_d("c1", c1);
+    p.s1 = up_d("s1", s1);
+    p.c2 = up_d("c2", c2);
+    p.s2 = up_d("s2", s2);
+    p.cT = up_d("cT", cT);
+    p.sT = up_d("sT", sT);
+    p.mk = up_d("mk", mk);
+    c->dct[m] = p;
+    return p;
+}
+
+constexpr size_t kDctSmemMax = 200u << 10;
+
+void dct_kernel_attrs() {
+    static unsigned long long done = 0;  // per device
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (done >> (dev & 63) & 1ull) return;
+    const int mx = (int)kDctSmemMax;
+    CK(cudaFuncSetAttribute(dct_rows_fwd_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(dct_rows_fwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(dct_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(dct_rows_inv_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(dct_rows_inv_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(dct_rows_inv_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(dct_rows_inv_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    done |= 1ull << (dev & 63);
+}
+
+// Vectors per CTA of a DCT launch: the most (<= 16) that still give about two
+// CTAs per SM over the batch and fit the shared-memory budget (`extra`
+// vectors are transformed on top, e.g. the post step's halo row).
+int dct_vectors_per_cta(const DctPlan& p, int B, int num_sms, int extra) {
+    int R = 16;
+    while (R > 1 && ((long)((p.m + R - 1) / R) * B < 2L * num_sms ||
+                     dct_smem_bytes(p, R + extra) > kDctSmemMax))
+        R >>= 1;
+    if (dct_smem_bytes(p, R + extra) > kDctSmemMax)
+        fail(W1MG_EINVAL, "Poisson solve: grid too large for the shared-memory DCT");
+    return R;
 }
 
 PLevel make_plevel(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, double tau,
@@ -148,37 +245,13 @@ PLevel make_plevel(w1mg_ctx* c, const std::string& tag, int n, int B, double mu,
     a.hist_cap = hist_cap;
     a.ndone = lv.ndone;
     a.partial = c->get<double>(tag + ".partial", (size_t)B * lv.grid.x * lv.grid.y * 3);
-    dct_operators(c, n, &lv.C, &lv.S, &lv.lam);
-    const int m = n + 1;
-    if ((m & 1) && m >= 3 && (g_pdhg_fold == 2 || (g_pdhg_fold == 1 && m >= kFoldMinM))) {
-        lv.fold = true;
-        lv.fg.h = (m + 1) / 2;
-        lv.fg.lq = lv.L.pitch / 2;
-        const int h = lv.fg.h;
-        const double* ops = fold_operators(c, n);
-        const double* Cm[2] = {ops, ops + (size_t)h * h};
-        const double* Sm[2] = {ops + 2 * (size_t)h * h, ops + 3 * (size_t)h * h};
-        // stage s, array t (A, B, C), entry e = 4 b + q
-        std::vector<const double*> P((size_t)12 * 4 * B);
-        auto at = [&](int st, int t, int e) -> const double*& { return P[((size_t)st * 3 + t) * 4 * B + e]; };
-        for (int b = 0; b < B; ++b)
-            for (int q = 0; q < 4; ++q) {
-                const int e = 4 * b + q, qa = q >> 1, qb = q & 1;
-                auto quad = [&](int slot) {
-                    return lv.base + ((long)b * P_NSLOT + slot) * lv.L.plane + lv.L.at(0, 0) +
-                           (long)q * h * lv.fg.lq;
-                };
-                at(0, 0, e) = Cm[qa]; at(0, 1, e) = quad(P_RES); at(0, 2, e) = quad(P_T);
-                at(1, 0, e) = quad(P_T); at(1, 1, e) = Cm[qb]; at(1, 2, e) = quad(P_RES);
-                at(2, 0, e) = Sm[qa]; at(2, 1, e) = quad(P_RES); at(2, 2, e) = quad(P_T);
-                at(3, 0, e) = quad(P_T); at(3, 1, e) = Sm[qb]; at(3, 2, e) = quad(P_PSI);
-            }
-        const double** dp = c->get<const double*>(tag + ".foldptr", P.size());
-        CK(cudaMemcpyAsync(dp, P.data(), P.size() * sizeof(void*), cudaMemcpyHostToDevice,
-                           c->stream));
-        CK(cudaStreamSynchronize(c->stream));  // host vector dies here
-        lv.gp = dp;
-    }
+    lv.lam = dct_lambda(c, n);
+    if (n + 1 <= kPdhgSmallMaxM) dct_operators(c, n, &lv.C, &lv.S);
+    lv.dp = dct_plan(c, n + 1);
+    lv.rows_f = dct_vectors_per_cta(lv.dp, B, c->num_sms, 0);
+    lv.cols = dct_vectors_per_cta(lv.dp, B, c->num_sms, 0);
+    lv.rows_i = dct_vectors_per_cta(lv.dp, B, c->num_sms, 1);
+    dct_kernel_attrs();
     CK(cudaMemsetAsync(lv.ticket, 0, sizeof(unsigned) * B, c->stream));
     return lv;
 }
@@ -197,38 +270,21 @@ void pget(w1mg_ctx* c, const PLevel& lv, int pair, int slot, double* dst, int w,
                          (size_t)w * 8, rows, cudaMemcpyDefault, c->stream));
 }
 
-// psi = (A A*)^+ r on every pair: slot `in` -> P_PSI (P_T scratch; `in` is
-// overwritten).  Column-major view of a node array: element (i, j) at
-// i + j*pitch, so both 1D transforms are the same sandwich Y = C X C^T.
+// psi = (A A*)^+ r on every pair: slot `in` -> P_PSI through the three DCT
+// launches (P_T scratch), poisson.cpp:72-99 without the mean removal.
 void poisson_apply(w1mg_ctx* c, const PLevel& lv, int in, bool check_done) {
-    cublasHandle_t h = blas(c);
-    const int m = lv.n + 1;
-    const int ld = lv.L.pitch;
-    const long long stride = (long long)P_NSLOT * lv.L.plane;
-    double* X = pslot_ptr(lv, 0, in);
-    double* T = pslot_ptr(lv, 0, P_T);
-    double* Psi = pslot_ptr(lv, 0, P_PSI);
-    const double one = 1.0, zero = 0.0;
+    const int m = lv.n + 1, cd = check_done ? 1 : 0;
+    const DctPlan& p = lv.dp;
     const double scale = 1.0 / (4.0 * double(m) * double(m));  // poisson.cpp:93
-    // DCT-II along both directions: T = C X, X = T C^T
-    blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, lv.C, m, 0, X,
-                                         ld, stride, &zero, T, ld, stride, lv.B),
-               "dgemm");
-    blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_T, m, m, m, &one, T, ld, stride,
-                                         lv.C, m, 0, &zero, X, ld, stride, lv.B),
-               "dgemm");
-    spectral_divide_kernel<<<dim3((m + 31) / 32, (m + 7) / 8, lv.B), dim3(32, 8), 0, c->stream>>>(
-        lv.args, in, lv.lam, check_done ? 1 : 0);
-    ++c->launches;
+    dct_rows_fwd_kernel<0><<<dim3((m + lv.rows_f - 1) / lv.rows_f, lv.B), 256,
+                             dct_smem_bytes(p, lv.rows_f), c->stream>>>(lv.args, p, in, lv.rows_f, cd);
+    dct_cols_kernel<<<dim3((m + lv.cols - 1) / lv.cols, lv.B), 256, dct_smem_bytes(p, lv.cols),
+                      c->stream>>>(lv.args, p, lv.lam, lv.cols, cd);
+    dct_rows_inv_kernel<0, 1><<<dim3((m + lv.rows_i - 1) / lv.rows_i, lv.B), 256,
+                                dct_smem_bytes(p, lv.rows_i), c->stream>>>(lv.args, p, lv.rows_i,
+                                                                            scale, cd);
     CK(cudaGetLastError());
-    // DCT-III along both directions, scaled by 1/(4 m^2)
-    blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, m, m, m, &one, lv.S, m, 0, X,
-                                         ld, stride, &zero, T, ld, stride, lv.B),
-               "dgemm");
-    blas_check(cublasDgemmStridedBatched(h, CUBLAS_OP_N, CUBLAS_OP_T, m, m, m, &scale, T, ld,
-                                         stride, lv.S, m, 0, &zero, Psi, ld, stride, lv.B),
-               "dgemm");
-    c->launches += 4;
+    c->launches += 3;
 }
 
 // psi -= compensated mean (poisson.cpp:96-98)
@@ -240,54 +296,27 @@ void remove_mean(w1mg_ctx* c, const PLevel& lv, int slot) {
     CK(cudaGetLastError());
 }
 
-// The iteration with folded DCTs: pre (folding), 4 batched GEMM stages over
-// the (pair, quadrant) products with the divide after stage 2, post.
-void pdhg_iteration_fold(w1mg_ctx* c, const PLevel& lv, int q) {
-    const FoldGeom g = lv.fg;
-    const int h = g.h, nb = 4 * lv.B;
-    const dim3 fblk(32, 8);
-    pdhg_pre_fold_kernel<<<dim3((h + 31) / 32, (h + 7) / 8, lv.B), fblk, 0, c->stream>>>(lv.args, g);
-    CK(cudaGetLastError());
-    cublasHandle_t hb = blas(c);
-    const double one = 1.0, zero = 0.0;
-    const int m = lv.n + 1;
-    const double scale = 1.0 / (4.0 * double(m) * double(m));  // poisson.cpp:93
-    auto arr = [&](int st, int t) { return lv.gp + ((size_t)st * 3 + t) * nb; };
-    auto gemm = [&](int st, cublasOperation_t tb, const double* alpha, int lda, int ldb) {
-        blas_check(cublasDgemmBatched(hb, CUBLAS_OP_N, tb, h, h, h, alpha, arr(st, 0), lda,
-                                      arr(st, 1), ldb, &zero,
-                                      const_cast<double* const*>(arr(st, 2)), g.lq, nb),
-                   "dgemm batched");
-    };
-    gemm(0, CUBLAS_OP_N, &one, h, g.lq);     // T = C_a X
-    gemm(1, CUBLAS_OP_T, &one, g.lq, h);     // X = T C_b^T
-    spectral_divide_fold_kernel<<<dim3((h + 31) / 32, (h + 7) / 8, nb), fblk, 0, c->stream>>>(
-        lv.args, g, lv.lam);
-    CK(cudaGetLastError());
-    gemm(2, CUBLAS_OP_N, &one, h, g.lq);     // T = S_a Y
-    gemm(3, CUBLAS_OP_T, &scale, g.lq, h);   // P = T S_b^T / (4 m^2)
-    switch (q) {
-        case 0: pdhg_post_fold_kernel<0><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args, g); break;
-        case 1: pdhg_post_fold_kernel<1><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args, g); break;
-        default: pdhg_post_fold_kernel<2><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args, g); break;
-    }
-    CK(cudaGetLastError());
-    c->launches += 7;
-}
+// One PDHG iteration = three launches: rows (pre step + DCT-II), columns
+// (DCT-II, divide, DCT-III), rows (DCT-III + post step + Eq. 12 + stop rule).
+constexpr int kPdhgLaunches = 3;
 
 void pdhg_iteration(w1mg_ctx* c, const PLevel& lv, int q) {
-    if (lv.fold) {
-        pdhg_iteration_fold(c, lv, q);
-        return;
-    }
-    pdhg_pre_kernel<<<lv.grid, lv.blk, 0, c->stream>>>(lv.args);
-    poisson_apply(c, lv, P_RES, true);
+    const int m = lv.n + 1;
+    const DctPlan& p = lv.dp;
+    const double scale = 1.0 / (4.0 * double(m) * double(m));  // poisson.cpp:93
+    dct_rows_fwd_kernel<1><<<dim3((m + lv.rows_f - 1) / lv.rows_f, lv.B), 256,
+                             dct_smem_bytes(p, lv.rows_f), c->stream>>>(lv.args, p, P_RES,
+                                                                        lv.rows_f, 1);
+    dct_cols_kernel<<<dim3((m + lv.cols - 1) / lv.cols, lv.B), 256, dct_smem_bytes(p, lv.cols),
+                      c->stream>>>(lv.args, p, lv.lam, lv.cols, 1);
+    const dim3 gi((m + lv.rows_i - 1) / lv.rows_i, lv.B);
+    const size_t si = dct_smem_bytes(p, lv.rows_i + 1);
     switch (q) {
-        case 0: pdhg_post_kernel<0><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args); break;
-        case 1: pdhg_post_kernel<1><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args); break;
-        default: pdhg_post_kernel<2><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args); break;
+        case 0: dct_rows_inv_kernel<1, 0><<<gi, 256, si, c->stream>>>(lv.args, p, lv.rows_i, scale, 1); break;
+        case 1: dct_rows_inv_kernel<1, 1><<<gi, 256, si, c->stream>>>(lv.args, p, lv.rows_i, scale, 1); break;
+        default: dct_rows_inv_kernel<1, 2><<<gi, 256, si, c->stream>>>(lv.args, p, lv.rows_i, scale, 1); break;
     }
-    c->launches += 2;
+    c->launches += kPdhgLaunches;
     CK(cudaGetLastError());
 }
 
@@ -333,13 +362,13 @@ void run_pdhg_iters(w1mg_ctx* c, const PLevel& lv, int q, long max_iters) {
         return;
     }
     std::string key(reinterpret_cast<const char*>(&lv.args), sizeof(SweepArgs));
-    key += "pdhg:" + std::to_string(q) + ":" + std::to_string(lv.B) + (lv.fold ? ":fold" : ":dense");
+    key += "pdhg:" + std::to_string(q) + ":" + std::to_string(lv.B) + ":dct" +
+           std::to_string(lv.rows_f) + "." + std::to_string(lv.cols) + "." + std::to_string(lv.rows_i);
     cudaGraphExec_t ex;
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) {
         ex = it->second;
     } else {
-        blas(c);  // create the handle outside the capture
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         const long before = c->launches;
@@ -354,7 +383,7 @@ void run_pdhg_iters(w1mg_ctx* c, const PLevel& lv, int q, long max_iters) {
     for (long g = 0;; ++g) {
         CK(cudaGraphLaunch(ex, c->stream));
         launched += K;
-        c->launches += 7L * K;
+        c->launches += (long)kPdhgLaunches * K;
         CK(cudaMemcpyAsync(c->pinned + (g & 1), lv.ndone, sizeof(int), cudaMemcpyDeviceToHost,
                            c->stream));
         CK(cudaEventRecord(c->ev[g & 1], c->stream));

@@ -11,13 +11,14 @@
 //   G^k = h^2 (sum dm^2/mu + sum dvarphi^2/tau + 2 sum dvarphi dm)     (Eq. 12)
 //
 // Poisson solve (poisson.cpp:72-99, FFTW REDFT10 -> divide -> REDFT01): the
-// 2D DCT-II/III on the m x m node grid (m = n+1, odd at the configs) is a
-// sandwich C X C^T, done as four fp64 GEMMs (cuBLAS DGEMM on the B200's
-// DMMA pipe) with the spectral divide in between.  Everything else of an
-// iteration is two fused node kernels:
-//   pdhg_pre_kernel   v = m - mu varphi_bar, r = A v - rho   (writes r only)
-//   pdhg_post_kernel  m, varphi, varphi_bar update + G^k partials + stop rule
-// v is recomputed in the post kernel (same expression, same bits) instead of
+// separable 2D DCT-II/III on the m x m node grid (m = n+1) runs in the
+// hand-written prime-factor DCT kernels of dct_kernels.cuh, which also fuse
+// the two node steps of an iteration (three launches per iteration):
+//   pre   v = m - mu varphi_bar, r = A v - rho   (into the row DCT-II)
+//   post  m, varphi, varphi_bar update + G^k partials + stop rule (after the
+//         row DCT-III; pdhg_post_kernel below is the standalone form used by
+//         the affine projection)
+// v is recomputed in the post step (same expression, same bits) instead of
 // being stored.  The mean removal of psi is skipped inside the iteration: A*
 // annihilates constants, so it only perturbs rounding; the public solve
 // (w1mg_poisson_solve) does remove it like poisson.cpp:96-98.
@@ -35,7 +36,7 @@ enum PSlot {
     P_BX = 4, P_BY = 5,   // varphi_bar
     P_RHO = 6,
     P_RES = 7,            // A v - rho / Poisson RHS (m x m, ld = pitch)
-    P_T = 8,              // GEMM temporary
+    P_T = 8,              // DCT intermediate (rows transformed)
     P_PSI = 9,            // Poisson solution
     P_NSLOT = 10
 };
@@ -68,23 +69,6 @@ __global__ void __launch_bounds__(256) pdhg_pre_kernel(const SweepArgs a) {
     const double b_ = (j > 0) ? my[o - L.pitch] - mu * by[o - L.pitch] : 0.0;
     const double div = (r_ - l_) * ih + (a_ - b_) * ih;
     pslot_w(a, b, P_RES)[o] = div - pslot(a, b, P_RHO)[o];
-}
-
-// Spectral divide (poisson.cpp:84-89): Y(k1,k2) /= lambda_k1 + lambda_k2,
-// constant mode pinned to zero.  Y is the pair's P_T slot viewed as an m x m
-// column-major matrix with ld = pitch (k1 = fast index).
-__global__ void spectral_divide_kernel(const SweepArgs a, int slot,
-                                       const double* __restrict__ lambda, int check_done) {
-    const int b = blockIdx.z;
-    if (check_done && *(volatile int*)&a.ctl[b].done) return;
-    const Layout L = a.L;
-    const int m = L.n + 1;
-    const int k1 = blockIdx.x * blockDim.x + threadIdx.x;
-    const int k2 = blockIdx.y * blockDim.y + threadIdx.y;
-    if (k1 >= m || k2 >= m) return;
-    double* Y = pslot_w(a, b, slot) + L.at(0, 0);
-    const long o = (long)k2 * L.pitch + k1;
-    Y[o] = (k1 == 0 && k2 == 0) ? 0.0 : Y[o] / (lambda[k1] + lambda[k2]);
 }
 
 // m, varphi, varphi_bar update + Eq. 12 partials + stop rule.

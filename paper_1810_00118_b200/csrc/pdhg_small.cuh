@@ -1,8 +1,7 @@
 // pdhg_small.cuh -- level-resident G-prox PDHG for small levels (m = n+1 <= 33).
 //
-// On the 33^2 level of a PDHG cascade the streaming iteration (pre kernel,
-// four cuBLAS DGEMMs, spectral divide, post kernel: seven launches) costs
-// ~19 us, almost all launch latency.  Here one CTA per pair
+// On the 33^2 level of a PDHG cascade a streaming iteration (three DCT
+// launches, dct_kernels.cuh) is almost all launch latency.  Here one CTA per pair
 // runs EVERY iteration of the level in one launch:
 //   pre      X = A (m - mu varphi_bar) - rho            (pdhg_pre_kernel)
 //   Poisson  T = C X, X = T C^T, divide by lambda_k1 + lambda_k2,
@@ -12,7 +11,7 @@
 // with the DCT operators C, S and the two m x m work arrays in shared memory
 // (4 m^2 doubles: 135 KB at m = 65) and the pair's state in its level buffer
 // (L2-resident).  Node arithmetic is the streaming kernels'; the DCT sums run
-// in a different order than cuBLAS (fp64 FMA), which the PDHG parity bar
+// in a different order than the streaming DCT (fp64 FMA), which the PDHG parity bar
 // (<= 1e-9 relative at fixed iterations) covers.
 #pragma once
 
@@ -25,10 +24,11 @@ constexpr int kPdhgSmallThreads = 1024;  // launch bound; the launch uses pdhg_s
 // passes) and the 561 DCT GEMM tiles (ncu: barrier stalls dominated with 1024)
 __host__ __device__ inline int pdhg_small_threads(int m) { return m <= 33 ? 576 : 1024; }
 constexpr int kPdhgSmallMaxM = 65;  // shared-memory capacity of the kernel
-// Measured on one B200 (config 3 levels, tools/configs.py 3): 33^2 level
-// 13.7 us per iteration vs 19 us streaming; 65^2 level 50 us vs 21 us (the
-// four m^3 GEMMs on ONE SM's fp64 pipe lose to cuBLAS on the whole GPU), so
-// the engine is used up to m = kPdhgSmallAutoM.
+// Measured on one B200 (config 3 levels, tools/configs.py 3, against the
+// earlier library-GEMM streaming iteration): 33^2 level 13.7 us per iteration
+// vs 19 us streaming; 65^2 level 50 us vs 21 us (the four m^3 GEMMs on ONE
+// SM's fp64 pipe lose to the whole GPU), so the engine is used up to
+// m = kPdhgSmallAutoM.
 constexpr int kPdhgSmallAutoM = 33;
 
 // levels up to kPdhgStateM also keep the pair's state (m, varphi, varphi_bar,

@@ -2,7 +2,8 @@
 solve and the affine projection, against oracle/pdhg_oracle.py (numpy +
 scipy DCT) -- itself pinned to the reference poisson.cpp in
 tests/test_oracle_vs_ref.py.  The DCT is computed differently on the GPU
-(DGEMM sandwich vs FFT), so fields agree to rounding, not bit for bit:
+(prime-factor DCT kernels, dct_kernels.cuh, vs scipy's FFT), so fields agree
+to rounding, not bit for bit:
 tolerance 1e-9 relative at fixed iterations (BASELINE.json), 1e-4 on W1 at
 convergence."""
 import numpy as np
@@ -25,7 +26,11 @@ def _src(rho):
     return w1mg.SourceField(w1mg.ScalarField(w1mg.GridSpec(rho.shape[0] - 1), rho))
 
 
-@pytest.mark.parametrize("n", [4, 8, 32, 100, 256, 512])
+# m = n+1 covers every DCT plan shape: prime (5, 257), even with a Nyquist
+# row (9 -> 9, 100 -> 101 prime, 31 -> 32 = 2^5, 47 -> 48 = 16 x 3, 63 -> 64),
+# two coprime factors with odd/even parts (33 = 11 x 3, 65 = 13 x 5,
+# 129 = 43 x 3, 513 = 27 x 19, 1025 = 41 x 25, 2049 = 683 x 3)
+@pytest.mark.parametrize("n", [1, 4, 8, 31, 32, 47, 63, 64, 100, 128, 256, 512, 1024, 2048])
 def test_poisson_solve_matches_oracle(n):
     rng = np.random.default_rng(n)
     b = rng.standard_normal((n + 1, n + 1))
@@ -62,22 +67,20 @@ def test_project_affine(n):
     assert _rel(again.x_edges, out.x_edges) <= 1e-10
 
 
-@pytest.fixture(params=["streaming", "resident", "streaming-folded"])
+@pytest.fixture(params=["streaming", "resident"])
 def pdhg_engine(request):
-    """streaming: 7-launch iteration with the dense DCT sandwich; resident:
-    one CTA per pair for m <= 65; streaming-folded: symmetry-folded DCTs
-    (forced on every odd m; auto uses them from m >= 400)."""
+    """streaming: 3-launch iteration (row DCT-II + pre, column DCT-II /
+    divide / DCT-III, row DCT-III + post); resident: one CTA per pair for
+    m <= 65."""
     from paper_1810_00118_b200 import _lib
 
     L = _lib.lib()
     L.w1mg_set_pdhg_small(2 if request.param == "resident" else 0)
-    L.w1mg_set_option(b"pdhg_fold", 2 if request.param == "streaming-folded" else 0)
     yield request.param
     L.w1mg_set_pdhg_small(1)
-    L.w1mg_set_option(b"pdhg_fold", 1)
 
 
-@pytest.mark.parametrize("n", [32, 64, 128, 256])
+@pytest.mark.parametrize("n", [31, 32, 64, 128, 256])
 @pytest.mark.parametrize("p", [0, 1, 2])
 def test_pdhg_fixed_iterations(p, n, pdhg_engine):
     rho = instances.config1_source(n)

@@ -74,9 +74,10 @@ def test_engine_switches_validate_host():
     L = _lib.lib()
     assert L.w1mg_set_option(b"no_such_option", 1) == _lib.W1MG_EINVAL
     assert L.w1mg_set_option(b"tmap_nw", 3) == _lib.W1MG_EINVAL
-    assert L.w1mg_set_option(b"pdhg_fold", 7) == _lib.W1MG_EINVAL
+    assert L.w1mg_set_option(b"pdhg_fold", 1) == _lib.W1MG_EINVAL  # engine removed
+    assert L.w1mg_set_option(b"pdhg_small", 7) == _lib.W1MG_EINVAL
     assert L.w1mg_set_option(None, 1) == _lib.W1MG_EINVAL
-    for name, val in ((b"tmap_nw", 4), (b"pdhg_fold", 1), (b"compact", 1), (b"cluster_pick", 1)):
+    for name, val in ((b"tmap_nw", 4), (b"pdhg_small", 1), (b"compact", 1), (b"cluster_pick", 1)):
         assert L.w1mg_set_option(name, val) == _lib.W1MG_OK
     assert L.w1mg_set_option(b"tmap_nw", 0) == _lib.W1MG_OK  # back to auto
     assert L.w1mg_set_option(b"tile_depth", 3) == _lib.W1MG_EINVAL
