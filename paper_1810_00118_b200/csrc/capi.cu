@@ -76,6 +76,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_PDHG_SMALL")) g_pdhg_small = std::atoi(v);
         if (const char* v = std::getenv("W1MG_WARPS_PER_SM")) g_warps_per_sm = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_PDL")) g_pdl = std::atoi(v) != 0;
+        if (const char* v = std::getenv("W1MG_FAST")) g_fast = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_TILE")) g_tile = std::atoi(v);
         if (const char* v = std::getenv("W1MG_TILE_MIN")) g_tile_min = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TILE_MAX")) g_tile_max = std::max(1, std::atoi(v));
@@ -613,6 +614,7 @@ int w1mg_set_option(const char* name, long value) {
     else if (k == "compact_step" && v >= 1) g_compact_step = v;
     else if (k == "warps_per_sm" && v >= 1) g_warps_per_sm = v;
     else if (k == "pdl" && (v == 0 || v == 1)) g_pdl = v;
+    else if (k == "fast" && (v == 0 || v == 1)) g_fast = v;
     else if (k == "tmap_nw" && (v == 0 || v == 2 || v == 4 || v == 8)) g_tmap_nw = v;
     else if (k == "tile" && v >= 0 && v <= 2) g_tile = v;
     else if (k == "tile_min" && v >= 1) g_tile_min = v;

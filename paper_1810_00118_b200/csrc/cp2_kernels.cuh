@@ -321,9 +321,9 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                 node_flux<PN>(hx, hy, pc, pr, pu, mxo, myo, mu, zt, ih, uxA, uyAn, dxA, dyAn);
                 const double uxl = __shfl_up_sync(0xffffffffu, uxA, 1);
                 const double dxl = __shfl_up_sync(0xffffffffu, dxA, 1);
-                const double divm = (uxA - uxl) * ih + (uyAn - uyA) * ih;
-                const double divd = (dxA - dxl) * ih + (dyAn - dyA) * ih;
-                const double d = tau * (divm + divd - r);
+                double divd;
+                const double d =
+                    phi_delta<PN>(uxA, uxl, uyAn, uyA, dxA, dxl, dyAn, dyA, r, ih, tau, divd);
                 fA = pc + d;
                 if (kMode == 3 || (own && rA >= j0 && rA < j1)) {
                     a_dm2 = __fma_rn(dyAn, dyAn, __fma_rn(dxA, dxA, a_dm2));
@@ -344,9 +344,9 @@ __device__ __forceinline__ void march2(const SweepArgs& a, int pair, int parity,
                                    ux, uy, dx, dy);
                 const double uxl = __shfl_up_sync(0xffffffffu, ux, 1);
                 const double dxl = __shfl_up_sync(0xffffffffu, dx, 1);
-                const double divm = (ux - uxl) * ih + (uy - uyB) * ih;
-                const double divd = (dx - dxl) * ih + (dy - dyB) * ih;
-                const double d = tau * (divm + divd - r_prev);
+                double divd;
+                const double d =
+                    phi_delta<PN>(ux, uxl, uy, uyB, dx, dxl, dy, dyB, r_prev, ih, tau, divd);
                 if (own && (kMode == 3 || rB >= j0)) {  // rB < j1 always
                     *wph = pcB + d;
                     if (hx) *wmx = ux;

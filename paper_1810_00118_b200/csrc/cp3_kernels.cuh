@@ -231,9 +231,9 @@ __device__ __forceinline__ void march3(const SweepArgs& a, int pair, int parity,
             node_flux<PN>(hx, hy, pc, pr, pu, mxo, myo, mu, zt, ih, uxA, uyAn, dxA, dyAn);
             const double uxl = __shfl_up_sync(0xffffffffu, uxA, 1);
             const double dxl = __shfl_up_sync(0xffffffffu, dxA, 1);
-            const double divm = (uxA - uxl) * ih + (uyAn - uyA) * ih;
-            const double divd = (dxA - dxl) * ih + (dyAn - dyA) * ih;
-            const double d = tau * (divm + divd - r);
+            double divd;
+            const double d =
+                phi_delta<PN>(uxA, uxl, uyAn, uyA, dxA, dxl, dyAn, dyA, r, ih, tau, divd);
             fA = pc + d;
             if (kMode == 3 || (own && rA >= j0 && rA < j1)) {
                 acc[0] = __fma_rn(dyAn, dyAn, __fma_rn(dxA, dxA, acc[0]));
@@ -254,9 +254,9 @@ __device__ __forceinline__ void march3(const SweepArgs& a, int pair, int parity,
                           uxB, uyBn, dx, dy);
             const double uxl = __shfl_up_sync(0xffffffffu, uxB, 1);
             const double dxl = __shfl_up_sync(0xffffffffu, dx, 1);
-            const double divm = (uxB - uxl) * ih + (uyBn - uyB) * ih;
-            const double divd = (dx - dxl) * ih + (dy - dyB) * ih;
-            const double d = tau * (divm + divd - r_prev);
+            double divd;
+            const double d =
+                phi_delta<PN>(uxB, uxl, uyBn, uyB, dx, dxl, dy, dyB, r_prev, ih, tau, divd);
             fB = fA_prev + d;
             if (kMode == 3 || (own && rB >= j0 && rB < j1)) {
                 acc[3] = __fma_rn(dy, dy, __fma_rn(dx, dx, acc[3]));
@@ -276,9 +276,9 @@ __device__ __forceinline__ void march3(const SweepArgs& a, int pair, int parity,
                           uy, dx, dy);
             const double uxl = __shfl_up_sync(0xffffffffu, ux, 1);
             const double dxl = __shfl_up_sync(0xffffffffu, dx, 1);
-            const double divm = (ux - uxl) * ih + (uy - uyC) * ih;
-            const double divd = (dx - dxl) * ih + (dy - dyC) * ih;
-            const double d = tau * (divm + divd - r_prev2);
+            double divd;
+            const double d =
+                phi_delta<PN>(ux, uxl, uy, uyC, dx, dxl, dy, dyC, r_prev2, ih, tau, divd);
             if (own && (kMode == 3 || rC >= j0)) {  // rC < j1 always
                 *wph = fB_prev + d;
                 if (hx) *wmx = ux;

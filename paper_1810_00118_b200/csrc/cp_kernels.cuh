@@ -124,13 +124,24 @@ constexpr int kTmaSmem = kSweepWarps * (kStages * kStageBytes + kStages * 8);
 // kNB: branch-free p = 2 shrink (shrink2_nb: the restated fast paths of
 // sqrt and division plus selects, bit-identical to shrink<1>) -- no
 // divergent region per node, so the scheduler can interleave nodes.
+// PN = 3: p = 2 in tolerance mode ("fast" numerics, streaming sweep kernels
+// only): v = m - (mu ih)(pc - pr) by one FMA and shrink2_fast.
 template <int PN, bool kNB = true>
 __device__ __forceinline__ void node_flux(bool hx, bool hy, double pc, double pr, double pu,
                                           double mxo, double myo, double mu, double zt, double ih,
                                           double& ux, double& uy, double& dx, double& dy) {
-    double vx = hx ? mxo - mu * ((pc - pr) * ih) : 0.0;
-    double vy = hy ? myo - mu * ((pc - pu) * ih) : 0.0;
-    if constexpr (kNB && PN == 1) {
+    double vx, vy;
+    if constexpr (PN == 3) {
+        const double muih = mu * ih;  // loop-invariant, hoisted
+        vx = hx ? __fma_rn(-muih, pc - pr, mxo) : 0.0;
+        vy = hy ? __fma_rn(-muih, pc - pu, myo) : 0.0;
+    } else {
+        vx = hx ? mxo - mu * ((pc - pr) * ih) : 0.0;
+        vy = hy ? myo - mu * ((pc - pu) * ih) : 0.0;
+    }
+    if constexpr (PN == 3) {
+        shrink2_fast(vx, vy, mu, zt, ux, uy);
+    } else if constexpr (kNB && PN == 1) {
         shrink2_nb(vx, vy, mu, zt, ux, uy);
     } else {
         shrink<PN>(vx, vy, mu, ux, uy);
@@ -139,6 +150,25 @@ __device__ __forceinline__ void node_flux(bool hx, bool hy, double pc, double pr
     ux = hx ? ux : 0.0;
     dy = hy ? uy - myo : 0.0;
     uy = hy ? uy : 0.0;
+}
+
+// phi increment d = tau (div m^{k+1} + div dm - rho) (solver_cp.cpp:61-64,
+// divergence_into's x-then-y order) and div dm for the residual cross term.
+// PN = 3 (tolerance mode): tau ih ((x-diffs) + (y-diffs)) - tau rho by one FMA.
+template <int PN>
+__device__ __forceinline__ double phi_delta(double ux, double uxl, double uy, double uyb,
+                                            double dx, double dxl, double dy, double dyb,
+                                            double r, double ih, double tau, double& divd) {
+    if constexpr (PN == 3) {
+        const double dd = (dx - dxl) + (dy - dyb);
+        const double dm = (ux - uxl) + (uy - uyb);
+        divd = dd * ih;
+        return __fma_rn(tau * ih, dm + dd, -(tau * r));
+    } else {
+        const double divm = (ux - uxl) * ih + (uy - uyb) * ih;
+        divd = (dx - dxl) * ih + (dy - dyb) * ih;
+        return tau * (divm + divd - r);
+    }
 }
 
 // Everything a warp needs about its strip.
@@ -213,9 +243,8 @@ __device__ __forceinline__ void row_update(const SweepArgs& a, const Strip& s, i
     node_flux<PN>(s.hx, hy, pc, pr, pu, mxo, myo, a.mu, a.zt, ih, ux, uy, dx, dy);
     double uxl = __shfl_up_sync(0xffffffffu, ux, 1);
     double dxl = __shfl_up_sync(0xffffffffu, dx, 1);
-    double divm = (ux - uxl) * ih + (uy - uyb) * ih;
-    double divd = (dx - dxl) * ih + (dy - dyb) * ih;
-    double d = a.tau * (divm + divd - r);
+    double divd;
+    const double d = phi_delta<PN>(ux, uxl, uy, uyb, dx, dxl, dy, dyb, r, ih, a.tau, divd);
     if (s.own) {
         s.phw[o] = pc + d;
         if (s.hx) s.mxw[o] = ux;

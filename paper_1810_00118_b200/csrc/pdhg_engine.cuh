@@ -244,7 +244,10 @@ PLevel make_plevel(w1mg_ctx* c, const std::string& tag, int n, int B, double mu,
     a.hist = hist;
     a.hist_cap = hist_cap;
     a.ndone = lv.ndone;
-    a.partial = c->get<double>(tag + ".partial", (size_t)B * lv.grid.x * lv.grid.y * 3);
+    // residual partials: node-grid blocks (pdhg_post_kernel) or one block per
+    // DCT row group (dct_rows_inv_kernel, at most m)
+    a.partial = c->get<double>(tag + ".partial",
+                               (size_t)B * std::max<size_t>((size_t)lv.grid.x * lv.grid.y, n + 1) * 3);
     lv.lam = dct_lambda(c, n);
     if (n + 1 <= kPdhgSmallMaxM) dct_operators(c, n, &lv.C, &lv.S);
     lv.dp = dct_plan(c, n + 1);

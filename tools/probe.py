@@ -24,6 +24,20 @@ def probe(ctx, n, B, p=1, warm=20, iters=50):
             "frac": gbs / HBM, "cell_updates_per_s": V * B / (ms.value * 1e-3)}
 
 
+def probe_clocked(ctx, n, B, p=1):
+    """probe() sized to ~1 s of sweeps, with nvidia-smi clocks sampled while
+    it runs (bench.ClockSampler): every probe line carries its clock record."""
+    from bench import ClockSampler
+
+    first = probe(ctx, n, B, p)
+    iters = max(50, int(1.0 / (first["ms_per_sweep"] * 1e-3)))
+    with ClockSampler(0) as clk:
+        r = probe(ctx, n, B, p, warm=20, iters=iters)
+    r["clocks"] = clk.summary()
+    r["fast"] = int(os.environ.get("W1MG_FAST", "0"))
+    return r
+
+
 if __name__ == "__main__":
     ctx = _lib.Context(0)
     engines = [int(e) for e in os.environ.get("ENGINES", "3").split(",")]  # 0 ldg, 1 tma, 2 tma2, 3 auto, 4 tma2w, 5 tma2t, 6 tma3
@@ -34,7 +48,7 @@ if __name__ == "__main__":
     for n, B in cases:
         for e in engines:
             ctx.L.w1mg_set_sweep_engine(e)
-            r = probe(ctx, n, B)
+            r = probe_clocked(ctx, n, B)
             r["engine"] = ["ldg", "tma", "tma2", "auto", "tma2w", "tma2t", "tma3"][e]
             print(json.dumps(r), flush=True)
 
