@@ -121,17 +121,21 @@ def read_image(path: str) -> np.ndarray:
 
 # --------------------------------------------------------- discretisation
 def discretize(img: np.ndarray, n: int) -> np.ndarray:
-    """Bilinear resampling of the pixel lattice (centres at (c+0.5)/M) onto
-    the (n+1)^2 nodes (i/n, j/n), clamped at the border, scaled to unit mass
+    """Bilinear resampling of the pixel lattice onto the (n+1)^2 nodes, with
+    the pixel centres mapped onto [0,1]^2 (pixel centre c of an
+    M-pixel side sits at c/(M-1), so corner pixels land on corner nodes; node
+    j at x = j/n reads pixel coordinate j (M-1)/n), then scaled to unit mass
     in the L1_h sense: sum rho h^2 = 1."""
     M = img.shape[0]
-    t = np.arange(n + 1) / n * M - 0.5  # node position in pixel-centre index space
-    t = np.clip(t, 0.0, M - 1.0)
-    i0 = np.minimum(np.floor(t).astype(int), M - 2) if M > 1 else np.zeros(n + 1, int)
-    f = t - i0 if M > 1 else np.zeros(n + 1)
-    i1 = np.minimum(i0 + 1, M - 1)
-    rows = img[i0, :] * (1 - f)[:, None] + img[i1, :] * f[:, None]
-    out = rows[:, i0] * (1 - f)[None, :] + rows[:, i1] * f[None, :]
+    if M == 1:
+        out = np.full((n + 1, n + 1), float(img[0, 0]))
+    else:
+        t = np.arange(n + 1) * ((M - 1) / n)  # node position in pixel-centre index space
+        i0 = np.minimum(np.floor(t).astype(int), M - 2)
+        f = t - i0
+        i1 = i0 + 1
+        rows = img[i0, :] * (1 - f)[:, None] + img[i1, :] * f[:, None]
+        out = rows[:, i0] * (1 - f)[None, :] + rows[:, i1] * f[None, :]
     h = 1.0 / n
     return out / (math.fsum(out.ravel().tolist()) * h * h)
 

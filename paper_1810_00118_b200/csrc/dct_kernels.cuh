@@ -49,24 +49,34 @@ namespace w1mg_dev {
 
 // H = N/2 + 1 outputs of a real length-N DFT, T = (N-1)/2 symmetric pairs
 // (t, N-t), E = 1 for even N: the Nyquist element N/2 enters once, as an
-// extra row T of the cosine GEMM.
+// extra row T of the cosine GEMM (its twiddle cos(2 pi (N/2) k / N) = (-1)^k
+// is the natural continuation of the table index).
+//
+// Twiddles are never stored as matrices: the GEMM operand A(t, k) of a stage
+// over a factor N is +-tab[((t+1) k) mod N] with tab = cos / sin of 2 pi j/N,
+// so a CTA stages only 2 (N1 + N2) + 2 m doubles (and the index maps) in
+// shared memory -- 9 KB at m = 513, 4 KB at the prime m = 257, where a dense
+// twiddle matrix would be 270 KB.
 struct DctPlan {
     int m, N1, N2, H1, T1, E1, H2, T2, E2, H1p, H2p;
+    const double* tw1;  // [2][N1] cos, sin of 2 pi j / N1
+    const double* tw2;  // [2][N2] cos, sin of 2 pi j / N2
+    const double* mk;   // [2m] cos, sin of pi k / 2m (interleaved)
     const short* idxA;  // [N2][N1] row position of v[(N2 t + N1 n2) mod m]
     const short* crt;   // [N2][H1] k with k mod N1 = k1 and k mod N2 = k2
-    const double* c1;   // [T1+E1][H1p]  cos(2 pi (t+1) k1 / N1); Nyquist row (-1)^k1
-    const double* s1;   // [T1][H1p]    -sin(2 pi (t+1) k1 / N1)
-    const double* c2;   // [T2+E2][H2p]  cos(2 pi (t+1) k2 / N2); Nyquist row (-1)^k2
-    const double* s2;   // [T2][H2p]     sin(2 pi (t+1) k2 / N2)
-    const double* cT;   // [T1+E1][H1p]  cos(2 pi n1 (k1+1) / N1); Nyquist row (-1)^n1 / 2
-    const double* sT;   // [T1][H1p]     sin(2 pi n1 (k1+1) / N1)
-    const double* mk;   // [2m] cos, sin of pi k / 2m
 };
 
 __host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
 
+// doubles of the staged tables: tw1, tw2, mk, then the short index maps
+__host__ __device__ inline int dct_tab_doubles(const DctPlan& p) {
+    const int d = 2 * p.N1 + 2 * p.N2 + 2 * p.m;
+    const int sh = p.N2 * p.N1 + p.N2 * p.H1;
+    return round4(d + (sh + 3) / 4);
+}
+
 // Shared-memory arenas (doubles) for NV vectors: P and Q (ping-pong scratch
-// of the stages), then X (NV x m).
+// of the stages), then X (NV x m); the staged tables come first.
 __host__ __device__ inline void dct_arena(const DctPlan& p, int NV, int& szP, int& szQ) {
     const int NpA = round4(NV * p.N2);
     szP = (2 * p.T1 + 1 + p.E1) * NpA;
@@ -84,53 +94,107 @@ __host__ __device__ inline void dct_arena(const DctPlan& p, int NV, int& szP, in
 __host__ __device__ inline size_t dct_smem_bytes(const DctPlan& p, int NV) {
     int a, b;
     dct_arena(p, NV, a, b);
-    return sizeof(double) * ((size_t)a + b + (size_t)NV * p.m);
+    return sizeof(double) * ((size_t)dct_tab_doubles(p) + a + b + (size_t)NV * p.m);
 }
 
-// C[i][j] = (C0 ? C0[j] : 0) + sum_k A[k*lda + i] * B[k*ldb + j] for
-// i < 4 Mt, j < 4 Nt.  A: twiddle table in global memory (read-only path);
-// B, C, C0: shared memory, rows 16-B aligned.  One 4 x 4 tile per thread.
-__device__ __forceinline__ void tgemm(const double* __restrict__ A, int lda, int Mt, int K,
-                                      const double* B, int ldb, int Nt, double* C, int ldc,
+// C[k][j] = (C0 ? C0[j] : 0) + sgn sum_{t<K} tab[((t+1) k) mod N] B[t*ldb + j]
+// for k < Mp, j < Np (multiples of 4); tab, B, C, C0 in shared memory.
+// Wide GEMMs: 4 x 4 register tiles (lanes of a warp share the rows, so the
+// twiddle loads broadcast); thin ones (few tiles per thread block): one output
+// per thread, two accumulators.
+__device__ __forceinline__ void tgemm(const double* tab, int N, double sgn, int Mp, int K,
+                                      const double* B, int ldb, int Np, double* C, int ldc,
                                       const double* C0) {
-    const int tiles = Mt * Nt;
-    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
-        const int ti = t / Nt, tj = t - ti * Nt;
-        double acc[4][4];
-        double2 z01 = make_double2(0.0, 0.0), z23 = z01;
-        if (C0) {
-            z01 = *reinterpret_cast<const double2*>(C0 + 4 * tj);
-            z23 = *reinterpret_cast<const double2*>(C0 + 4 * tj + 2);
-        }
+    const int Nt = Np >> 2, tiles = (Mp >> 2) * Nt;
+    if (2 * tiles >= (int)blockDim.x) {
+        for (int tt = threadIdx.x; tt < tiles; tt += blockDim.x) {
+            const int ti = tt / Nt, tj = tt - ti * Nt;
+            int kr[4], ix[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            acc[r][0] = z01.x;
-            acc[r][1] = z01.y;
-            acc[r][2] = z23.x;
-            acc[r][3] = z23.y;
-        }
-        const double* a = A + 4 * ti;
-        const double* b = B + 4 * tj;
-#pragma unroll 4
-        for (int k = 0; k < K; ++k) {
-            const double2 a01 = __ldg(reinterpret_cast<const double2*>(a + (long)k * lda));
-            const double2 a23 = __ldg(reinterpret_cast<const double2*>(a + (long)k * lda + 2));
-            const double2 b01 = *reinterpret_cast<const double2*>(b + k * ldb);
-            const double2 b23 = *reinterpret_cast<const double2*>(b + k * ldb + 2);
-            const double av[4] = {a01.x, a01.y, a23.x, a23.y};
-            const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+            for (int r = 0; r < 4; ++r) {
+                kr[r] = (4 * ti + r) % N;
+                ix[r] = kr[r];
+            }
+            double acc[4][4];
 #pragma unroll
             for (int r = 0; r < 4; ++r)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[r][q] = fma(av[r], bv[q], acc[r][q]);
-        }
+                for (int q = 0; q < 4; ++q) acc[r][q] = 0.0;
+            const double* b = B + 4 * tj;
+#pragma unroll 2
+            for (int t = 0; t < K; ++t) {
+                const double2 b01 = *reinterpret_cast<const double2*>(b + t * ldb);
+                const double2 b23 = *reinterpret_cast<const double2*>(b + t * ldb + 2);
+                const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            double* cr = C + (4 * ti + r) * ldc + 4 * tj;
-            *reinterpret_cast<double2*>(cr) = make_double2(acc[r][0], acc[r][1]);
-            *reinterpret_cast<double2*>(cr + 2) = make_double2(acc[r][2], acc[r][3]);
+                for (int r = 0; r < 4; ++r) {
+                    const double av = tab[ix[r]];
+                    ix[r] += kr[r];
+                    if (ix[r] >= N) ix[r] -= N;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[r][q] = fma(av, bv[q], acc[r][q]);
+                }
+            }
+            double c0[4] = {0.0, 0.0, 0.0, 0.0};
+            if (C0) {
+                const double2 z01 = *reinterpret_cast<const double2*>(C0 + 4 * tj);
+                const double2 z23 = *reinterpret_cast<const double2*>(C0 + 4 * tj + 2);
+                c0[0] = z01.x;
+                c0[1] = z01.y;
+                c0[2] = z23.x;
+                c0[3] = z23.y;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                double* cr = C + (4 * ti + r) * ldc + 4 * tj;
+                *reinterpret_cast<double2*>(cr) =
+                    make_double2(c0[0] + sgn * acc[r][0], c0[1] + sgn * acc[r][1]);
+                *reinterpret_cast<double2*>(cr + 2) =
+                    make_double2(c0[2] + sgn * acc[r][2], c0[3] + sgn * acc[r][3]);
+            }
+        }
+    } else {
+        for (int e = threadIdx.x; e < Mp * Np; e += blockDim.x) {
+            const int k = e / Np, j = e - k * Np;
+            const int kr = k % N;
+            int ix = kr;
+            double a0 = 0.0, a1 = 0.0;
+            int t = 0;
+            for (; t + 1 < K; t += 2) {
+                const double w0 = tab[ix];
+                ix += kr;
+                if (ix >= N) ix -= N;
+                const double w1 = tab[ix];
+                ix += kr;
+                if (ix >= N) ix -= N;
+                a0 = fma(w0, B[t * ldb + j], a0);
+                a1 = fma(w1, B[(t + 1) * ldb + j], a1);
+            }
+            if (t < K) a0 = fma(tab[ix], B[t * ldb + j], a0);
+            C[k * ldc + j] = (C0 ? C0[j] : 0.0) + sgn * (a0 + a1);
         }
     }
+}
+
+// Stage the plan's tables into shared memory; returns the smem view.
+__device__ __forceinline__ DctPlan dct_stage_tables(const DctPlan& g, double* sm) {
+    DctPlan p = g;
+    double* tw1 = sm;
+    double* tw2 = tw1 + 2 * g.N1;
+    double* mk = tw2 + 2 * g.N2;
+    short* ia = reinterpret_cast<short*>(mk + 2 * g.m);
+    short* cr = ia + g.N2 * g.N1;
+    for (int e = threadIdx.x; e < 2 * g.N1; e += blockDim.x) tw1[e] = g.tw1[e];
+    for (int e = threadIdx.x; e < 2 * g.N2; e += blockDim.x) tw2[e] = g.tw2[e];
+    for (int e = threadIdx.x; e < 2 * g.m; e += blockDim.x) mk[e] = g.mk[e];
+    for (int e = threadIdx.x; e < g.N2 * g.N1; e += blockDim.x) ia[e] = g.idxA[e];
+    for (int e = threadIdx.x; e < g.N2 * g.H1; e += blockDim.x) cr[e] = g.crt[e];
+    p.tw1 = tw1;
+    p.tw2 = tw2;
+    p.mk = mk;
+    p.idxA = ia;
+    p.crt = cr;
+    return p;
 }
 
 // Forward DCT-II of NV vectors X[v*m + i] in place (P, Q scratch).
@@ -168,8 +232,8 @@ __device__ void dct2_vectors(const DctPlan& p, int NV, double* X, double* P, dou
     // stage 1: A[k1][j] = X0 + sum cos S - i sum sin D, k1 < H1
     double* ReA = Q;
     double* ImA = Q + p.H1p * NpA;
-    tgemm(p.c1, p.H1p, p.H1p / 4, T1 + E1, SA, NpA, NpA / 4, ReA, NpA, X0);
-    tgemm(p.s1, p.H1p, p.H1p / 4, T1, DA, NpA, NpA / 4, ImA, NpA, nullptr);
+    tgemm(p.tw1, N1, 1.0, p.H1p, T1 + E1, SA, NpA, NpA, ReA, NpA, X0);
+    tgemm(p.tw1 + N1, N1, -1.0, p.H1p, T1, DA, NpA, NpA, ImA, NpA, nullptr);
     __syncthreads();
     const int NB = NV * H1, NpB = round4(NB), W2 = 2 * NpB, H2 = p.H2;
     double* Cp = Q;
@@ -214,8 +278,8 @@ __device__ void dct2_vectors(const DctPlan& p, int NV, double* X, double* P, dou
             }
         }
         __syncthreads();
-        tgemm(p.c2, p.H2p, p.H2p / 4, T2 + E2, SB, W2, W2 / 4, Cp, W2, A0);
-        tgemm(p.s2, p.H2p, p.H2p / 4, T2, DB, W2, W2 / 4, Sn, W2, nullptr);
+        tgemm(p.tw2, N2, 1.0, p.H2p, T2 + E2, SB, W2, W2, Cp, W2, A0);
+        tgemm(p.tw2 + N2, N2, 1.0, p.H2p, T2, DB, W2, W2, Sn, W2, nullptr);
         __syncthreads();
     }
     // V[k1, k2] = Cp - i Sn (k2 < H2), V[k1, N2 - k2] = Cp + i Sn; V[m-k] = conj V[k];
@@ -281,7 +345,7 @@ __device__ void dct3_vectors(const DctPlan& p, int NV, double* X, double* P, dou
             if (t == 0) {
                 B0[j] = wr;
             } else {
-                BR[(t - 1) * NpA + j] = wr;
+                BR[(t - 1) * NpA + j] = (t <= T1) ? wr : 0.5 * wr;  // Nyquist enters once
                 if (t <= T1) BI[(t - 1) * NpA + j] = wi;
             }
         }
@@ -327,8 +391,8 @@ __device__ void dct3_vectors(const DctPlan& p, int NV, double* X, double* P, dou
         __syncthreads();
         double* Cp = Q;
         double* Sn = Q + p.H2p * W2;
-        tgemm(p.c2, p.H2p, p.H2p / 4, T2 + E2, SB, W2, W2 / 4, Cp, W2, A0);
-        tgemm(p.s2, p.H2p, p.H2p / 4, T2, DB, W2, W2 / 4, Sn, W2, nullptr);
+        tgemm(p.tw2, N2, 1.0, p.H2p, T2 + E2, SB, W2, W2, Cp, W2, A0);
+        tgemm(p.tw2 + N2, N2, 1.0, p.H2p, T2, DB, W2, W2, Sn, W2, nullptr);
         __syncthreads();
         // b[k1][n2] = Cp + i Sn (n2 < H2), b[k1][N2 - n2] = Cp - i Sn -> stage 1 inputs
         // (vector j = n2 NV + v): BR / BI rows k1 = 1..H1-1, B0 = Re b[0]
@@ -352,7 +416,7 @@ __device__ void dct3_vectors(const DctPlan& p, int NV, double* X, double* P, dou
             if (t == 0) {
                 B0[j] = br;
             } else {
-                BR[(t - 1) * NpA + j] = br;
+                BR[(t - 1) * NpA + j] = (t <= T1) ? br : 0.5 * br;  // Nyquist enters once
                 if (t <= T1) BI[(t - 1) * NpA + j] = bi;
             }
         }
@@ -361,8 +425,8 @@ __device__ void dct3_vectors(const DctPlan& p, int NV, double* X, double* P, dou
     // stage 1 (inverse, over k1): w[n1] = b0 + 2 (P - Q), w[N1 - n1] = b0 + 2 (P + Q)
     double* PP = Q;
     double* QQ = Q + p.H1p * NpA;
-    tgemm(p.cT, p.H1p, p.H1p / 4, T1 + E1, BR, NpA, NpA / 4, PP, NpA, nullptr);
-    tgemm(p.sT, p.H1p, p.H1p / 4, T1, BI, NpA, NpA / 4, QQ, NpA, nullptr);
+    tgemm(p.tw1, N1, 1.0, p.H1p, T1 + E1, BR, NpA, NpA, PP, NpA, nullptr);
+    tgemm(p.tw1 + N1, N1, 1.0, p.H1p, T1, BI, NpA, NpA, QQ, NpA, nullptr);
     __syncthreads();
     // un-reorder: n = (N2 n1 + N1 n2) mod m -> y[2n] / y[2(m-1-n)+1]
     for (int e = threadIdx.x; e < NA * N1; e += blockDim.x) {
@@ -379,13 +443,14 @@ __device__ void dct3_vectors(const DctPlan& p, int NV, double* X, double* P, dou
     __syncthreads();
 }
 
-__device__ __forceinline__ void dct_smem(const DctPlan& p, int NV, double*& P, double*& Q,
-                                         double*& X) {
+__device__ __forceinline__ void dct_smem(const DctPlan& g, int NV, DctPlan& p, double*& P,
+                                         double*& Q, double*& X) {
     extern __shared__ __align__(16) double dct_sm[];
     int a, b;
-    dct_arena(p, NV, a, b);
-    P = dct_sm;
-    Q = dct_sm + a;
+    dct_arena(g, NV, a, b);
+    p = dct_stage_tables(g, dct_sm);
+    P = dct_sm + dct_tab_doubles(g);
+    Q = P + a;
     X = Q + b;
 }
 
@@ -410,12 +475,13 @@ __device__ __forceinline__ double pdhg_rhs(const SweepArgs& a, int b, int i, int
 // Rows j0 .. j0+R-1: (MODE 0) slot `in` or (MODE 1) the PDHG right-hand side
 // -> DCT-II along i -> slot P_T.
 template <int MODE>
-__global__ void __launch_bounds__(256) dct_rows_fwd_kernel(const SweepArgs a, const DctPlan p, int in,
+__global__ void __launch_bounds__(256) dct_rows_fwd_kernel(const SweepArgs a, const DctPlan g, int in,
                                                            int R, int check_done) {
     const int b = blockIdx.y;
     if (check_done && *(volatile int*)&a.ctl[b].done) return;
+    DctPlan p;
     double *P, *Q, *X;
-    dct_smem(p, R, P, Q, X);
+    dct_smem(g, R, p, P, Q, X);
     const int m = p.m, j0 = blockIdx.x * R;
     const Layout L = a.L;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -440,13 +506,14 @@ __global__ void __launch_bounds__(256) dct_rows_fwd_kernel(const SweepArgs a, co
 
 // Columns k1 = c0 .. c0+Wc-1 of P_T: DCT-II along j, spectral divide
 // (poisson.cpp:84-89), DCT-III along j, back to P_T.
-__global__ void __launch_bounds__(256) dct_cols_kernel(const SweepArgs a, const DctPlan p,
+__global__ void __launch_bounds__(256) dct_cols_kernel(const SweepArgs a, const DctPlan g,
                                                        const double* __restrict__ lambda, int Wc,
                                                        int check_done) {
     const int b = blockIdx.y;
     if (check_done && *(volatile int*)&a.ctl[b].done) return;
+    DctPlan p;
     double *P, *Q, *X;
-    dct_smem(p, Wc, P, Q, X);
+    dct_smem(g, Wc, p, P, Q, X);
     const int m = p.m, c0 = blockIdx.x * Wc;
     const Layout L = a.L;
     double* T = pslot_w(a, b, P_T);
@@ -475,13 +542,14 @@ __global__ void __launch_bounds__(256) dct_cols_kernel(const SweepArgs a, const 
 // MODE 0: psi -> P_PSI.  MODE 1 (Q = conjugate norm): the PDHG post step on
 // these rows (pdhg_post_kernel's arithmetic) with psi from shared memory.
 template <int MODE, int QN>
-__global__ void __launch_bounds__(256) dct_rows_inv_kernel(const SweepArgs a, const DctPlan p, int R,
+__global__ void __launch_bounds__(256) dct_rows_inv_kernel(const SweepArgs a, const DctPlan g, int R,
                                                            double scale, int check_done) {
     const int b = blockIdx.y;
     if (check_done && *(volatile int*)&a.ctl[b].done) return;
     const int NV = MODE ? R + 1 : R;
+    DctPlan p;
     double *P, *Q, *X;
-    dct_smem(p, NV, P, Q, X);
+    dct_smem(g, NV, p, P, Q, X);
     const int m = p.m, j0 = blockIdx.x * R;
     const Layout L = a.L;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;

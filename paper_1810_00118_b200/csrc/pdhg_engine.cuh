@@ -132,33 +132,15 @@ DctPlan dct_plan(w1mg_ctx* c, int m) {
         for (int t = 0; t < N1; ++t) idxA[(size_t)n2 * N1 + t] = (short)pos((int)(((long)N2 * t + (long)N1 * n2) % m));
     for (int k = 0; k < m; ++k)
         if (k % N1 < p.H1) crt[(size_t)(k % N2) * p.H1 + k % N1] = (short)k;
-    const int r1 = p.T1 + p.E1, r2 = p.T2 + p.E2;
-    std::vector<double> c1((size_t)std::max(r1, 1) * p.H1p, 0.0), s1((size_t)std::max(p.T1, 1) * p.H1p, 0.0);
-    std::vector<double> cT(c1.size(), 0.0), sT(s1.size(), 0.0);
-    std::vector<double> c2((size_t)std::max(r2, 1) * p.H2p, 0.0), s2((size_t)std::max(p.T2, 1) * p.H2p, 0.0);
-    for (int t = 0; t < r1; ++t)
-        for (int k = 0; k < p.H1; ++k) {
-            const size_t e = (size_t)t * p.H1p + k;
-            if (t < p.T1) {
-                c1[e] = cosN((long)(t + 1) * k, N1);
-                s1[e] = -sinN((long)(t + 1) * k, N1);
-                cT[e] = cosN((long)(t + 1) * k, N1);
-                sT[e] = sinN((long)(t + 1) * k, N1);
-            } else {  // Nyquist row (even N1)
-                c1[e] = (k & 1) ? -1.0 : 1.0;
-                cT[e] = (k & 1) ? -0.5 : 0.5;
-            }
-        }
-    for (int t = 0; t < r2; ++t)
-        for (int k = 0; k < p.H2; ++k) {
-            const size_t e = (size_t)t * p.H2p + k;
-            if (t < p.T2) {
-                c2[e] = cosN((long)(t + 1) * k, N2);
-                s2[e] = sinN((long)(t + 1) * k, N2);
-            } else {
-                c2[e] = (k & 1) ? -1.0 : 1.0;
-            }
-        }
+    std::vector<double> tw1(2 * (size_t)N1), tw2(2 * (size_t)N2);
+    for (int j = 0; j < N1; ++j) {
+        tw1[j] = cosN(j, N1);
+        tw1[N1 + j] = sinN(j, N1);
+    }
+    for (int j = 0; j < N2; ++j) {
+        tw2[j] = cosN(j, N2);
+        tw2[N2 + j] = sinN(j, N2);
+    }
     std::vector<double> mk(2 * (size_t)m);
     for (int k = 0; k < m; ++k) {  // pi k / 2m = 2 pi k / 4m
         mk[2 * k] = cosN(k, 4L * m);
@@ -177,12 +159,8 @@ DctPlan dct_plan(w1mg_ctx* c, int m) {
     };
     p.idxA = up_s("idxA", idxA);
     p.crt = up_s("crt", crt);
-    p.c1 = up_d("c1", c1);
-    p.s1 = up_d("s1", s1);
-    p.c2 = up_d("c2", c2);
-    p.s2 = up_d("s2", s2);
-    p.cT = up_d("cT", cT);
-    p.sT = up_d("sT", sT);
+    p.tw1 = up_d("tw1", tw1);
+    p.tw2 = up_d("tw2", tw2);
     p.mk = up_d("mk", mk);
     c->dct[m] = p;
     return p;
@@ -206,14 +184,17 @@ void dct_kernel_attrs() {
     done |= 1ull << (dev & 63);
 }
 
-// Vectors per CTA of a DCT launch: the most (<= 16) that still give about two
-// CTAs per SM over the batch and fit the shared-memory budget (`extra`
-// vectors are transformed on top, e.g. the post step's halo row).
+// Vectors per CTA of a DCT launch: the fewest (a power of two <= 16) whose
+// grid still runs in ONE wave of two CTAs per SM -- a CTA's transform is a
+// chain of dependent shared-memory phases, so the launch takes one CTA
+// latency per wave -- within the shared-memory budget (`extra` vectors are
+// transformed on top, e.g. the post step's halo row).
 int dct_vectors_per_cta(const DctPlan& p, int B, int num_sms, int extra) {
-    int R = 16;
-    while (R > 1 && ((long)((p.m + R - 1) / R) * B < 2L * num_sms ||
-                     dct_smem_bytes(p, R + extra) > kDctSmemMax))
-        R >>= 1;
+    int R = 1;
+    while (R < 16 && (long)((p.m + R - 1) / R) * B > 2L * num_sms &&
+           dct_smem_bytes(p, 2 * R + extra) <= kDctSmemMax)
+        R <<= 1;
+    while (R > 1 && dct_smem_bytes(p, R + extra) > kDctSmemMax) R >>= 1;
     if (dct_smem_bytes(p, R + extra) > kDctSmemMax)
         fail(W1MG_EINVAL, "Poisson solve: grid too large for the shared-memory DCT");
     return R;

@@ -4,6 +4,10 @@ benchmark sweeps.
   * ``all_pairs`` -- the paper's all-vs-all timing (45 pairs of 10 images,
     PAPER.md:1281) on the batched config-4 engine: pairs of equal size and
     (p, tolerance) go to the device as ONE batch (``w1mg.ml_run_batch``).
+  * ``solve_pairs`` -- the batched heterogeneous driver: any list of image
+    pairs with mixed sizes, norms, level counts and tolerances; pairs that
+    share (size, L, p, tolerance rule) form one device batch, results come
+    back in input order (SPEC.md:497 ``bench`` over mixed configurations).
   * ``sweep`` -- iteration / time sweeps over algorithms, level counts and
     the Eq. 16 exponent alpha (the shape of paper Tables 4-6).
   * ``validate_assumptions`` -- Table 3: per-level
@@ -58,6 +62,59 @@ def _sources(img_a: np.ndarray, img_b: np.ndarray, levels: int) -> list:
 def _src(rho: np.ndarray) -> SourceField:
     n = rho.shape[0] - 1
     return SourceField(ScalarField(GridSpec(n), rho))
+
+
+# ------------------------------------------------- heterogeneous batches
+@dataclass
+class PairJob:
+    """One density pair of a heterogeneous batch: two square m x m cell
+    images, the cascade depth (None: SPEC.md:359 default log2 m - 3), the
+    norm, and the tolerance rule (rel_tol * R_cold,l, or the Eq. 16 schedule
+    of eps_finest with exponent alpha when eps_finest is given)."""
+    a: np.ndarray
+    b: np.ndarray
+    levels: Optional[int] = None
+    p: PNorm = PNorm.p2
+    rel_tol: float = 1e-5
+    eps_finest: Optional[float] = None
+    alpha: float = -1.0
+
+
+def solve_pairs(jobs: Sequence[PairJob], max_iters: int = 5_000_000) -> list:
+    """Solve every job by the cascadic CP solver on the batched config-4
+    engine.  Jobs are grouped by (m, L, p, tolerance rule); each group is ONE
+    device batch (w1mg.ml_run_batch), so a mixed workload costs one batched
+    cascade per distinct configuration instead of one launch sequence per
+    pair.  Returns one dict per job, in input order."""
+    groups: dict = {}
+    for k, job in enumerate(jobs):
+        a = np.ascontiguousarray(job.a, dtype=np.float64)
+        b = np.ascontiguousarray(job.b, dtype=np.float64)
+        if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape != b.shape:
+            raise ValueError(f"solve_pairs: job {k} needs two square images of one size")
+        m = a.shape[0]
+        L = job.levels if job.levels is not None else w1mg.default_levels(m)
+        if L < 1 or m % (1 << (L - 1)):
+            raise ValueError(f"solve_pairs: job {k}: N={m} not divisible by 2^(L-1) for L={L}")
+        rule = ("eps", float(job.eps_finest), float(job.alpha)) if job.eps_finest is not None \
+            else ("rel", float(job.rel_tol))
+        groups.setdefault((m, L, int(job.p), rule), []).append((k, a, b))
+    out: list = [None] * len(jobs)
+    for (m, L, p, rule), members in sorted(groups.items(), key=lambda kv: (kv[0][0], kv[0][1], kv[0][2], str(kv[0][3]))):
+        A = np.stack([a for _, a, _ in members])
+        Bi = np.stack([b for _, _, b in members])
+        eps = w1mg.make_schedule(m, L, rule[1], rule[2]) if rule[0] == "eps" else None
+        t0 = time.perf_counter()
+        dist, dual, iters, conv = w1mg.ml_run_batch(A, Bi, L, p=PNorm(p),
+                                                    rel_tol=rule[1] if rule[0] == "rel" else 1e-5,
+                                                    eps=eps, max_iters=max_iters)
+        secs = time.perf_counter() - t0
+        for q, (k, _, _) in enumerate(members):
+            out[k] = {"job": k, "n": m, "levels": L, "p": p, "distance": float(dist[q]),
+                      "dual_value": float(dual[q]), "iters": [int(x) for x in iters[q]],
+                      "converged": bool(conv[q]), "batch_pairs": len(members),
+                      "batch_seconds": secs}
+    return out
 
 
 # ---------------------------------------------------------- all-vs-all

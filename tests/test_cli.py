@@ -42,17 +42,26 @@ def test_bad_inputs_are_format_errors(tmp_path):
     assert cli.main(["nonsense"]) == cli.EXIT_USAGE
 
 
-def test_discretize_matches_source_rule_and_unit_mass():
-    """At N = M the bilinear resampling equals the cell->node mean used by
-    the device restriction; mass is 1 in the L1_h sense."""
-    img = np.random.default_rng(0).random((16, 16)) + 0.1
-    d = cli.discretize(img, 16)
+def test_discretize_spec_examples():
+    """pixel centres on [0,1]^2 (an M x M image resampled
+    onto M nodes is the image itself, scaled), unit mass in the L1_h sense,
+    constant image -> constant field, checkerboard 64 -> N = 32 mass 1 to 1e-12,
+    corner pixels on corner nodes."""
+    img = np.random.default_rng(0).random((17, 17)) + 0.1
+    d = cli.discretize(img, 16)  # 17 nodes per side = the pixel lattice
     h = 1.0 / 16
     assert abs(d.sum() * h * h - 1.0) <= 1e-12
-    nodes = instances.image_to_nodes(img)
-    np.testing.assert_allclose(d / d.sum(), nodes / nodes.sum(), rtol=1e-12)
-    const = cli.discretize(np.ones((8, 8)), 32)  # SPEC.md:474: constant image -> constant
+    np.testing.assert_allclose(d / d.sum(), img / img.sum(), rtol=1e-12)
+    two = np.array([[1.0, 2.0], [3.0, 4.0]])
+    np.testing.assert_allclose(cli.discretize(two, 1), two / 10.0, rtol=1e-15)
+    const = cli.discretize(np.ones((8, 8)), 32)
     assert np.allclose(const, const[0, 0])
+    cb = (np.indices((64, 64)).sum(axis=0) % 2).astype(float)
+    assert abs(cli.discretize(cb, 32).sum() / 32 ** 2 - 1.0) <= 1e-12
+    dirac = np.zeros((64, 64))
+    dirac[0, 63] = 1.0
+    dd = cli.discretize(dirac, 64)
+    assert np.unravel_index(dd.argmax(), dd.shape) == (0, 64)
 
 
 def test_field_csv_roundtrip_bit_exact(tmp_path):
@@ -76,22 +85,25 @@ def test_gen_deterministic(tmp_path):
 
 
 @pytest.mark.gpu
-def test_cli_solve_dirac_pair(tmp_path):
-    """dirac_pair corners, p = 1 -> distance 1 +- 1e-3."""
+@pytest.mark.parametrize("p", ["1", "2", "inf"])
+def test_cli_solve_dirac_pair(tmp_path, p):
+    """SPEC.md:502 (and acceptance 2): dirac_pair corners ->
+    distance 1 +- 1e-3.  The corner pixels land on the corner nodes
+    (SPEC.md:468); the bilinear weight 1/n that leaks to the next node inward
+    moves the transport length by ~2/n^2."""
+    n = 64
     a, b = tmp_path / "a.csv", tmp_path / "b.csv"
-    assert cli.main(["gen", "--kind", "dirac_pair", "--n", "16", "--out-a", str(a),
+    assert cli.main(["gen", "--kind", "dirac_pair", "--n", str(n), "--out-a", str(a),
                      "--out-b", str(b)]) == 0
     out = tmp_path / "r.json"
-    rc = cli.main(["solve", "--a", str(a), "--b", str(b), "--p", "1", "--algo", "pdhg",
+    rc = cli.main(["solve", "--a", str(a), "--b", str(b), "--p", p, "--algo", "pdhg",
                    "--tol", "1e-10", "--out", str(out), "--export-flux", str(tmp_path / "f.csv"),
                    "--export-potential", str(tmp_path / "p.csv")])
     rep = json.loads(out.read_text())
     assert rc == 0 and rep["converged"]
-    # the images' corner pixels sit half a pixel in: the node-resampled masses
-    # are 15/16 apart plus the bilinear spread; distance is close to 1
-    assert abs(rep["distance"] - 1.0) <= 0.1
+    assert abs(rep["distance"] - 1.0) <= 1e-3
     f = cli.read_field_csv(str(tmp_path / "f.csv"))
-    assert f["x_edges"].shape == (17, 16)
+    assert f["x_edges"].shape == (n + 1, n)
 
 
 @pytest.mark.gpu
