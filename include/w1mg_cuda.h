@@ -275,19 +275,19 @@ int w1mg_ml_slab_cp_run(w1mg_ctx* ctx, w1mg_slab_comm* comm, int nslabs, int n_f
 
 /* --------------------------------------------------------------- probes */
 /* Select the engine of the fused sweep for subsequent launches in this
- * process: 0 = register-pipelined LDG, 1 = one-sweep TMA bulk-copy ring,
- * 2 = two-sweep (temporally blocked) TMA ring, 3 = auto (default: two-sweep
- * for n >= 96, one-sweep below), 4 = two-sweep with two column sets per lane.
- * Also W1MG_SWEEP=ldg|tma|tma2|auto|tma2w.  Results are bit-identical across
+ * process: 1 = one-sweep TMA bulk-copy ring, 2 = two-sweep (temporally
+ * blocked) bulk-copy ring, 3 = auto (default: three sweeps per pass on batched
+ * levels n >= 384 and one-pair 192..384, two sweeps for other n >= 96, one
+ * below; tensor-map rings), 5 = two-sweep tensor-map ring, 6 = three-sweep
+ * tensor-map ring.  W1MG_EINVAL for 0 and 4 (engines removed).  Also
+ * W1MG_SWEEP=tma|tma2|auto|tma2t|tma3.  Results are bit-identical across
  * engines. */
 int w1mg_set_sweep_engine(int engine);
 /* Level-resident engines (whole level in one launch, state in shared memory):
  * 1 = auto (default: thread-block-cluster engine for small batches with
  * n <= 128, one CTA per pair for n <= 64), 2 = one-CTA engine only,
- * 3 = cluster engine wherever it fits (n <= 256), 4 = cooperative-grid engine
- * for every one-pair level (L2-resident, one launch per level; slower than
- * streaming as measured, kept for A/B), 0 = off (streaming sweeps only).
- * Also W1MG_RESIDENT=0..4. */
+ * 3 = cluster engine wherever it fits (n <= 256), 0 = off (streaming sweeps
+ * only); W1MG_EINVAL otherwise.  Also W1MG_RESIDENT=0..3. */
 int w1mg_set_resident_engine(int on);
 /* Tail compaction of batched levels (1 = on, default): once at most half of
  * the pairs still run, sweep grids span only the running pairs.  Also
@@ -301,7 +301,10 @@ int w1mg_set_pdhg_small(int mode);
  * environment variable read at context creation): "pdhg_small" (0-2),
  * "cluster_pick" (0/1), "compact" (0/1), "compact_step" (>= 1),
  * "warps_per_sm" (strip target, default 32), "tmap_nw" (2/4/8, 0 = auto),
- * "tile" (0-2), "tile_min", "tile_max", "tile_grid".
+ * "pdl" (0/1), "fast" (0 = numerics bit-identical to the reference
+ * (default); 1 = tolerance mode for p = 2 in the streaming sweep kernels:
+ * FMA-contracted node update and an rsqrt shrink, fields within 1e-9 of the
+ * reference at fixed sweeps; W1MG_FAST).
  * W1MG_EINVAL for an unknown name or value. */
 int w1mg_set_option(const char* name, long value);
 /* Times the fused sweep kernel alone: `iters` sweeps over B pairs of an

@@ -33,11 +33,7 @@
 #include "ref_kernels.cuh"
 #include "cp2_kernels.cuh"
 #include "cluster_kernels.cuh"
-#include "cp2w_kernels.cuh"
-#include "grid_kernels.cuh"
-#include "tile_kernels.cuh"
 #include "cp3_kernels.cuh"
-#include "tile2_kernels.cuh"
 #include "dct_kernels.cuh"
 
 using namespace w1mg_dev;
@@ -63,10 +59,8 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
         if (major < 10) fail(W1MG_ECUDA, "this build targets sm_100a (B200)");
         if (const char* v = std::getenv("W1MG_SWEEP"))
-            g_sweep_variant = (std::string(v) == "ldg") ? kLdg
-                              : (std::string(v) == "tma") ? kTma
+            g_sweep_variant = (std::string(v) == "tma") ? kTma
                               : (std::string(v) == "tma2") ? kTma2
-                              : (std::string(v) == "tma2w") ? kTma2W
                               : (std::string(v) == "tma2t") ? kTma2T
                               : (std::string(v) == "tma3")  ? kTma3
                                                             : kAuto;
@@ -77,11 +71,6 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_WARPS_PER_SM")) g_warps_per_sm = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_PDL")) g_pdl = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_FAST")) g_fast = std::atoi(v) != 0;
-        if (const char* v = std::getenv("W1MG_TILE")) g_tile = std::atoi(v);
-        if (const char* v = std::getenv("W1MG_TILE_MIN")) g_tile_min = std::max(1, std::atoi(v));
-        if (const char* v = std::getenv("W1MG_TILE_MAX")) g_tile_max = std::max(1, std::atoi(v));
-        if (const char* v = std::getenv("W1MG_TILE_GRID")) g_tile_grid = std::max(0, std::atoi(v));
-        if (const char* v = std::getenv("W1MG_TILE_DEPTH")) g_tile_depth = std::atoi(v) == 2 ? 2 : 1;
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
             const int w = std::atoi(v);
@@ -594,13 +583,14 @@ int w1mg_interpolate_flux(w1mg_ctx* c, int nc, const double* cx, const double* c
 // Kernel probe: `iters` fused sweeps on B pairs of an n-cell level with the
 // stop rule disabled, after `warm` untimed sweeps; returns ms per sweep.
 int w1mg_set_sweep_engine(int engine) {
-    if (engine < kLdg || engine > kTma3) return W1MG_EINVAL;
+    if (engine < kTma || engine > kTma3 || engine == 4) return W1MG_EINVAL;
     g_sweep_variant = engine;
     return W1MG_OK;
 }
 
 int w1mg_set_resident_engine(int on) {
-    g_resident = (on >= 0 && on <= 4) ? on : 1;
+    if (on < 0 || on > 3) return W1MG_EINVAL;
+    g_resident = on;
     return W1MG_OK;
 }
 
@@ -616,11 +606,6 @@ int w1mg_set_option(const char* name, long value) {
     else if (k == "pdl" && (v == 0 || v == 1)) g_pdl = v;
     else if (k == "fast" && (v == 0 || v == 1)) g_fast = v;
     else if (k == "tmap_nw" && (v == 0 || v == 2 || v == 4 || v == 8)) g_tmap_nw = v;
-    else if (k == "tile" && v >= 0 && v <= 2) g_tile = v;
-    else if (k == "tile_min" && v >= 1) g_tile_min = v;
-    else if (k == "tile_max" && v >= 1) g_tile_max = v;
-    else if (k == "tile_grid" && v >= 0) g_tile_grid = v;
-    else if (k == "tile_depth" && (v == 1 || v == 2)) g_tile_depth = v;
     else return W1MG_EINVAL;
     return W1MG_OK;
 }

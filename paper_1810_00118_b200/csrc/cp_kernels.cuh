@@ -400,59 +400,6 @@ __device__ __forceinline__ void finish_sweep(const SweepArgs& a, int pair, int p
     }
 }
 
-// ------------------------------------------------------------ kLdg engine
-template <int PN>
-__global__ void __launch_bounds__(kSweepWarps * 32)
-cp_sweep_kernel(const SweepArgs a, const int parity_arg) {
-    const int pair = sweep_pair(a);
-    int parity;
-    if (pair < 0 || !sweep_gate(a.ctl + pair, parity_arg, parity)) return;
-    const int lane = threadIdx.x & 31;
-    const int tile = blockIdx.x * kSweepWarps + (threadIdx.x >> 5);
-    double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
-
-    if (tile < a.ntiles) {
-        const Strip s = make_strip(a, pair, parity, tile, lane);
-        const Layout L = a.L;
-        const int n = L.n;
-        const int P = L.pitch;
-        double uyb, dyb;
-        below_row<PN>(a, s, lane, uyb, dyb);
-
-        long o = L.at(s.i, s.j0);
-        double pc = s.in ? __ldg(s.phr + o) : 0.0;
-        double pr = __shfl_down_sync(0xffffffffu, pc, 1);
-        if (lane == 31) pr = s.hx ? __ldg(s.phr + o + 1) : 0.0;
-
-        const bool l31 = (lane == 31) && s.hx;
-        double n_pu, n_pur, n_mx, n_my, n_r;
-        {
-            const bool hy = s.in && (s.j0 < n);
-            n_pu = hy ? __ldg(s.phr + o + P) : 0.0;
-            n_pur = (l31 && s.j0 < n) ? __ldg(s.phr + o + P + 1) : 0.0;
-            n_mx = s.hx ? __ldg(s.mxr + o) : 0.0;
-            n_my = hy ? __ldg(s.myr + o) : 0.0;
-            n_r = s.in ? __ldg(s.rho + o) : 0.0;
-        }
-        for (int j = s.j0; j < s.j1; ++j, o += P) {
-            const double pu = n_pu, pur = n_pur, mxo = n_mx, myo = n_my, r = n_r;
-            if (j + 1 < s.j1) {  // loads of row j+1 overlap row j's math
-                const long q = o + P;
-                const bool hy1 = s.in && (j + 1 < n);
-                n_pu = hy1 ? __ldg(s.phr + q + P) : 0.0;
-                n_pur = (l31 && j + 1 < n) ? __ldg(s.phr + q + P + 1) : 0.0;
-                n_mx = s.hx ? __ldg(s.mxr + q) : 0.0;
-                n_my = hy1 ? __ldg(s.myr + q) : 0.0;
-                n_r = s.in ? __ldg(s.rho + q) : 0.0;
-            }
-            row_update<PN>(a, s, j, o, pc, pr, pu, mxo, myo, r, uyb, dyb, s_dm2, s_dp2, s_cr);
-            double nr = __shfl_down_sync(0xffffffffu, pu, 1);
-            pr = (lane == 31) ? pur : nr;
-            pc = pu;
-        }
-    }
-    finish_sweep(a, pair, parity, blockIdx.x, gridDim.x, s_dm2, s_dp2, s_cr);
-}
 
 // ------------------------------------------------------------ kTma engine
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -23,8 +23,6 @@ struct Level {
     dim3 grid;
     SweepArgs args2{};  // two-sweep engine
     dim3 grid2;
-    SweepArgs args2w{};  // two-sweep engine, two column sets per lane
-    dim3 grid2w;
     dim3 grid2t;  // two-sweep tensor-map engine (args2 geometry, tmap_nw-warp blocks)
     SweepArgs args3{};  // three-sweep tensor-map engine
     dim3 grid3;
@@ -104,10 +102,8 @@ void set_geometry(Level& lv, int pairs, int num_sms) {
     const long target = (long)num_sms * g_warps_per_sm;
     strip_geometry(lv.args, kOwn, pairs, target, 2);       // 31 owned columns per warp
     strip_geometry(lv.args2, kOwn2, pairs, target, 4);     // two-sweep: 29 per warp
-    strip_geometry(lv.args2w, kOwnW, pairs, target / 2, 4);  // wide: 61 per warp, 4-warp blocks
     lv.grid = dim3((lv.args.ntiles + kSweepWarps - 1) / kSweepWarps, pairs, 1);
     lv.grid2 = dim3((lv.args2.ntiles + kSweepWarps - 1) / kSweepWarps, pairs, 1);
-    lv.grid2w = dim3((lv.args2w.ntiles + kWarpsW - 1) / kWarpsW, pairs, 1);
     strip_geometry(lv.args3, kOwn3, pairs, target, 4);     // three-sweep: 27 per warp
     lv.grid3 = dim3((lv.args3.ntiles + kWarps3 - 1) / kWarps3, pairs, 1);
     lv.tmap_nw = g_tmap_nw ? g_tmap_nw : ((pairs == 1 && lv.n >= 384 && lv.n <= 640) ? 8 : kWarpsT);
@@ -160,7 +156,6 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     a.act = nullptr;
     a.nact = nullptr;
     lv.args2 = a;
-    lv.args2w = a;
     lv.args3 = a;
     set_geometry(lv, B, c->num_sms);
     // a compacted launch over fewer pairs uses shorter strips (more tiles per
@@ -170,19 +165,17 @@ Level make_level(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, d
     lv.partial = c->get<double>(
         tag + ".partial",
         (size_t)B * std::max<size_t>({(size_t)one.args.ntiles * 3, (size_t)one.args2.ntiles * 6,
-                                      (size_t)one.args2w.ntiles * 6, (size_t)lv.args.ntiles * 3,
-                                      (size_t)lv.args2.ntiles * 6, (size_t)lv.args2w.ntiles * 6,
+                                      (size_t)lv.args.ntiles * 3, (size_t)lv.args2.ntiles * 6,
                                       (size_t)one.args3.ntiles * 9, (size_t)lv.args3.ntiles * 9}));
     a.partial = lv.partial;
     lv.args2.partial = lv.partial;
-    lv.args2w.partial = lv.partial;
     lv.args3.partial = lv.partial;
     if (!lv.slab) {  // two-level residual reduction of the two-sweep kernels
         const int gs = (one.args2.ntiles + kRedGroup - 1) / kRedGroup + 1;
         double* gp = c->get<double>(tag + ".gpart", (size_t)B * gs * 6);
         unsigned* gt = c->get<unsigned>(tag + ".gticket", (size_t)B * gs);
         CK(cudaMemsetAsync(gt, 0, sizeof(unsigned) * B * gs, c->stream));
-        for (SweepArgs* x : {&lv.args2, &lv.args2w}) {
+        for (SweepArgs* x : {&lv.args2}) {
             x->gpart = gp;
             x->gticket = gt;
             x->gstride = gs;
@@ -276,7 +269,8 @@ constexpr int kAuto = 3;
 constexpr int kTma3 = 6;
 int g_sweep_variant = kAuto;
 
-constexpr int kTma2W = 4;  // two-sweep, two column sets per lane (cp2w_kernels.cuh)
+// engine ids 0 (register-pipelined LDG) and 4 (two column sets per lane) were
+// measured slower than the tensor-map engines and removed
 constexpr int kTma2T = 5;  // two-sweep, ring fed by one tensor-map box per row
 
 // programmatic dependent launch for the two-sweep kernel (option "pdl"):
@@ -345,7 +339,7 @@ void launch_tmap(const Level& lv, int pn, int parity, cudaStream_t s) {
 
 bool two_sweep(const Level& lv) {
     if (lv.slab) return false;  // slabs exchange a one-row halo per sweep
-    return g_sweep_variant == kTma2 || g_sweep_variant == kTma2W || g_sweep_variant == kTma2T ||
+    return g_sweep_variant == kTma2 || g_sweep_variant == kTma2T ||
            (g_sweep_variant == kAuto && lv.n >= 96);
 }
 // auto picks it for a one-pair level of 192..384 (one 256^2 pair: 22.4 ->
@@ -392,15 +386,6 @@ void launch_sweep2(const Level& lv, int pn, int parity, cudaStream_t s) {
         }
         return;
     }
-    if (g_sweep_variant == kTma2W) {
-        dim3 blk(kWarpsW * 32);
-        switch (pn) {
-            case 0: cp_sweep2w_tma_kernel<0><<<lv.grid2w, blk, kTmaSmemW, s>>>(lv.args2w, parity); break;
-            case 1: cp_sweep2w_tma_kernel<1><<<lv.grid2w, blk, kTmaSmemW, s>>>(lv.args2w, parity); break;
-            default: cp_sweep2w_tma_kernel<2><<<lv.grid2w, blk, kTmaSmemW, s>>>(lv.args2w, parity); break;
-        }
-        return;
-    }
     dim3 blk(kSweepWarps * 32);
     switch (pn) {
         case 0: cp_sweep2_tma_kernel<0><<<lv.grid2, blk, kTmaSmem, s>>>(lv.args2, parity); break;
@@ -411,19 +396,11 @@ void launch_sweep2(const Level& lv, int pn, int parity, cudaStream_t s) {
 
 void launch_sweep(const Level& lv, int pn, int parity, cudaStream_t s) {
     dim3 blk(kSweepWarps * 32);
-    if (g_sweep_variant != kLdg) {
-        switch (stream_pn(pn)) {
-            case 0: cp_sweep_tma_kernel<0><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
-            case 1: cp_sweep_tma_kernel<1><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
-            case 3: cp_sweep_tma_kernel<3><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
-            default: cp_sweep_tma_kernel<2><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
-        }
-        return;
-    }
-    switch (pn) {
-        case 0: cp_sweep_kernel<0><<<lv.grid, blk, 0, s>>>(lv.args, parity); break;
-        case 1: cp_sweep_kernel<1><<<lv.grid, blk, 0, s>>>(lv.args, parity); break;
-        default: cp_sweep_kernel<2><<<lv.grid, blk, 0, s>>>(lv.args, parity); break;
+    switch (stream_pn(pn)) {
+        case 0: cp_sweep_tma_kernel<0><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
+        case 1: cp_sweep_tma_kernel<1><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
+        case 3: cp_sweep_tma_kernel<3><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
+        default: cp_sweep_tma_kernel<2><<<lv.grid, blk, kTmaSmem, s>>>(lv.args, parity); break;
     }
 }
 
@@ -434,7 +411,7 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
     std::string key(reinterpret_cast<const char*>(&lv.args), sizeof(SweepArgs));
     key += std::to_string(pn) + ":" + std::to_string(K) + ":" + std::to_string(lv.grid.x) + ":" +
            std::to_string(lv.grid.y) + ":" + std::to_string(lv.grid2.x) + ":" +
-           std::to_string(lv.grid2w.x) + ":" + std::to_string(lv.grid2t.x) + ":" +
+           std::to_string(lv.grid2t.x) + ":" +
            std::to_string(lv.grid3.x) + ":B" +
            std::to_string(lv.B) + ":v" +
            std::to_string(g_sweep_variant) + ":nw" + std::to_string(lv.tmap_nw) + ":pdl" +
@@ -471,7 +448,7 @@ int g_compact_step = 1 << 30;  // bucket granularity (W1MG_COMPACT_STEP; default
 Level compacted(const Level& lv, int pairs, int num_sms) {
     Level b = lv;
     set_geometry(b, pairs, num_sms);
-    for (SweepArgs* a : {&b.args, &b.args2, &b.args2w, &b.args3}) {
+    for (SweepArgs* a : {&b.args, &b.args2, &b.args3}) {
         a->act = lv.act;
         a->nact = lv.nact;
     }
@@ -482,40 +459,12 @@ Level compacted(const Level& lv, int pairs, int num_sms) {
 // (device-side, solver_cp.cpp:128-136 semantics).  The host only watches a
 // done-counter one graph behind, so it never stalls the GPU per iteration.
 // level-resident engines (W1MG_RESIDENT): 1 = auto (cluster engine for small
-// batches with n <= 128, single-CTA engine for n <= 64 otherwise, cooperative
-// grid engine for one pair on an L2-sized level; default), 2 = single-CTA
-// engine only, 3 = cluster engine wherever it fits (n <= 256), 4 = grid engine
-// for every one-pair level, 0 = off (streaming sweeps only)
+// batches with n <= 128, single-CTA engine for n <= 64 otherwise;
+// default), 2 = single-CTA engine only, 3 = cluster engine wherever it fits
+// (n <= 256), 0 = off (streaming sweeps only).  (A cooperative-grid engine and
+// level-persistent shared-memory tile engines were measured slower than the
+// streaming launches for one pair and removed.)
 int g_resident = 1;
-
-// Cooperative-grid engine (grid_kernels.cuh): one pair, whole level in one
-// launch, state in L2.  Only on request (W1MG_RESIDENT=4): measured per sweep
-// it costs 7.2 us at 32^2, 7.6 us at 256^2 and 9.7 us at 512^2 (grid barrier
-// + L2 round trips of the strip ramps), vs 6.0 / 7.9 us for the streaming
-// two-sweep launches of one pair, so auto never picks it.
-bool grid_ok(const w1mg_ctx* c, const Level& lv) {
-    (void)c;
-    return g_resident == 4 && !lv.slab && lv.B == 1;
-}
-
-template <int PN>
-void launch_grid_pn(w1mg_ctx* c, const Level& lv) {
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cp_grid_kernel<PN>, kGridWarps * 32, 0));
-    if (occ < 1) fail(W1MG_ECUDA, "grid engine: kernel does not fit an SM");
-    const int G = c->num_sms * std::min(occ, 2);
-    SweepArgs ag = lv.args;
-    const long TW = (long)G * kGridWarps;
-    const int nrows = ag.jhi - ag.jlo;
-    const long per_col = std::max(1L, TW / ag.ncx);
-    ag.H = std::max(2, (int)((nrows + per_col - 1) / per_col));
-    ag.nsy = (nrows + ag.H - 1) / ag.H;
-    ag.ntiles = ag.ncx * ag.nsy;
-    double* gp = c->get<double>("grid.partial", (size_t)2 * G * 3);
-    void* args[] = {(void*)&ag, (void*)&gp};
-    CK(cudaLaunchCooperativeKernel((const void*)cp_grid_kernel<PN>, dim3(G), dim3(kGridWarps * 32),
-                                   args, 0, c->stream));
-}
 
 template <int PN>
 void launch_resident_pn(const Level& lv, cudaStream_t s) {
@@ -615,107 +564,8 @@ bool launch_cluster_pn(const Level& lv, int C, cudaStream_t s) {
     return true;
 }
 
-// Level-persistent tile engine (tile_kernels.cuh): one pair, whole level in
-// one cooperative launch, TR x TC tiles in shared memory (one CTA per SM)
-// plus a controller CTA.  0 = off, 1 = auto (one-pair levels with
-// g_tile_min <= n <= g_tile_max while the resident engines are on auto),
-// 2 = every one-pair level that fits.
-int g_tile = 0;
-int g_tile_min = 96;
-int g_tile_max = 640;
-int g_tile_grid = 0;  // tiles per side (0: floor(sqrt(SMs - 1)))
-int g_tile_depth = 1;  // sweeps per halo exchange: 1 (tile_kernels.cuh) or 2 (tile2_kernels.cuh)
-
-struct TileGeom {
-    int TR = 0, TC = 0, LW = 0, LH = 0;
-};
-
-bool tile_geometry(const w1mg_ctx* c, const Level& lv, TileGeom& g) {
-    if (!g_tile || lv.slab || lv.B != 1) return false;
-    if (g_tile == 1 && (g_resident != 1 || lv.n < g_tile_min || lv.n > g_tile_max)) return false;
-    int t = g_tile_grid ? g_tile_grid : (int)std::floor(std::sqrt((double)(c->num_sms - 1)));
-    t = std::min(t, (lv.n + 1) / 4);  // tiles at least 4 nodes wide
-    if (t < 1 || (long)lv.B * (t * t + 1) > c->num_sms) return false;
-    g.TR = g.TC = t;
-    const int ring = g_tile_depth == 2 ? 4 : 2;
-    g.LW = (lv.n + 1 + t - 1) / t + ring;
-    g.LH = g.LW;
-    return (g_tile_depth == 2 ? tile2_smem_bytes(g.LW, g.LH) : tile_smem_bytes(g.LW, g.LH)) <= 200 * 1024;
-}
-
-template <int PN>
-void launch_tile_pn(w1mg_ctx* c, const Level& lv, const TileGeom& g) {
-    const int T = g.TR * g.TC;
-    const size_t B = lv.B;
-    TileArgs t;
-    t.a = lv.args;
-    t.TR = g.TR;
-    t.TC = g.TC;
-    t.LW = g.LW;
-    t.LH = g.LH;
-    const bool two = g_tile_depth == 2;
-    t.ES = g.LW - (two ? 4 : 2);
-    t.LCAP = two ? tile2_list_cap(g.LW, g.LH) : tile_list_cap(g.LW, g.LH);
-    t.edges = c->get<double>("tile.edges", B * 2 * T * (two ? kT2Secs : kTileSecs) * t.ES);
-    t.flags = c->get<unsigned>("tile.flags", B * T * kTileFlagStride);
-    t.part = c->get<double>("tile.part", B * kTileSlots * T * 3);
-    t.cnt = c->get<unsigned>("tile.cnt", B * kTileSlots);
-    t.dec = c->get<double>("tile.dec", B * kTileSlots * 2);
-    t.dseq = c->get<unsigned long long>("tile.dseq", B * kTileSlots);
-    t.err = c->get<int>("tile.err", 1);
-    t.dbg = nullptr;
-    if (std::getenv("W1MG_TILE_DEBUG")) {  // diagnostics: per-step stamps of tile 0
-        t.dbg = c->get<long long>("tile.dbg", (size_t)kTileDbgSteps * kTileDbgPts);
-        CK(cudaMemsetAsync(t.dbg, 0, sizeof(long long) * kTileDbgSteps * kTileDbgPts, c->stream));
-    }
-    CK(cudaMemsetAsync(t.flags, 0, sizeof(unsigned) * B * T * kTileFlagStride, c->stream));
-    CK(cudaMemsetAsync(t.cnt, 0, sizeof(unsigned) * B * kTileSlots, c->stream));
-    CK(cudaMemsetAsync(t.dseq, 0, sizeof(unsigned long long) * B * kTileSlots, c->stream));
-    CK(cudaMemsetAsync(t.err, 0, sizeof(int), c->stream));
-    const int smem = (int)(two ? tile2_smem_bytes(g.LW, g.LH) : tile_smem_bytes(g.LW, g.LH));
-    const void* kfn = two ? (const void*)cp_tile2_kernel<PN> : (const void*)cp_tile_kernel<PN>;
-    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kTileThreads, smem));
-    if ((long)occ * c->num_sms < (long)B * (T + 1))
-        fail(W1MG_ECUDA, "tile engine: the tiles do not fit co-resident");
-    void* args[] = {(void*)&t};
-    CK(cudaLaunchCooperativeKernel(kfn, dim3((unsigned)(B * (T + 1))), dim3(kTileThreads), args, smem,
-                                   c->stream));
-    if (t.dbg) {
-        std::vector<long long> h((size_t)kTileDbgSteps * kTileDbgPts);
-        CK(cudaMemcpyAsync(h.data(), t.dbg, h.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        std::fprintf(stderr, "tile n=%d TRxTC=%dx%d smem=%d\n", lv.n, g.TR, g.TC, smem);
-        for (int q = 0; q < T; ++q) {
-            const long long* r = &h[(size_t)q * kTileDbgPts];
-            // per-step averages of the segments between the kernel's stamps
-            // (depth 1: top, A-int, wait, halo, borders, B-int+post; depth 2:
-            // -, wait, halo, sweep 1, sweep 2, sums+post), steps 8..135 / 4..67
-            const int ns = two ? 64 : 128;
-            std::fprintf(stderr, "tile %3d: seg %lld %lld %lld %lld %lld %lld\n", q, r[0] / ns,
-                         r[1] / ns, r[2] / ns, r[3] / ns, r[4] / ns, r[5] / ns);
-        }
-    }
-}
-
 void run_sweeps(w1mg_ctx* c, const Level& lv, int pn, long max_iters) {
     if (max_iters <= 0) return;
-    if (grid_ok(c, lv)) {  // whole one-pair level in one cooperative launch
-        if (pn == 0) launch_grid_pn<0>(c, lv);
-        else if (pn == 1) launch_grid_pn<1>(c, lv);
-        else launch_grid_pn<2>(c, lv);
-        ++c->launches;
-        return;
-    }
-    TileGeom tg;
-    if (tile_geometry(c, lv, tg)) {  // whole one-pair level in one launch, tiles in shared memory
-        if (pn == 0) launch_tile_pn<0>(c, lv, tg);
-        else if (pn == 1) launch_tile_pn<1>(c, lv, tg);
-        else launch_tile_pn<2>(c, lv, tg);
-        ++c->launches;
-        return;
-    }
     if (lv.has_tmap) mirror_rho(c, lv);
     if (const int C = cluster_size(lv, c->num_sms)) {  // whole level in one cluster launch
         bool ok = (pn == 0)   ? launch_cluster_pn<0>(lv, C, c->stream)

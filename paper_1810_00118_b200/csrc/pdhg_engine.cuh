@@ -30,6 +30,7 @@ struct PLevel {
     const double* lam = nullptr;  // lambda_k, poisson.cpp:28-30
     DctPlan dp{};                 // prime-factor DCT plan (dct_kernels.cuh)
     int rows_f = 1, cols = 1, rows_i = 1;  // vectors per CTA of the three DCT launches
+    int rows_p = 0;  // ... of the fused row DCT-III + post launch (0: does not fit, unfused)
 };
 
 // Dense DCT matrices for m = n+1, built once per size on the host in long
@@ -166,7 +167,7 @@ DctPlan dct_plan(w1mg_ctx* c, int m) {
     return p;
 }
 
-constexpr size_t kDctSmemMax = 200u << 10;
+constexpr size_t kDctSmemMax = 227u << 10;  // the sm_100 per-block opt-in limit
 
 void dct_kernel_attrs() {
     static unsigned long long done = 0;  // per device
@@ -195,9 +196,7 @@ int dct_vectors_per_cta(const DctPlan& p, int B, int num_sms, int extra) {
            dct_smem_bytes(p, 2 * R + extra) <= kDctSmemMax)
         R <<= 1;
     while (R > 1 && dct_smem_bytes(p, R + extra) > kDctSmemMax) R >>= 1;
-    if (dct_smem_bytes(p, R + extra) > kDctSmemMax)
-        fail(W1MG_EINVAL, "Poisson solve: grid too large for the shared-memory DCT");
-    return R;
+    return dct_smem_bytes(p, R + extra) <= kDctSmemMax ? R : 0;
 }
 
 PLevel make_plevel(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, double tau,
@@ -234,7 +233,10 @@ PLevel make_plevel(w1mg_ctx* c, const std::string& tag, int n, int B, double mu,
     lv.dp = dct_plan(c, n + 1);
     lv.rows_f = dct_vectors_per_cta(lv.dp, B, c->num_sms, 0);
     lv.cols = dct_vectors_per_cta(lv.dp, B, c->num_sms, 0);
-    lv.rows_i = dct_vectors_per_cta(lv.dp, B, c->num_sms, 1);
+    lv.rows_i = dct_vectors_per_cta(lv.dp, B, c->num_sms, 0);
+    lv.rows_p = dct_vectors_per_cta(lv.dp, B, c->num_sms, 1);
+    if (!lv.rows_f || !lv.cols || !lv.rows_i)
+        fail(W1MG_EINVAL, "Poisson solve: grid too large for the shared-memory DCT");
     dct_kernel_attrs();
     CK(cudaMemsetAsync(lv.ticket, 0, sizeof(unsigned) * B, c->stream));
     return lv;
@@ -293,12 +295,24 @@ void pdhg_iteration(w1mg_ctx* c, const PLevel& lv, int q) {
                                                                         lv.rows_f, 1);
     dct_cols_kernel<<<dim3((m + lv.cols - 1) / lv.cols, lv.B), 256, dct_smem_bytes(p, lv.cols),
                       c->stream>>>(lv.args, p, lv.lam, lv.cols, 1);
-    const dim3 gi((m + lv.rows_i - 1) / lv.rows_i, lv.B);
-    const size_t si = dct_smem_bytes(p, lv.rows_i + 1);
-    switch (q) {
-        case 0: dct_rows_inv_kernel<1, 0><<<gi, 256, si, c->stream>>>(lv.args, p, lv.rows_i, scale, 1); break;
-        case 1: dct_rows_inv_kernel<1, 1><<<gi, 256, si, c->stream>>>(lv.args, p, lv.rows_i, scale, 1); break;
-        default: dct_rows_inv_kernel<1, 2><<<gi, 256, si, c->stream>>>(lv.args, p, lv.rows_i, scale, 1); break;
+    if (lv.rows_p) {
+        const dim3 gi((m + lv.rows_p - 1) / lv.rows_p, lv.B);
+        const size_t si = dct_smem_bytes(p, lv.rows_p + 1);
+        switch (q) {
+            case 0: dct_rows_inv_kernel<1, 0><<<gi, 256, si, c->stream>>>(lv.args, p, lv.rows_p, scale, 1); break;
+            case 1: dct_rows_inv_kernel<1, 1><<<gi, 256, si, c->stream>>>(lv.args, p, lv.rows_p, scale, 1); break;
+            default: dct_rows_inv_kernel<1, 2><<<gi, 256, si, c->stream>>>(lv.args, p, lv.rows_p, scale, 1); break;
+        }
+    } else {  // very large m: psi through P_PSI, then the node-grid post kernel
+        dct_rows_inv_kernel<0, 1><<<dim3((m + lv.rows_i - 1) / lv.rows_i, lv.B), 256,
+                                    dct_smem_bytes(p, lv.rows_i), c->stream>>>(lv.args, p, lv.rows_i,
+                                                                                scale, 1);
+        switch (q) {
+            case 0: pdhg_post_kernel<0><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args); break;
+            case 1: pdhg_post_kernel<1><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args); break;
+            default: pdhg_post_kernel<2><<<lv.grid, lv.blk, 0, c->stream>>>(lv.args); break;
+        }
+        ++c->launches;
     }
     c->launches += kPdhgLaunches;
     CK(cudaGetLastError());
@@ -347,7 +361,8 @@ void run_pdhg_iters(w1mg_ctx* c, const PLevel& lv, int q, long max_iters) {
     }
     std::string key(reinterpret_cast<const char*>(&lv.args), sizeof(SweepArgs));
     key += "pdhg:" + std::to_string(q) + ":" + std::to_string(lv.B) + ":dct" +
-           std::to_string(lv.rows_f) + "." + std::to_string(lv.cols) + "." + std::to_string(lv.rows_i);
+           std::to_string(lv.rows_f) + "." + std::to_string(lv.cols) + "." + std::to_string(lv.rows_i) + "." +
+           std::to_string(lv.rows_p);
     cudaGraphExec_t ex;
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) {
@@ -367,7 +382,7 @@ void run_pdhg_iters(w1mg_ctx* c, const PLevel& lv, int q, long max_iters) {
     for (long g = 0;; ++g) {
         CK(cudaGraphLaunch(ex, c->stream));
         launched += K;
-        c->launches += (long)kPdhgLaunches * K;
+        c->launches += (long)(lv.rows_p ? kPdhgLaunches : kPdhgLaunches + 1) * K;
         CK(cudaMemcpyAsync(c->pinned + (g & 1), lv.ndone, sizeof(int), cudaMemcpyDeviceToHost,
                            c->stream));
         CK(cudaEventRecord(c->ev[g & 1], c->stream));

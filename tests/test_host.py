@@ -80,10 +80,13 @@ def test_engine_switches_validate_host():
     for name, val in ((b"tmap_nw", 4), (b"pdhg_small", 1), (b"compact", 1), (b"cluster_pick", 1)):
         assert L.w1mg_set_option(name, val) == _lib.W1MG_OK
     assert L.w1mg_set_option(b"tmap_nw", 0) == _lib.W1MG_OK  # back to auto
-    assert L.w1mg_set_option(b"tile_depth", 3) == _lib.W1MG_EINVAL
-    assert L.w1mg_set_option(b"tile", 3) == _lib.W1MG_EINVAL
-    for name, val in ((b"tile_depth", 2), (b"tile_depth", 1), (b"tile", 0), (b"tile_grid", 0)):
-        assert L.w1mg_set_option(name, val) == _lib.W1MG_OK
+    for gone in (b"tile", b"tile_depth", b"tile_grid", b"pdhg_fold"):  # engines removed
+        assert L.w1mg_set_option(gone, 1) == _lib.W1MG_EINVAL
+    assert L.w1mg_set_sweep_engine(0) == _lib.W1MG_EINVAL  # LDG engine removed
+    assert L.w1mg_set_sweep_engine(4) == _lib.W1MG_EINVAL  # two-column-set engine removed
+    assert L.w1mg_set_sweep_engine(3) == _lib.W1MG_OK
+    assert L.w1mg_set_resident_engine(4) == _lib.W1MG_EINVAL  # cooperative-grid engine removed
+    assert L.w1mg_set_resident_engine(1) == _lib.W1MG_OK
     assert L.w1mg_set_sweep_engine(7) == _lib.W1MG_EINVAL
     assert L.w1mg_set_sweep_engine(6) == _lib.W1MG_OK  # three-sweep engine
     assert L.w1mg_set_sweep_engine(3) == _lib.W1MG_OK

@@ -40,7 +40,7 @@ def probe_clocked(ctx, n, B, p=1):
 
 if __name__ == "__main__":
     ctx = _lib.Context(0)
-    engines = [int(e) for e in os.environ.get("ENGINES", "3").split(",")]  # 0 ldg, 1 tma, 2 tma2, 3 auto, 4 tma2w, 5 tma2t, 6 tma3
+    engines = [int(e) for e in os.environ.get("ENGINES", "3").split(",")]  # 1 tma, 2 tma2, 3 auto, 5 tma2t, 6 tma3
     cases = [(4096, 1), (2048, 1), (1024, 1), (512, 1), (512, 64), (512, 256), (256, 1024),
              (128, 1024), (64, 1024), (32, 1024)]
     if len(sys.argv) > 1:
@@ -49,7 +49,7 @@ if __name__ == "__main__":
         for e in engines:
             ctx.L.w1mg_set_sweep_engine(e)
             r = probe_clocked(ctx, n, B)
-            r["engine"] = ["ldg", "tma", "tma2", "auto", "tma2w", "tma2t", "tma3"][e]
+            r["engine"] = ["-", "tma", "tma2", "auto", "-", "tma2t", "tma3"][e]
             print(json.dumps(r), flush=True)
 
 
