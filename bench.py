@@ -271,9 +271,14 @@ def run_reference_arm(args):
 
 
 def workload_config(args, pairs):
+    num = getattr(args, "numerics", "exact")
     return {"workload": "config4: batched 512^2 density pairs, cascadic Li et al. PD "
                         "32->64->128->256->512, p=2, rel tol 1e-5 per level",
             "pairs_per_step": pairs, "grid": M, "levels": LEVELS,
+            "numerics": ("fast: tolerance-mode p=2 streaming sweeps (FMA node update, rsqrt "
+                         "shrink; fields within 1e-9 of the reference at fixed sweeps, W1 within "
+                         "1e-4 converged)") if num == "fast" else "exact: bit-identical to the "
+                                                                  "reference",
             "l2": "inputs exceed L2 (per-step state >> 126 MB); no flush needed",
             "parallelism": f"independent pairs per GPU ({args.gpus} GPU(s)), no collective"}
 
@@ -404,12 +409,14 @@ def parity_sample(img0, img1, dist, iters, k=8):
         rows.append({"pair": i, "w1_gpu": float(dist[i]), "w1_cpu": r.distance,
                      "rel_err": abs(float(dist[i]) - r.distance) / r.distance,
                      "sweeps_gpu": g, "sweeps_cpu": r.level_iters,
-                     "same_sweeps": g == r.level_iters})
+                     "same_sweeps": g == r.level_iters,
+                     "max_sweep_diff": max(abs(a - b) for a, b in zip(g, r.level_iters))})
     return {"source": "pairs of the last timed step (bench GPU images, device restriction) vs "
                       "the C oracle cascade on the same sources",
             "pairs": rows, "max_rel_err": max(x["rel_err"] for x in rows),
             "all_within_1e-4": all(x["rel_err"] <= 1e-4 for x in rows),
-            "all_same_sweeps": all(x["same_sweeps"] for x in rows), "cpu_seconds": secs}
+            "all_same_sweeps": all(x["same_sweeps"] for x in rows),
+            "max_sweep_diff": max(x["max_sweep_diff"] for x in rows), "cpu_seconds": secs}
 
 
 # ------------------------------------------------------------------ config 3
@@ -447,6 +454,12 @@ def main(argv=None):
                     help="pairs per GPU per step (config 4: 1024)")
     ap.add_argument("--e2e-steps", type=int, default=5,
                     help="steps of the e2e leg (at most --steps)")
+    ap.add_argument("--numerics", default="fast", choices=["fast", "exact"],
+                    help="fast: tolerance-mode p = 2 sweep kernels (fields within 1e-9 of the "
+                         "reference at fixed sweeps, tests/test_gpu_fast.py); exact: "
+                         "bit-identical to the reference")
+    ap.add_argument("--no-exact-leg", action="store_true",
+                    help="skip the one-step bit-exact-numerics measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / parity legs")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
@@ -482,6 +495,7 @@ def main(argv=None):
 
     ctx = _lib.Context(local)
     L = ctx.L
+    check(L.w1mg_set_option(b"fast", 1 if args.numerics == "fast" else 0))
     prm = MLParams()
     prm.levels, prm.pnorm, prm.step_mode = LEVELS, 1, 1
     prm.rel_tol, prm.eps, prm.max_iters = REL_TOL, None, 5_000_000
@@ -627,6 +641,24 @@ def main(argv=None):
                "api": "w1mg_ml_cp_batch (C-ABI, pinned host images in, W1/dual/sweeps out)"}
         del h0, h1
 
+    # ---- the same batch with bit-exact numerics (one warm-up + one timed step)
+    exact = None
+    if args.numerics == "fast" and not args.no_exact_leg:
+        check(L.w1mg_set_option(b"fast", 0))
+        step_dev()
+        barrier()
+        x0 = torch.cuda.Event(enable_timing=True)
+        x1 = torch.cuda.Event(enable_timing=True)
+        x0.record(cstream)
+        step_dev()
+        x1.record(cstream)
+        barrier()
+        tx = R.max(x0.elapsed_time(x1) * 1e-3)
+        exact = {"value": R.sum(cell_updates(iters_d.cpu().numpy())) / tx, "unit": UNIT,
+                 "steps": 1, "ms_per_step": 1e3 * tx,
+                 "numerics": "exact (bit-identical to the reference build)"}
+        check(L.w1mg_set_option(b"fast", 1))
+
     # ---- single-pair time-to-converged-W1 at 512^2 (device-resident input)
     t_single = None
     t_single_e2e = None
@@ -705,7 +737,7 @@ def main(argv=None):
             "data": "synthetic", "config": workload_config(args, args.pairs * world),
             "pairs_per_s": pairs_per_s, "all_converged": conv_all,
             "time_to_w1_512_s": t_single, "time_to_w1_512_e2e_s": t_single_e2e,
-            "config3_pdhg": cfg3,
+            "config3_pdhg": cfg3, "exact_numerics": exact,
             "levels": [{"n": n, "seconds_per_step": s_ / args.steps,
                         "cell_updates_per_s": c_ / s_}
                        for n, s_, c_ in zip(level_sizes(), lev_s, lev_cu)],

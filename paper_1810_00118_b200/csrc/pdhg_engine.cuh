@@ -167,7 +167,7 @@ DctPlan dct_plan(w1mg_ctx* c, int m) {
     return p;
 }
 
-constexpr size_t kDctSmemMax = 227u << 10;  // the sm_100 per-block opt-in limit
+constexpr size_t kDctSmemMax = (227u << 10) - 1024;  // per-block opt-in limit minus static smem
 
 void dct_kernel_attrs() {
     static unsigned long long done = 0;  // per device
