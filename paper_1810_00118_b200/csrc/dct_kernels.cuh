@@ -284,9 +284,9 @@ __device__ void dct2_vectors(const DctPlan& p, int NV, double* X, double* P, dou
     }
     // V[k1, k2] = Cp - i Sn (k2 < H2), V[k1, N2 - k2] = Cp + i Sn; V[m-k] = conj V[k];
     // X_k = 2 (cos(pi k/2m) Re V_k + sin(pi k/2m) Im V_k)
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int v = warp; v < NV; v += nw) {
-        for (int k = lane; k < m; k += 32) {
+    for (int e = threadIdx.x; e < NV * m; e += blockDim.x) {
+        const int v = e / m, k = e - v * m;
+        {
             int kk = k;
             int k1 = kk % N1;
             const bool cj = k1 >= H1;
@@ -484,23 +484,21 @@ __global__ void __launch_bounds__(256) dct_rows_fwd_kernel(const SweepArgs a, co
     dct_smem(g, R, p, P, Q, X);
     const int m = p.m, j0 = blockIdx.x * R;
     const Layout L = a.L;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const double* src = pslot(a, b, in);
-    for (int v = warp; v < R; v += nw) {
-        const int j = j0 + v;
-        for (int i = lane; i < m; i += 32) {
-            double x = 0.0;
-            if (j < m) x = MODE ? pdhg_rhs(a, b, i, j) : src[L.at(i, j)];
-            X[v * m + i] = x;
-        }
+    // every phase is spread over all threads: a CTA's time is its chain of
+    // barrier-separated phases, so no phase may run on a few warps only
+    for (int e = threadIdx.x; e < R * m; e += blockDim.x) {
+        const int v = e / m, i = e - v * m, j = j0 + v;
+        double x = 0.0;
+        if (j < m) x = MODE ? pdhg_rhs(a, b, i, j) : src[L.at(i, j)];
+        X[e] = x;
     }
     __syncthreads();
     dct2_vectors(p, R, X, P, Q);
     double* T = pslot_w(a, b, P_T);
-    for (int v = warp; v < R; v += nw) {
-        const int j = j0 + v;
-        if (j >= m) break;
-        for (int i = lane; i < m; i += 32) T[L.at(i, j)] = X[v * m + i];
+    for (int e = threadIdx.x; e < R * m; e += blockDim.x) {
+        const int v = e / m, i = e - v * m, j = j0 + v;
+        if (j < m) T[L.at(i, j)] = X[e];
     }
 }
 
@@ -552,20 +550,18 @@ __global__ void __launch_bounds__(256) dct_rows_inv_kernel(const SweepArgs a, co
     dct_smem(g, NV, p, P, Q, X);
     const int m = p.m, j0 = blockIdx.x * R;
     const Layout L = a.L;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const double* T = pslot(a, b, P_T);
-    for (int v = warp; v < NV; v += nw) {
-        const int j = j0 + v;
-        for (int i = lane; i < m; i += 32) X[v * m + i] = (j < m) ? T[L.at(i, j)] : 0.0;
+    for (int e = threadIdx.x; e < NV * m; e += blockDim.x) {
+        const int v = e / m, i = e - v * m, j = j0 + v;
+        X[e] = (j < m) ? T[L.at(i, j)] : 0.0;
     }
     __syncthreads();
     dct3_vectors(p, NV, X, P, Q);
     if (MODE == 0) {
         double* psi = pslot_w(a, b, P_PSI);
-        for (int v = warp; v < R; v += nw) {
-            const int j = j0 + v;
-            if (j >= m) break;
-            for (int i = lane; i < m; i += 32) psi[L.at(i, j)] = scale * X[v * m + i];
+        for (int e = threadIdx.x; e < R * m; e += blockDim.x) {
+            const int v = e / m, i = e - v * m, j = j0 + v;
+            if (j < m) psi[L.at(i, j)] = scale * X[e];
         }
         return;
     }
@@ -578,10 +574,9 @@ __global__ void __launch_bounds__(256) dct_rows_inv_kernel(const SweepArgs a, co
     double* bx = pslot_w(a, b, P_BX);
     double* by = pslot_w(a, b, P_BY);
     double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
-    for (int v = warp; v < R; v += nw) {
-        const int j = j0 + v;
-        if (j > n) break;
-        for (int i = lane; i <= n; i += 32) {
+    for (int e = threadIdx.x; e < R * m; e += blockDim.x) {
+        const int v = e / m, i = e - v * m, j = j0 + v;
+        if (j <= n) {
             const long o = L.at(i, j);
             const bool hx = i < n, hy = j < n;
             const double pc = scale * X[v * m + i];

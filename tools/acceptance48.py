@@ -56,5 +56,5 @@ if __name__ == "__main__":
                            ("annulus_pair", 0), ("config2", 2)):
             a4(kind, seed)
     if "a8" in what:
-        for kind in ("two_blobs", "annulus_pair"):
+        for kind in ("two_blobs", "annulus_pair", "config2", "config3"):
             a8(kind)
