@@ -64,6 +64,7 @@ struct DctPlan {
     const double* mk;   // [2m] cos, sin of pi k / 2m (interleaved)
     const short* idxA;  // [N2][N1] row position of v[(N2 t + N1 n2) mod m]
     const short* crt;   // [N2][H1] k with k mod N1 = k1 and k mod N2 = k2
+    const double* tabs; // the five tables above as one contiguous block (smem layout)
 };
 
 __host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
@@ -91,10 +92,13 @@ __host__ __device__ inline void dct_arena(const DctPlan& p, int NV, int& szP, in
     szQ = round4(szQ);
 }
 
+// row stride of X: even, so every row starts 16-B aligned (bulk copies)
+__host__ __device__ inline int dct_xs(const DctPlan& p) { return (p.m + 1) & ~1; }
+
 __host__ __device__ inline size_t dct_smem_bytes(const DctPlan& p, int NV) {
     int a, b;
     dct_arena(p, NV, a, b);
-    return sizeof(double) * ((size_t)dct_tab_doubles(p) + a + b + (size_t)NV * p.m);
+    return sizeof(double) * ((size_t)dct_tab_doubles(p) + a + b + (size_t)NV * dct_xs(p));
 }
 
 // C[k][j] = (C0 ? C0[j] : 0) + sgn sum_{t<K} tab[((t+1) k) mod N] B[t*ldb + j]
@@ -102,7 +106,7 @@ __host__ __device__ inline size_t dct_smem_bytes(const DctPlan& p, int NV) {
 // Wide GEMMs: 4 x 4 register tiles (lanes of a warp share the rows, so the
 // twiddle loads broadcast); thin ones (few tiles per thread block): one output
 // per thread, two accumulators.
-__device__ __forceinline__ void tgemm(const double* tab, int N, double sgn, int Mp, int K,
+__device__ __noinline__ void tgemm(const double* tab, int N, double sgn, int Mp, int K,
                                       const double* B, int ldb, int Np, double* C, int ldc,
                                       const double* C0) {
     const int Nt = Np >> 2, tiles = (Mp >> 2) * Nt;
@@ -176,29 +180,20 @@ __device__ __forceinline__ void tgemm(const double* tab, int N, double sgn, int 
     }
 }
 
-// Stage the plan's tables into shared memory; returns the smem view.
-__device__ __forceinline__ DctPlan dct_stage_tables(const DctPlan& g, double* sm) {
+// Smem view of the staged table block (same layout as p.tabs in global).
+__device__ __forceinline__ DctPlan dct_view(const DctPlan& g, double* sm) {
     DctPlan p = g;
-    double* tw1 = sm;
-    double* tw2 = tw1 + 2 * g.N1;
-    double* mk = tw2 + 2 * g.N2;
-    short* ia = reinterpret_cast<short*>(mk + 2 * g.m);
-    short* cr = ia + g.N2 * g.N1;
-    for (int e = threadIdx.x; e < 2 * g.N1; e += blockDim.x) tw1[e] = g.tw1[e];
-    for (int e = threadIdx.x; e < 2 * g.N2; e += blockDim.x) tw2[e] = g.tw2[e];
-    for (int e = threadIdx.x; e < 2 * g.m; e += blockDim.x) mk[e] = g.mk[e];
-    for (int e = threadIdx.x; e < g.N2 * g.N1; e += blockDim.x) ia[e] = g.idxA[e];
-    for (int e = threadIdx.x; e < g.N2 * g.H1; e += blockDim.x) cr[e] = g.crt[e];
-    p.tw1 = tw1;
-    p.tw2 = tw2;
-    p.mk = mk;
-    p.idxA = ia;
-    p.crt = cr;
+    p.tw1 = sm;
+    p.tw2 = sm + 2 * g.N1;
+    p.mk = p.tw2 + 2 * g.N2;
+    p.idxA = reinterpret_cast<const short*>(p.mk + 2 * g.m);
+    p.crt = p.idxA + g.N2 * g.N1;
     return p;
 }
 
 // Forward DCT-II of NV vectors X[v*m + i] in place (P, Q scratch).
-__device__ void dct2_vectors(const DctPlan& p, int NV, double* X, double* P, double* Q) {
+__device__ __noinline__ void dct2_vectors(const DctPlan& p, int NV, int xs, double* X, double* P,
+                                          double* Q) {
     const int m = p.m, N1 = p.N1, N2 = p.N2, H1 = p.H1, T1 = p.T1, E1 = p.E1;
     const int NA = NV * N2, NpA = round4(NA);
     // stage 1 fold: X0 = x_0, S_t = x_t + x_{N1-t}, D_t = x_t - x_{N1-t}
@@ -212,7 +207,7 @@ __device__ void dct2_vectors(const DctPlan& p, int NV, double* X, double* P, dou
         if (j < NA) {
             const int n2 = j / NV, v = j - n2 * NV;
             const short* ix = p.idxA + n2 * N1;
-            const double* xv = X + v * m;
+            const double* xv = X + v * xs;
             if (t == 0 || t > T1) {
                 s = xv[ix[t]];
             } else {
@@ -314,7 +309,7 @@ __device__ void dct2_vectors(const DctPlan& p, int NV, double* X, double* P, dou
             }
             if (cj) vi = -vi;
             const double c = p.mk[2 * k], s = p.mk[2 * k + 1];
-            X[v * m + k] = 2.0 * (c * vr + s * vi);
+            X[v * xs + k] = 2.0 * (c * vr + s * vi);
         }
     }
     __syncthreads();
@@ -330,7 +325,8 @@ __device__ __forceinline__ void dct3_w(const DctPlan& p, const double* x, int k,
 }
 
 // DCT-III of NV vectors X[v*m + k] in place (P, Q scratch).
-__device__ void dct3_vectors(const DctPlan& p, int NV, double* X, double* P, double* Q) {
+__device__ __noinline__ void dct3_vectors(const DctPlan& p, int NV, int xs, double* X, double* P,
+                                          double* Q) {
     const int m = p.m, N1 = p.N1, N2 = p.N2, H1 = p.H1, T1 = p.T1, E1 = p.E1;
     const int NA = NV * N2, NpA = round4(NA);
     // stage 1 inputs: BR / BI rows k1 = 1..T1 (BR row T1: Nyquist k1 = N1/2), B0 = Re b[0]
@@ -341,7 +337,7 @@ __device__ void dct3_vectors(const DctPlan& p, int NV, double* X, double* P, dou
         for (int e = threadIdx.x; e < H1 * NpA; e += blockDim.x) {
             const int t = e / NpA, j = e - t * NpA;
             double wr = 0.0, wi = 0.0;
-            if (j < NV) dct3_w(p, X + j * m, t, wr, wi);
+            if (j < NV) dct3_w(p, X + j * xs, t, wr, wi);
             if (t == 0) {
                 B0[j] = wr;
             } else {
@@ -361,7 +357,7 @@ __device__ void dct3_vectors(const DctPlan& p, int NV, double* X, double* P, dou
             double sr = 0.0, si = 0.0, dr = 0.0, di = 0.0;
             if (jb < NB) {
                 const int k1 = jb / NV, v = jb - k1 * NV;
-                const double* x = X + v * m;
+                const double* x = X + v * xs;
                 if (t == 0 || t > T2) {
                     dct3_w(p, x, p.crt[t * H1 + k1], sr, si);
                 } else {
@@ -438,20 +434,48 @@ __device__ void dct3_vectors(const DctPlan& p, int NV, double* X, double* P, dou
         else w = B0[j] + 2.0 * (PP[(N1 - n1) * NpA + j] + QQ[(N1 - n1) * NpA + j]);
         const int n = (N2 * n1 + N1 * n2) % m;
         const int pos = (n <= (m - 1) / 2) ? 2 * n : 2 * (m - 1 - n) + 1;
-        X[v * m + pos] = w;
+        X[v * xs + pos] = w;
     }
     __syncthreads();
 }
 
-__device__ __forceinline__ void dct_smem(const DctPlan& g, int NV, DctPlan& p, double*& P,
-                                         double*& Q, double*& X) {
+// Shared-memory layout of a DCT launch and the start of its loads: the
+// table block (one TMA bulk copy of the plan's contiguous global block) and,
+// for `rows` > 0, rows j0 .. j0+rows-1 of `src` (one bulk copy per row, m
+// rounded up to an even count -- the padding column is never used), all
+// completing on one mbarrier.  The caller waits with dct_wait().
+struct DctSmem {
+    DctPlan p;
+    double *P, *Q, *X;
+    int xs;
+};
+
+__device__ __forceinline__ DctSmem dct_begin(const DctPlan& g, int NV, const double* src,
+                                             const Layout& L, int j0, int rows, uint64_t* bar) {
     extern __shared__ __align__(16) double dct_sm[];
+    DctSmem d;
     int a, b;
     dct_arena(g, NV, a, b);
-    p = dct_stage_tables(g, dct_sm);
-    P = dct_sm + dct_tab_doubles(g);
-    Q = P + a;
-    X = Q + b;
+    d.p = dct_view(g, dct_sm);
+    d.P = dct_sm + dct_tab_doubles(g);
+    d.Q = d.P + a;
+    d.X = d.Q + b;
+    d.xs = dct_xs(g);
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t tb = (uint32_t)(dct_tab_doubles(g) * sizeof(double));
+        const uint32_t rb = (uint32_t)(d.xs * sizeof(double));
+        mbar_expect_tx(bar, tb + (uint32_t)rows * rb);
+        bulk_g2s(dct_sm, g.tabs, tb, bar);
+        for (int v = 0; v < rows; ++v) bulk_g2s(d.X + v * d.xs, src + L.at(0, j0 + v), rb, bar);
+    }
+    return d;
+}
+
+__device__ __forceinline__ void dct_wait(uint64_t* bar) {
+    __syncthreads();  // mbarrier initialised before anyone polls it; gathers done
+    mbar_wait(bar, 0u);
 }
 
 // r = A v - rho with v = m - mu varphi_bar (pdhg_pre_kernel's expression)
@@ -472,96 +496,126 @@ __device__ __forceinline__ double pdhg_rhs(const SweepArgs& a, int b, int i, int
     return div - pslot(a, b, P_RHO)[o];
 }
 
-// Rows j0 .. j0+R-1: (MODE 0) slot `in` or (MODE 1) the PDHG right-hand side
-// -> DCT-II along i -> slot P_T.
+// Rows j0 .. j0+R-1: (MODE 0) slot `in` (bulk copies) or (MODE 1) the PDHG
+// right-hand side (gathered, four nodes per thread in flight) -> DCT-II
+// along i -> slot P_T.
 template <int MODE>
 __global__ void __launch_bounds__(256) dct_rows_fwd_kernel(const SweepArgs a, const DctPlan g, int in,
                                                            int R, int check_done) {
     const int b = blockIdx.y;
     if (check_done && *(volatile int*)&a.ctl[b].done) return;
-    DctPlan p;
-    double *P, *Q, *X;
-    dct_smem(g, R, p, P, Q, X);
-    const int m = p.m, j0 = blockIdx.x * R;
+    __shared__ uint64_t bar;
+    const int m = g.m, j0 = blockIdx.x * R;
+    const int rows = MODE ? 0 : min(R, m - j0);
     const Layout L = a.L;
-    const double* src = pslot(a, b, in);
-    // every phase is spread over all threads: a CTA's time is its chain of
-    // barrier-separated phases, so no phase may run on a few warps only
-    for (int e = threadIdx.x; e < R * m; e += blockDim.x) {
-        const int v = e / m, i = e - v * m, j = j0 + v;
-        double x = 0.0;
-        if (j < m) x = MODE ? pdhg_rhs(a, b, i, j) : src[L.at(i, j)];
-        X[e] = x;
+    DctSmem d = dct_begin(g, R, pslot(a, b, in), L, j0, rows, &bar);
+    const int xs = d.xs;
+    if (MODE) {
+        // every phase is spread over all threads: a CTA's time is its chain
+        // of barrier-separated phases, so no phase may run on a few warps only
+        constexpr int U = 4;
+        const int tot = R * m;
+        for (int e0 = threadIdx.x; e0 < tot; e0 += U * blockDim.x) {
+            double x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * blockDim.x;
+                const int v = e / m, i = e - v * m, j = j0 + v;
+                x[u] = (e < tot && j < m) ? pdhg_rhs(a, b, i, j) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * blockDim.x;
+                if (e < tot) d.X[(e / m) * xs + e % m] = x[u];
+            }
+        }
+    } else {
+        for (int e = threadIdx.x; e < (R - rows) * xs; e += blockDim.x) d.X[rows * xs + e] = 0.0;
     }
-    __syncthreads();
-    dct2_vectors(p, R, X, P, Q);
+    dct_wait(&bar);
+    dct2_vectors(d.p, R, xs, d.X, d.P, d.Q);
     double* T = pslot_w(a, b, P_T);
     for (int e = threadIdx.x; e < R * m; e += blockDim.x) {
         const int v = e / m, i = e - v * m, j = j0 + v;
-        if (j < m) T[L.at(i, j)] = X[e];
+        if (j < m) T[L.at(i, j)] = d.X[v * xs + i];
     }
 }
 
 // Columns k1 = c0 .. c0+Wc-1 of P_T: DCT-II along j, spectral divide
-// (poisson.cpp:84-89), DCT-III along j, back to P_T.
+// (poisson.cpp:84-89), DCT-III along j, back to P_T.  X rows are the columns
+// (stride m, odd: the column gather is bank-conflict free).
 __global__ void __launch_bounds__(256) dct_cols_kernel(const SweepArgs a, const DctPlan g,
                                                        const double* __restrict__ lambda, int Wc,
                                                        int check_done) {
     const int b = blockIdx.y;
     if (check_done && *(volatile int*)&a.ctl[b].done) return;
-    DctPlan p;
-    double *P, *Q, *X;
-    dct_smem(g, Wc, p, P, Q, X);
-    const int m = p.m, c0 = blockIdx.x * Wc;
+    __shared__ uint64_t bar;
+    const int m = g.m, c0 = blockIdx.x * Wc;
     const Layout L = a.L;
+    DctSmem d = dct_begin(g, Wc, nullptr, L, 0, 0, &bar);
+    const int xs = m;
     double* T = pslot_w(a, b, P_T);
-    for (int e = threadIdx.x; e < Wc * m; e += blockDim.x) {
-        const int j = e / Wc, v = e - j * Wc;
-        X[v * m + j] = (c0 + v < m) ? T[L.at(c0 + v, j)] : 0.0;
+    {
+        constexpr int U = 4;
+        const int tot = Wc * m;
+        for (int e0 = threadIdx.x; e0 < tot; e0 += U * blockDim.x) {
+            double x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * blockDim.x;
+                const int j = e / Wc, v = e - j * Wc;
+                x[u] = (e < tot && c0 + v < m) ? T[L.at(c0 + v, j)] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * blockDim.x;
+                const int j = e / Wc, v = e - j * Wc;
+                if (e < tot) d.X[v * xs + j] = x[u];
+            }
+        }
     }
-    __syncthreads();
-    dct2_vectors(p, Wc, X, P, Q);
+    dct_wait(&bar);
+    dct2_vectors(d.p, Wc, xs, d.X, d.P, d.Q);
     for (int e = threadIdx.x; e < Wc * m; e += blockDim.x) {
         const int v = e / m, k2 = e - v * m, k1 = c0 + v;
         if (k1 < m) {
-            double& y = X[v * m + k2];
+            double& y = d.X[v * xs + k2];
             y = (k1 == 0 && k2 == 0) ? 0.0 : y / (lambda[k1] + lambda[k2]);
         }
     }
     __syncthreads();
-    dct3_vectors(p, Wc, X, P, Q);
+    dct3_vectors(d.p, Wc, xs, d.X, d.P, d.Q);
     for (int e = threadIdx.x; e < Wc * m; e += blockDim.x) {
         const int j = e / Wc, v = e - j * Wc;
-        if (c0 + v < m) T[L.at(c0 + v, j)] = X[v * m + j];
+        if (c0 + v < m) T[L.at(c0 + v, j)] = d.X[v * xs + j];
     }
 }
 
-// Rows j0 .. j0+R-1 of P_T: DCT-III along i, psi = y / (4 m^2) (poisson.cpp:93).
-// MODE 0: psi -> P_PSI.  MODE 1 (Q = conjugate norm): the PDHG post step on
-// these rows (pdhg_post_kernel's arithmetic) with psi from shared memory.
+// Rows j0 .. j0+R-1 of P_T (bulk copies): DCT-III along i, psi = y / (4 m^2)
+// (poisson.cpp:93).  MODE 0: psi -> P_PSI.  MODE 1 (QN = conjugate norm): the
+// PDHG post step on these rows (pdhg_post_kernel's arithmetic) with psi from
+// shared memory; one extra row is transformed for the y-difference.
 template <int MODE, int QN>
 __global__ void __launch_bounds__(256) dct_rows_inv_kernel(const SweepArgs a, const DctPlan g, int R,
                                                            double scale, int check_done) {
     const int b = blockIdx.y;
     if (check_done && *(volatile int*)&a.ctl[b].done) return;
+    __shared__ uint64_t bar;
     const int NV = MODE ? R + 1 : R;
-    DctPlan p;
-    double *P, *Q, *X;
-    dct_smem(g, NV, p, P, Q, X);
-    const int m = p.m, j0 = blockIdx.x * R;
+    const int m = g.m, j0 = blockIdx.x * R;
+    const int rows = min(NV, m - j0);
     const Layout L = a.L;
-    const double* T = pslot(a, b, P_T);
-    for (int e = threadIdx.x; e < NV * m; e += blockDim.x) {
-        const int v = e / m, i = e - v * m, j = j0 + v;
-        X[e] = (j < m) ? T[L.at(i, j)] : 0.0;
-    }
-    __syncthreads();
-    dct3_vectors(p, NV, X, P, Q);
+    DctSmem d = dct_begin(g, NV, pslot(a, b, P_T), L, j0, rows, &bar);
+    const int xs = d.xs;
+    for (int e = threadIdx.x; e < (NV - rows) * xs; e += blockDim.x) d.X[rows * xs + e] = 0.0;
+    dct_wait(&bar);
+    dct3_vectors(d.p, NV, xs, d.X, d.P, d.Q);
+    const double* X = d.X;
     if (MODE == 0) {
         double* psi = pslot_w(a, b, P_PSI);
         for (int e = threadIdx.x; e < R * m; e += blockDim.x) {
             const int v = e / m, i = e - v * m, j = j0 + v;
-            if (j < m) psi[L.at(i, j)] = scale * X[e];
+            if (j < m) psi[L.at(i, j)] = scale * X[v * xs + i];
         }
         return;
     }
@@ -579,19 +633,19 @@ __global__ void __launch_bounds__(256) dct_rows_inv_kernel(const SweepArgs a, co
         if (j <= n) {
             const long o = L.at(i, j);
             const bool hx = i < n, hy = j < n;
-            const double pc = scale * X[v * m + i];
+            const double pc = scale * X[v * xs + i];
             double mnx = 0.0, mny = 0.0, dmx = 0.0, dmy = 0.0, pox = 0.0, poy = 0.0;
             if (hx) {
                 const double mo = mx[o];
                 const double vv = mo - mu * bx[o];
-                mnx = vv - (pc - scale * X[v * m + i + 1]) * ih;  // poisson.cpp:124
+                mnx = vv - (pc - scale * X[v * xs + i + 1]) * ih;  // poisson.cpp:124
                 dmx = mnx - mo;
                 pox = px[o];
             }
             if (hy) {
                 const double mo = my[o];
                 const double vv = mo - mu * by[o];
-                mny = vv - (pc - scale * X[(v + 1) * m + i]) * ih;  // poisson.cpp:130
+                mny = vv - (pc - scale * X[(v + 1) * xs + i]) * ih;  // poisson.cpp:130
                 dmy = mny - mo;
                 poy = py[o];
             }

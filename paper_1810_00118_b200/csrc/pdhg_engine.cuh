@@ -147,22 +147,24 @@ DctPlan dct_plan(w1mg_ctx* c, int m) {
         mk[2 * k] = cosN(k, 4L * m);
         mk[2 * k + 1] = sinN(k, 4L * m);
     }
-    const std::string key = "dctp." + std::to_string(m) + ".";
-    auto up_d = [&](const char* name, const std::vector<double>& v) {
-        double* d = c->get<double>(key + name, v.size());
-        CK(cudaMemcpy(d, v.data(), v.size() * 8, cudaMemcpyHostToDevice));
-        return (const double*)d;
-    };
-    auto up_s = [&](const char* name, const std::vector<short>& v) {
-        short* d = c->get<short>(key + name, v.size());
-        CK(cudaMemcpy(d, v.data(), v.size() * sizeof(short), cudaMemcpyHostToDevice));
-        return (const short*)d;
-    };
-    p.idxA = up_s("idxA", idxA);
-    p.crt = up_s("crt", crt);
-    p.tw1 = up_d("tw1", tw1);
-    p.tw2 = up_d("tw2", tw2);
-    p.mk = up_d("mk", mk);
+    // one contiguous block in the shared-memory layout (dct_view): a CTA
+    // stages it with a single TMA bulk copy
+    std::vector<double> blk((size_t)dct_tab_doubles(p), 0.0);
+    double* bp = blk.data();
+    std::copy(tw1.begin(), tw1.end(), bp);
+    std::copy(tw2.begin(), tw2.end(), bp + 2 * N1);
+    std::copy(mk.begin(), mk.end(), bp + 2 * N1 + 2 * N2);
+    short* sp = reinterpret_cast<short*>(bp + 2 * N1 + 2 * N2 + 2 * m);
+    std::copy(idxA.begin(), idxA.end(), sp);
+    std::copy(crt.begin(), crt.end(), sp + idxA.size());
+    double* d = c->get<double>("dctp." + std::to_string(m), blk.size());
+    CK(cudaMemcpy(d, blk.data(), blk.size() * 8, cudaMemcpyHostToDevice));
+    p.tabs = d;
+    p.tw1 = d;
+    p.tw2 = d + 2 * N1;
+    p.mk = d + 2 * N1 + 2 * N2;
+    p.idxA = reinterpret_cast<const short*>(p.mk + 2 * m);
+    p.crt = p.idxA + idxA.size();
     c->dct[m] = p;
     return p;
 }

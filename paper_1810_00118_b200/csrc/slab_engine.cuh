@@ -37,6 +37,9 @@
 
 #include <nccl.h>
 
+#include <chrono>
+#include <thread>
+
 namespace w1mg_dev {
 
 // sums[k] = sum_r red[r*3+k] (r in order), then the stop rule for every slab
@@ -188,6 +191,30 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 void check_nccl(ncclResult_t r, const char* what) {
     if (r != ncclSuccess) fail(W1MG_ECUDA, std::string("NCCL ") + what + ": " + ncclGetErrorString(r));
+}
+
+// Host wait on an event of the context stream.  With a communicator the
+// wait polls ncclCommGetAsyncError: a failed or dead peer (network error,
+// remote abort) aborts the communicator and fails loudly instead of hanging
+// the host in cudaEventSynchronize.
+void wait_event_comm(cudaEvent_t e, w1mg_slab_comm* comm) {
+    if (!comm || !comm->comm) {
+        CK(cudaEventSynchronize(e));
+        return;
+    }
+    for (;;) {
+        const cudaError_t q = cudaEventQuery(e);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) CK(q);
+        ncclResult_t ar = ncclSuccess;
+        check_nccl(ncclCommGetAsyncError(comm->comm, &ar), "async error query");
+        if (ar != ncclSuccess && ar != ncclInProgress) {
+            ncclCommAbort(comm->comm);
+            comm->comm = nullptr;
+            fail(W1MG_ECUDA, std::string("NCCL asynchronous error: ") + ncclGetErrorString(ar));
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
 }
 
 // Emulated: all R slabs local.  NCCL: only slab `comm->rank` of `comm->world`.
@@ -418,7 +445,7 @@ void slab_run(w1mg_ctx* c, SlabSet& s, int pn, double tol, long max_iters) {
                            c->stream));
         CK(cudaEventRecord(c->ev[it & 1], c->stream));
         if (it > 0) {
-            CK(cudaEventSynchronize(c->ev[(it - 1) & 1]));
+            wait_event_comm(c->ev[(it - 1) & 1], s.comm);
             if (c->pinned[(it - 1) & 1] >= 1) break;
         }
         if (launched >= max_iters + K) break;
