@@ -64,7 +64,9 @@ struct DctPlan {
     const double* mk;   // [2m] cos, sin of pi k / 2m (interleaved)
     const short* idxA;  // [N2][N1] row position of v[(N2 t + N1 n2) mod m]
     const short* crt;   // [N2][H1] k with k mod N1 = k1 and k mod N2 = k2
-    const double* tabs; // the five tables above as one contiguous block (smem layout)
+    const int* f5;      // [m] output map of the forward transform: k1 | q << 16 |
+                        // (k2 >= H2) << 29 | (k1 >= H1: conjugate partner) << 30
+    const double* tabs; // the tables above as one contiguous block (smem layout)
 };
 
 __host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
@@ -72,8 +74,8 @@ __host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
 // doubles of the staged tables: tw1, tw2, mk, then the short index maps
 __host__ __device__ inline int dct_tab_doubles(const DctPlan& p) {
     const int d = 2 * p.N1 + 2 * p.N2 + 2 * p.m;
-    const int sh = p.N2 * p.N1 + p.N2 * p.H1;
-    return round4(d + (sh + 3) / 4);
+    const int sh = round4(p.N2 * p.N1 + p.N2 * p.H1);  // shorts, keeps f5 4-B aligned
+    return round4(d + sh / 4 + (p.m + 1) / 2);
 }
 
 // Shared-memory arenas (doubles) for NV vectors: P and Q (ping-pong scratch
@@ -101,23 +103,34 @@ __host__ __device__ inline size_t dct_smem_bytes(const DctPlan& p, int NV) {
     return sizeof(double) * ((size_t)dct_tab_doubles(p) + a + b + (size_t)NV * dct_xs(p));
 }
 
+// Loop over e = threadIdx.x + q blockDim.x < NA * NB as (a, b) = (e / NB,
+// e % NB) with one division per thread (at the start), not one per item:
+// the kernels are latency-bound chains of short phases, and per-item integer
+// divisions were most of their instructions (ncu).
+#define W1MG_FOR2(a, b, NA, NB)                                                           \
+    for (int a = (int)threadIdx.x / (NB), b = (int)threadIdx.x - a * (NB),                \
+             a##_d = (int)blockDim.x / (NB), b##_d = (int)blockDim.x - a##_d * (NB);      \
+         a < (NA); a += a##_d, b += b##_d, (b >= (NB) ? (b -= (NB), ++a) : 0))
+
 // C[k][j] = (C0 ? C0[j] : 0) + sgn sum_{t<K} tab[((t+1) k) mod N] B[t*ldb + j]
 // for k < Mp, j < Np (multiples of 4); tab, B, C, C0 in shared memory.
 // Wide GEMMs: 4 x 4 register tiles (lanes of a warp share the rows, so the
-// twiddle loads broadcast); thin ones (few tiles per thread block): one output
-// per thread, two accumulators.
+// twiddle loads broadcast); thin ones: one output per thread, two
+// accumulators.  k < Mp <= N + 3, so k mod N is one conditional subtraction.
 __device__ __noinline__ void tgemm(const double* tab, int N, double sgn, int Mp, int K,
-                                      const double* B, int ldb, int Np, double* C, int ldc,
-                                      const double* C0) {
-    const int Nt = Np >> 2, tiles = (Mp >> 2) * Nt;
-    if (2 * tiles >= (int)blockDim.x) {
-        for (int tt = threadIdx.x; tt < tiles; tt += blockDim.x) {
-            const int ti = tt / Nt, tj = tt - ti * Nt;
+                                   const double* B, int ldb, int Np, double* C, int ldc,
+                                   const double* C0) {
+    const int Nt = Np >> 2, Mt = Mp >> 2;
+    if (4 * Mt * Nt >= (int)blockDim.x) {
+        W1MG_FOR2(ti, tj, Mt, Nt) {
             int kr[4], ix[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                kr[r] = (4 * ti + r) % N;
-                ix[r] = kr[r];
+                int k = 4 * ti + r;
+                k -= (k >= N) ? N : 0;
+                k -= (k >= N) ? N : 0;
+                kr[r] = k;
+                ix[r] = k;
             }
             double acc[4][4];
 #pragma unroll
@@ -134,7 +147,7 @@ __device__ __noinline__ void tgemm(const double* tab, int N, double sgn, int Mp,
                 for (int r = 0; r < 4; ++r) {
                     const double av = tab[ix[r]];
                     ix[r] += kr[r];
-                    if (ix[r] >= N) ix[r] -= N;
+                    ix[r] -= (ix[r] >= N) ? N : 0;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) acc[r][q] = fma(av, bv[q], acc[r][q]);
                 }
@@ -158,23 +171,25 @@ __device__ __noinline__ void tgemm(const double* tab, int N, double sgn, int Mp,
             }
         }
     } else {
-        for (int e = threadIdx.x; e < Mp * Np; e += blockDim.x) {
-            const int k = e / Np, j = e - k * Np;
-            const int kr = k % N;
+        W1MG_FOR2(k, j, Mp, Np) {
+            int kr = k;
+            kr -= (kr >= N) ? N : 0;
+            kr -= (kr >= N) ? N : 0;
             int ix = kr;
             double a0 = 0.0, a1 = 0.0;
+            const double* bj = B + j;
             int t = 0;
             for (; t + 1 < K; t += 2) {
                 const double w0 = tab[ix];
                 ix += kr;
-                if (ix >= N) ix -= N;
+                ix -= (ix >= N) ? N : 0;
                 const double w1 = tab[ix];
                 ix += kr;
-                if (ix >= N) ix -= N;
-                a0 = fma(w0, B[t * ldb + j], a0);
-                a1 = fma(w1, B[(t + 1) * ldb + j], a1);
+                ix -= (ix >= N) ? N : 0;
+                a0 = fma(w0, bj[t * ldb], a0);
+                a1 = fma(w1, bj[(t + 1) * ldb], a1);
             }
-            if (t < K) a0 = fma(tab[ix], B[t * ldb + j], a0);
+            if (t < K) a0 = fma(tab[ix], bj[t * ldb], a0);
             C[k * ldc + j] = (C0 ? C0[j] : 0.0) + sgn * (a0 + a1);
         }
     }
@@ -188,26 +203,27 @@ __device__ __forceinline__ DctPlan dct_view(const DctPlan& g, double* sm) {
     p.mk = p.tw2 + 2 * g.N2;
     p.idxA = reinterpret_cast<const short*>(p.mk + 2 * g.m);
     p.crt = p.idxA + g.N2 * g.N1;
+    p.f5 = reinterpret_cast<const int*>(p.idxA + round4(g.N2 * g.N1 + g.N2 * g.H1));
     return p;
 }
 
-// Forward DCT-II of NV vectors X[v*m + i] in place (P, Q scratch).
+// Forward DCT-II of NV vectors X[v*xs + i] in place (P, Q scratch).  NV is a
+// power of two (lg = log2 NV): vector indices split by shifts.
 __device__ __noinline__ void dct2_vectors(const DctPlan& p, int NV, int xs, double* X, double* P,
                                           double* Q) {
-    const int m = p.m, N1 = p.N1, N2 = p.N2, H1 = p.H1, T1 = p.T1, E1 = p.E1;
+    const int N1 = p.N1, N2 = p.N2, H1 = p.H1, T1 = p.T1, E1 = p.E1;
+    const int lg = __ffs(NV) - 1, msk = NV - 1;
     const int NA = NV * N2, NpA = round4(NA);
     // stage 1 fold: X0 = x_0, S_t = x_t + x_{N1-t}, D_t = x_t - x_{N1-t}
-    // (S row T1 = x_{N1/2} for even N1)
+    // (S row T1 = x_{N1/2} for even N1); vector j = n2 NV + v
     double* SA = P;
     double* DA = P + (T1 + E1) * NpA;
     double* X0 = DA + T1 * NpA;
-    for (int e = threadIdx.x; e < (T1 + 1 + E1) * NpA; e += blockDim.x) {
-        const int t = e / NpA, j = e - t * NpA;
+    W1MG_FOR2(t, j, T1 + 1 + E1, NpA) {
         double s = 0.0, d = 0.0;
         if (j < NA) {
-            const int n2 = j / NV, v = j - n2 * NV;
-            const short* ix = p.idxA + n2 * N1;
-            const double* xv = X + v * xs;
+            const short* ix = p.idxA + (j >> lg) * N1;
+            const double* xv = X + (j & msk) * xs;
             if (t == 0 || t > T1) {
                 s = xv[ix[t]];
             } else {
@@ -230,7 +246,7 @@ __device__ __noinline__ void dct2_vectors(const DctPlan& p, int NV, int xs, doub
     tgemm(p.tw1, N1, 1.0, p.H1p, T1 + E1, SA, NpA, NpA, ReA, NpA, X0);
     tgemm(p.tw1 + N1, N1, -1.0, p.H1p, T1, DA, NpA, NpA, ImA, NpA, nullptr);
     __syncthreads();
-    const int NB = NV * H1, NpB = round4(NB), W2 = 2 * NpB, H2 = p.H2;
+    const int NB = NV * H1, NpB = round4(NB), W2 = 2 * NpB;
     double* Cp = Q;
     double* Sn = Q + p.H2p * W2;
     if (N2 > 1) {
@@ -240,18 +256,17 @@ __device__ __noinline__ void dct2_vectors(const DctPlan& p, int NV, int xs, doub
         double* SB = P;
         double* DB = P + (T2 + E2) * W2;
         double* A0 = DB + T2 * W2;
-        for (int e = threadIdx.x; e < (T2 + 1 + E2) * NpB; e += blockDim.x) {
-            const int t = e / NpB, jb = e - t * NpB;
+        W1MG_FOR2(t, jb, T2 + 1 + E2, NpB) {
             double sr = 0.0, si = 0.0, dr = 0.0, di = 0.0;
             if (jb < NB) {
-                const int k1 = jb / NV, v = jb - k1 * NV;
+                const int k1 = jb >> lg, v = jb & msk;
                 const double* re = ReA + k1 * NpA;
                 const double* im = ImA + k1 * NpA;
                 if (t == 0 || t > T2) {
-                    sr = re[t * NV + v];
-                    si = im[t * NV + v];
+                    sr = re[(t << lg) + v];
+                    si = im[(t << lg) + v];
                 } else {
-                    const int ja = t * NV + v, jc = (N2 - t) * NV + v;
+                    const int ja = (t << lg) + v, jc = ((N2 - t) << lg) + v;
                     sr = re[ja] + re[jc];
                     si = im[ja] + im[jc];
                     dr = re[ja] - re[jc];
@@ -262,13 +277,13 @@ __device__ __noinline__ void dct2_vectors(const DctPlan& p, int NV, int xs, doub
                 A0[jb] = sr;
                 A0[NpB + jb] = si;
             } else {
-                double* s = SB + (t - 1) * W2;
-                s[jb] = sr;
-                s[NpB + jb] = si;
+                double* sp = SB + (t - 1) * W2;
+                sp[jb] = sr;
+                sp[NpB + jb] = si;
                 if (t <= T2) {
-                    double* d = DB + (t - 1) * W2;
-                    d[jb] = dr;
-                    d[NpB + jb] = di;
+                    double* dp = DB + (t - 1) * W2;
+                    dp[jb] = dr;
+                    dp[NpB + jb] = di;
                 }
             }
         }
@@ -278,39 +293,30 @@ __device__ __noinline__ void dct2_vectors(const DctPlan& p, int NV, int xs, doub
         __syncthreads();
     }
     // V[k1, k2] = Cp - i Sn (k2 < H2), V[k1, N2 - k2] = Cp + i Sn; V[m-k] = conj V[k];
-    // X_k = 2 (cos(pi k/2m) Re V_k + sin(pi k/2m) Im V_k)
-    for (int e = threadIdx.x; e < NV * m; e += blockDim.x) {
-        const int v = e / m, k = e - v * m;
-        {
-            int kk = k;
-            int k1 = kk % N1;
-            const bool cj = k1 >= H1;
-            if (cj) {
-                kk = m - k;
-                k1 = kk % N1;
-            }
-            double vr, vi;
-            if (N2 == 1) {
-                vr = ReA[k1 * NpA + v];
-                vi = ImA[k1 * NpA + v];
+    // X_k = 2 (cos(pi k/2m) Re V_k + sin(pi k/2m) Im V_k); the (k1, row, flags)
+    // of every k come from the plan's f5 map
+    W1MG_FOR2(v, k, NV, p.m) {
+        const int f = p.f5[k];
+        const int k1 = f & 0xffff, q = (f >> 16) & 0x1fff;
+        double vr, vi;
+        if (N2 == 1) {
+            vr = ReA[k1 * NpA + v];
+            vi = ImA[k1 * NpA + v];
+        } else {
+            const int jb = (k1 << lg) + v;
+            const double* cp = Cp + q * W2;
+            const double* sn = Sn + q * W2;
+            if (!(f & (1 << 29))) {
+                vr = cp[jb] + sn[NpB + jb];
+                vi = cp[NpB + jb] - sn[jb];
             } else {
-                const int k2 = kk % N2, jb = k1 * NV + v;
-                if (k2 < H2) {
-                    const double* cp = Cp + k2 * W2;
-                    const double* sn = Sn + k2 * W2;
-                    vr = cp[jb] + sn[NpB + jb];
-                    vi = cp[NpB + jb] - sn[jb];
-                } else {
-                    const double* cp = Cp + (N2 - k2) * W2;
-                    const double* sn = Sn + (N2 - k2) * W2;
-                    vr = cp[jb] - sn[NpB + jb];
-                    vi = cp[NpB + jb] + sn[jb];
-                }
+                vr = cp[jb] - sn[NpB + jb];
+                vi = cp[NpB + jb] + sn[jb];
             }
-            if (cj) vi = -vi;
-            const double c = p.mk[2 * k], s = p.mk[2 * k + 1];
-            X[v * xs + k] = 2.0 * (c * vr + s * vi);
         }
+        if (f & (1 << 30)) vi = -vi;
+        const double c = p.mk[2 * k], sk = p.mk[2 * k + 1];
+        X[v * xs + k] = 2.0 * (c * vr + sk * vi);
     }
     __syncthreads();
 }
@@ -324,24 +330,25 @@ __device__ __forceinline__ void dct3_w(const DctPlan& p, const double* x, int k,
     wi = s * a - c * b;
 }
 
-// DCT-III of NV vectors X[v*m + k] in place (P, Q scratch).
+// DCT-III of NV vectors X[v*xs + k] in place (P, Q scratch); NV a power of two.
 __device__ __noinline__ void dct3_vectors(const DctPlan& p, int NV, int xs, double* X, double* P,
                                           double* Q) {
-    const int m = p.m, N1 = p.N1, N2 = p.N2, H1 = p.H1, T1 = p.T1, E1 = p.E1;
+    const int N1 = p.N1, N2 = p.N2, H1 = p.H1, T1 = p.T1, E1 = p.E1;
+    const int lg = __ffs(NV) - 1, msk = NV - 1;
     const int NA = NV * N2, NpA = round4(NA);
-    // stage 1 inputs: BR / BI rows k1 = 1..T1 (BR row T1: Nyquist k1 = N1/2), B0 = Re b[0]
+    // stage 1 inputs: BR / BI rows k1 = 1..T1 (BR row T1: Nyquist k1 = N1/2,
+    // halved: it enters the real inverse DFT once), B0 = Re b[0]
     double* BR = P;
     double* BI = P + (T1 + E1) * NpA;
     double* B0 = BI + T1 * NpA;
     if (N2 == 1) {
-        for (int e = threadIdx.x; e < H1 * NpA; e += blockDim.x) {
-            const int t = e / NpA, j = e - t * NpA;
+        W1MG_FOR2(t, j, H1, NpA) {
             double wr = 0.0, wi = 0.0;
             if (j < NV) dct3_w(p, X + j * xs, t, wr, wi);
             if (t == 0) {
                 B0[j] = wr;
             } else {
-                BR[(t - 1) * NpA + j] = (t <= T1) ? wr : 0.5 * wr;  // Nyquist enters once
+                BR[(t - 1) * NpA + j] = (t <= T1) ? wr : 0.5 * wr;
                 if (t <= T1) BI[(t - 1) * NpA + j] = wi;
             }
         }
@@ -352,11 +359,10 @@ __device__ __noinline__ void dct3_vectors(const DctPlan& p, int NV, int xs, doub
         double* SB = P;
         double* DB = P + (T2 + E2) * W2;
         double* A0 = DB + T2 * W2;
-        for (int e = threadIdx.x; e < (T2 + 1 + E2) * NpB; e += blockDim.x) {
-            const int t = e / NpB, jb = e - t * NpB;
+        W1MG_FOR2(t, jb, T2 + 1 + E2, NpB) {
             double sr = 0.0, si = 0.0, dr = 0.0, di = 0.0;
             if (jb < NB) {
-                const int k1 = jb / NV, v = jb - k1 * NV;
+                const int k1 = jb >> lg, v = jb & msk;
                 const double* x = X + v * xs;
                 if (t == 0 || t > T2) {
                     dct3_w(p, x, p.crt[t * H1 + k1], sr, si);
@@ -374,13 +380,13 @@ __device__ __noinline__ void dct3_vectors(const DctPlan& p, int NV, int xs, doub
                 A0[jb] = sr;
                 A0[NpB + jb] = si;
             } else {
-                double* s = SB + (t - 1) * W2;
-                s[jb] = sr;
-                s[NpB + jb] = si;
+                double* sp = SB + (t - 1) * W2;
+                sp[jb] = sr;
+                sp[NpB + jb] = si;
                 if (t <= T2) {
-                    double* d = DB + (t - 1) * W2;
-                    d[jb] = dr;
-                    d[NpB + jb] = di;
+                    double* dp = DB + (t - 1) * W2;
+                    dp[jb] = dr;
+                    dp[NpB + jb] = di;
                 }
             }
         }
@@ -391,12 +397,11 @@ __device__ __noinline__ void dct3_vectors(const DctPlan& p, int NV, int xs, doub
         tgemm(p.tw2 + N2, N2, 1.0, p.H2p, T2, DB, W2, W2, Sn, W2, nullptr);
         __syncthreads();
         // b[k1][n2] = Cp + i Sn (n2 < H2), b[k1][N2 - n2] = Cp - i Sn -> stage 1 inputs
-        // (vector j = n2 NV + v): BR / BI rows k1 = 1..H1-1, B0 = Re b[0]
-        for (int e = threadIdx.x; e < H1 * NpA; e += blockDim.x) {
-            const int t = e / NpA, j = e - t * NpA;
+        // (vector j = n2 NV + v)
+        W1MG_FOR2(t, j, H1, NpA) {
             double br = 0.0, bi = 0.0;
             if (j < NA) {
-                const int n2 = j / NV, v = j - n2 * NV, jb = t * NV + v;
+                const int n2 = j >> lg, jb = (t << lg) + (j & msk);
                 if (n2 < H2) {
                     const double* cp = Cp + n2 * W2;
                     const double* sn = Sn + n2 * W2;
@@ -412,7 +417,7 @@ __device__ __noinline__ void dct3_vectors(const DctPlan& p, int NV, int xs, doub
             if (t == 0) {
                 B0[j] = br;
             } else {
-                BR[(t - 1) * NpA + j] = (t <= T1) ? br : 0.5 * br;  // Nyquist enters once
+                BR[(t - 1) * NpA + j] = (t <= T1) ? br : 0.5 * br;
                 if (t <= T1) BI[(t - 1) * NpA + j] = bi;
             }
         }
@@ -424,17 +429,15 @@ __device__ __noinline__ void dct3_vectors(const DctPlan& p, int NV, int xs, doub
     tgemm(p.tw1, N1, 1.0, p.H1p, T1 + E1, BR, NpA, NpA, PP, NpA, nullptr);
     tgemm(p.tw1 + N1, N1, 1.0, p.H1p, T1, BI, NpA, NpA, QQ, NpA, nullptr);
     __syncthreads();
-    // un-reorder: n = (N2 n1 + N1 n2) mod m -> y[2n] / y[2(m-1-n)+1]
-    for (int e = threadIdx.x; e < NA * N1; e += blockDim.x) {
-        const int r = e / NV, v = e - r * NV;
-        const int n2 = r / N1, n1 = r - n2 * N1;
-        const int j = n2 * NV + v;
+    // un-reorder: n = (N2 n1 + N1 n2) mod m -> y at idxA[n2][n1] (the forward
+    // input map); r = n2 N1 + n1
+    W1MG_FOR2(n2, q, N2, N1 << lg) {
+        const int n1 = q >> lg, v = q & msk, r = n2 * N1 + n1;
+        const int j = (n2 << lg) + v;
         double w;
         if (n1 < H1) w = B0[j] + 2.0 * (PP[n1 * NpA + j] - QQ[n1 * NpA + j]);
         else w = B0[j] + 2.0 * (PP[(N1 - n1) * NpA + j] + QQ[(N1 - n1) * NpA + j]);
-        const int n = (N2 * n1 + N1 * n2) % m;
-        const int pos = (n <= (m - 1) / 2) ? 2 * n : 2 * (m - 1 - n) + 1;
-        X[v * xs + pos] = w;
+        X[v * xs + p.idxA[r]] = w;
     }
     __syncthreads();
 }
@@ -513,21 +516,9 @@ __global__ void __launch_bounds__(256) dct_rows_fwd_kernel(const SweepArgs a, co
     if (MODE) {
         // every phase is spread over all threads: a CTA's time is its chain
         // of barrier-separated phases, so no phase may run on a few warps only
-        constexpr int U = 4;
-        const int tot = R * m;
-        for (int e0 = threadIdx.x; e0 < tot; e0 += U * blockDim.x) {
-            double x[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int e = e0 + u * blockDim.x;
-                const int v = e / m, i = e - v * m, j = j0 + v;
-                x[u] = (e < tot && j < m) ? pdhg_rhs(a, b, i, j) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int e = e0 + u * blockDim.x;
-                if (e < tot) d.X[(e / m) * xs + e % m] = x[u];
-            }
+        W1MG_FOR2(v, i, R, m) {
+            const int j = j0 + v;
+            d.X[v * xs + i] = (j < m) ? pdhg_rhs(a, b, i, j) : 0.0;
         }
     } else {
         for (int e = threadIdx.x; e < (R - rows) * xs; e += blockDim.x) d.X[rows * xs + e] = 0.0;
@@ -535,9 +526,8 @@ __global__ void __launch_bounds__(256) dct_rows_fwd_kernel(const SweepArgs a, co
     dct_wait(&bar);
     dct2_vectors(d.p, R, xs, d.X, d.P, d.Q);
     double* T = pslot_w(a, b, P_T);
-    for (int e = threadIdx.x; e < R * m; e += blockDim.x) {
-        const int v = e / m, i = e - v * m, j = j0 + v;
-        if (j < m) T[L.at(i, j)] = d.X[v * xs + i];
+    W1MG_FOR2(v, i, R, m) {
+        if (j0 + v < m) T[L.at(i, j0 + v)] = d.X[v * xs + i];
     }
 }
 
@@ -555,29 +545,13 @@ __global__ void __launch_bounds__(256) dct_cols_kernel(const SweepArgs a, const 
     DctSmem d = dct_begin(g, Wc, nullptr, L, 0, 0, &bar);
     const int xs = m;
     double* T = pslot_w(a, b, P_T);
-    {
-        constexpr int U = 4;
-        const int tot = Wc * m;
-        for (int e0 = threadIdx.x; e0 < tot; e0 += U * blockDim.x) {
-            double x[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int e = e0 + u * blockDim.x;
-                const int j = e / Wc, v = e - j * Wc;
-                x[u] = (e < tot && c0 + v < m) ? T[L.at(c0 + v, j)] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int e = e0 + u * blockDim.x;
-                const int j = e / Wc, v = e - j * Wc;
-                if (e < tot) d.X[v * xs + j] = x[u];
-            }
-        }
+    W1MG_FOR2(j, v, m, Wc) {
+        d.X[v * xs + j] = (c0 + v < m) ? T[L.at(c0 + v, j)] : 0.0;
     }
     dct_wait(&bar);
     dct2_vectors(d.p, Wc, xs, d.X, d.P, d.Q);
-    for (int e = threadIdx.x; e < Wc * m; e += blockDim.x) {
-        const int v = e / m, k2 = e - v * m, k1 = c0 + v;
+    W1MG_FOR2(v, k2, Wc, m) {
+        const int k1 = c0 + v;
         if (k1 < m) {
             double& y = d.X[v * xs + k2];
             y = (k1 == 0 && k2 == 0) ? 0.0 : y / (lambda[k1] + lambda[k2]);
@@ -585,8 +559,7 @@ __global__ void __launch_bounds__(256) dct_cols_kernel(const SweepArgs a, const 
     }
     __syncthreads();
     dct3_vectors(d.p, Wc, xs, d.X, d.P, d.Q);
-    for (int e = threadIdx.x; e < Wc * m; e += blockDim.x) {
-        const int j = e / Wc, v = e - j * Wc;
+    W1MG_FOR2(j, v, m, Wc) {
         if (c0 + v < m) T[L.at(c0 + v, j)] = d.X[v * xs + j];
     }
 }
@@ -594,7 +567,8 @@ __global__ void __launch_bounds__(256) dct_cols_kernel(const SweepArgs a, const 
 // Rows j0 .. j0+R-1 of P_T (bulk copies): DCT-III along i, psi = y / (4 m^2)
 // (poisson.cpp:93).  MODE 0: psi -> P_PSI.  MODE 1 (QN = conjugate norm): the
 // PDHG post step on these rows (pdhg_post_kernel's arithmetic) with psi from
-// shared memory; one extra row is transformed for the y-difference.
+// shared memory; one extra row is transformed for the y-difference (R + 1
+// must be a power of two).
 template <int MODE, int QN>
 __global__ void __launch_bounds__(256) dct_rows_inv_kernel(const SweepArgs a, const DctPlan g, int R,
                                                            double scale, int check_done) {
@@ -613,9 +587,8 @@ __global__ void __launch_bounds__(256) dct_rows_inv_kernel(const SweepArgs a, co
     const double* X = d.X;
     if (MODE == 0) {
         double* psi = pslot_w(a, b, P_PSI);
-        for (int e = threadIdx.x; e < R * m; e += blockDim.x) {
-            const int v = e / m, i = e - v * m, j = j0 + v;
-            if (j < m) psi[L.at(i, j)] = scale * X[v * xs + i];
+        W1MG_FOR2(v, i, R, m) {
+            if (j0 + v < m) psi[L.at(i, j0 + v)] = scale * X[v * xs + i];
         }
         return;
     }
@@ -628,8 +601,8 @@ __global__ void __launch_bounds__(256) dct_rows_inv_kernel(const SweepArgs a, co
     double* bx = pslot_w(a, b, P_BX);
     double* by = pslot_w(a, b, P_BY);
     double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
-    for (int e = threadIdx.x; e < R * m; e += blockDim.x) {
-        const int v = e / m, i = e - v * m, j = j0 + v;
+    W1MG_FOR2(v, i, R, m) {
+        const int j = j0 + v;
         if (j <= n) {
             const long o = L.at(i, j);
             const bool hx = i < n, hy = j < n;

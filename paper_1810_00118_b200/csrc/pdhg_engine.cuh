@@ -157,6 +157,18 @@ DctPlan dct_plan(w1mg_ctx* c, int m) {
     short* sp = reinterpret_cast<short*>(bp + 2 * N1 + 2 * N2 + 2 * m);
     std::copy(idxA.begin(), idxA.end(), sp);
     std::copy(crt.begin(), crt.end(), sp + idxA.size());
+    int* fp = reinterpret_cast<int*>(sp + round4((int)(idxA.size() + crt.size())));
+    for (int k = 0; k < m; ++k) {  // forward output map (dct2_vectors)
+        int kk = k, k1 = k % N1, cj = 0;
+        if (k1 >= p.H1) {
+            kk = m - k;
+            k1 = kk % N1;
+            cj = 1;
+        }
+        const int k2 = kk % N2, mir = (N2 > 1 && k2 >= p.H2) ? 1 : 0;
+        const int q = mir ? N2 - k2 : k2;
+        fp[k] = k1 | (q << 16) | (mir << 29) | (cj << 30);
+    }
     double* d = c->get<double>("dctp." + std::to_string(m), blk.size());
     CK(cudaMemcpy(d, blk.data(), blk.size() * 8, cudaMemcpyHostToDevice));
     p.tabs = d;
@@ -165,6 +177,7 @@ DctPlan dct_plan(w1mg_ctx* c, int m) {
     p.mk = d + 2 * N1 + 2 * N2;
     p.idxA = reinterpret_cast<const short*>(p.mk + 2 * m);
     p.crt = p.idxA + idxA.size();
+    p.f5 = reinterpret_cast<const int*>(p.idxA + round4((int)(idxA.size() + crt.size())));
     c->dct[m] = p;
     return p;
 }
@@ -199,6 +212,19 @@ int dct_vectors_per_cta(const DctPlan& p, int B, int num_sms, int extra) {
         R <<= 1;
     while (R > 1 && dct_smem_bytes(p, R + extra) > kDctSmemMax) R >>= 1;
     return dct_smem_bytes(p, R + extra) <= kDctSmemMax ? R : 0;
+}
+
+// Rows per CTA of the fused row DCT-III + post launch: R + 1 vectors (one
+// halo row), R + 1 a power of two (the transforms split vector indices by
+// shifts): R in {1, 3, 7, 15}, the most that keep one wave of two CTAs per
+// SM within the shared-memory budget; 0 if even R = 1 does not fit.
+int dct_post_rows_per_cta(const DctPlan& p, int B, int num_sms) {
+    int R = 1;
+    while (R < 15 && (long)((p.m + R - 1) / R) * B > 2L * num_sms &&
+           dct_smem_bytes(p, 2 * (R + 1)) <= kDctSmemMax)
+        R = 2 * (R + 1) - 1;
+    while (R > 1 && dct_smem_bytes(p, R + 1) > kDctSmemMax) R = (R + 1) / 2 - 1;
+    return dct_smem_bytes(p, R + 1) <= kDctSmemMax ? R : 0;
 }
 
 PLevel make_plevel(w1mg_ctx* c, const std::string& tag, int n, int B, double mu, double tau,
@@ -236,7 +262,7 @@ PLevel make_plevel(w1mg_ctx* c, const std::string& tag, int n, int B, double mu,
     lv.rows_f = dct_vectors_per_cta(lv.dp, B, c->num_sms, 0);
     lv.cols = dct_vectors_per_cta(lv.dp, B, c->num_sms, 0);
     lv.rows_i = dct_vectors_per_cta(lv.dp, B, c->num_sms, 0);
-    lv.rows_p = dct_vectors_per_cta(lv.dp, B, c->num_sms, 1);
+    lv.rows_p = dct_post_rows_per_cta(lv.dp, B, c->num_sms);
     if (!lv.rows_f || !lv.cols || !lv.rows_i)
         fail(W1MG_EINVAL, "Poisson solve: grid too large for the shared-memory DCT");
     dct_kernel_attrs();
