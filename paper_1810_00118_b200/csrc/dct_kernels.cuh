@@ -112,15 +112,34 @@ __host__ __device__ inline size_t dct_smem_bytes(const DctPlan& p, int NV) {
              a##_d = (int)blockDim.x / (NB), b##_d = (int)blockDim.x - a##_d * (NB);      \
          a < (NA); a += a##_d, b += b##_d, (b >= (NB) ? (b -= (NB), ++a) : 0))
 
-// C[k][j] = (C0 ? C0[j] : 0) + sgn sum_{t<K} tab[((t+1) k) mod N] B[t*ldb + j]
-// for k < Mp, j < Np (multiples of 4); tab, B, C, C0 in shared memory.
-// Wide GEMMs: 4 x 4 register tiles (lanes of a warp share the rows, so the
-// twiddle loads broadcast); thin ones: one output per thread, two
-// accumulators.  k < Mp <= N + 3, so k mod N is one conditional subtraction.
-__device__ __noinline__ void tgemm(const double* tab, int N, double sgn, int Mp, int K,
-                                   const double* B, int ldb, int Np, double* C, int ldc,
-                                   const double* C0) {
+__device__ __forceinline__ double lds(const double* p) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+}
+__device__ __forceinline__ double2 lds2(const double* p) {
+    double2 v;
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];"
+        : "=d"(v.x), "=d"(v.y)
+        : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+}
+
+// The two GEMMs of one real-DFT stage over a factor N, sharing the twiddle
+// index walk:
+//   C1[k][j] = (C0 ? C0[j] : 0) + sum_{t<K1} cos(2 pi ((t+1) k mod N)/N) B1[t][j]
+//   C2[k][j] = s2 sum_{t<K2} sin(2 pi ((t+1) k mod N)/N) B2[t][j]
+// for k < Mp, j < Np (K1 = K2 or K2 + 1: the Nyquist row is cosine-only).
+// tab = [cos | sin] of N entries, in shared memory like B1, B2, C1, C2, C0.
+// Wide: 4 x 4 register tiles per matrix (lanes of a warp share the rows, so
+// the twiddle loads broadcast).  Thin: one (k, j) per thread over the first
+// Nr <= Np columns only (the padded columns of a one-vector transform are
+// not computed).  k < Mp <= N + 3: k mod N is a conditional subtraction.
+__device__ __noinline__ void tgemm2(const double* tab, int N, int Mp, int K1, int K2,
+                                    const double* B1, const double* B2, int ldb, int Np, int Nr,
+                                    double* C1, double* C2, int ldc, const double* C0, double s2) {
     const int Nt = Np >> 2, Mt = Mp >> 2;
+    const double* ts = tab + N;
     if (4 * Mt * Nt >= (int)blockDim.x) {
         W1MG_FOR2(ti, tj, Mt, Nt) {
             int kr[4], ix[4];
@@ -132,30 +151,38 @@ __device__ __noinline__ void tgemm(const double* tab, int N, double sgn, int Mp,
                 kr[r] = k;
                 ix[r] = k;
             }
-            double acc[4][4];
+            double c[4][4], d[4][4];
 #pragma unroll
             for (int r = 0; r < 4; ++r)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[r][q] = 0.0;
-            const double* b = B + 4 * tj;
-#pragma unroll 2
-            for (int t = 0; t < K; ++t) {
-                const double2 b01 = *reinterpret_cast<const double2*>(b + t * ldb);
-                const double2 b23 = *reinterpret_cast<const double2*>(b + t * ldb + 2);
-                const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+                for (int q = 0; q < 4; ++q) c[r][q] = d[r][q] = 0.0;
+            const double* b1 = B1 + 4 * tj;
+            const double* b2 = B2 + 4 * tj;
+            for (int t = 0; t < K1; ++t) {
+                const bool two = t < K2;
+                const double2 x01 = lds2(b1 + t * ldb), x23 = lds2(b1 + t * ldb + 2);
+                double2 y01 = make_double2(0.0, 0.0), y23 = y01;
+                if (two) {
+                    y01 = lds2(b2 + t * ldb);
+                    y23 = lds2(b2 + t * ldb + 2);
+                }
+                const double xv[4] = {x01.x, x01.y, x23.x, x23.y};
+                const double yv[4] = {y01.x, y01.y, y23.x, y23.y};
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    const double av = tab[ix[r]];
+                    const double cw = lds(tab + ix[r]), sw = lds(ts + ix[r]);
                     ix[r] += kr[r];
                     ix[r] -= (ix[r] >= N) ? N : 0;
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) acc[r][q] = fma(av, bv[q], acc[r][q]);
+                    for (int q = 0; q < 4; ++q) {
+                        c[r][q] = fma(cw, xv[q], c[r][q]);
+                        d[r][q] = fma(sw, yv[q], d[r][q]);
+                    }
                 }
             }
             double c0[4] = {0.0, 0.0, 0.0, 0.0};
             if (C0) {
-                const double2 z01 = *reinterpret_cast<const double2*>(C0 + 4 * tj);
-                const double2 z23 = *reinterpret_cast<const double2*>(C0 + 4 * tj + 2);
+                const double2 z01 = lds2(C0 + 4 * tj), z23 = lds2(C0 + 4 * tj + 2);
                 c0[0] = z01.x;
                 c0[1] = z01.y;
                 c0[2] = z23.x;
@@ -163,34 +190,34 @@ __device__ __noinline__ void tgemm(const double* tab, int N, double sgn, int Mp,
             }
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                double* cr = C + (4 * ti + r) * ldc + 4 * tj;
-                *reinterpret_cast<double2*>(cr) =
-                    make_double2(c0[0] + sgn * acc[r][0], c0[1] + sgn * acc[r][1]);
-                *reinterpret_cast<double2*>(cr + 2) =
-                    make_double2(c0[2] + sgn * acc[r][2], c0[3] + sgn * acc[r][3]);
+                double* o1 = C1 + (4 * ti + r) * ldc + 4 * tj;
+                double* o2 = C2 + (4 * ti + r) * ldc + 4 * tj;
+                *reinterpret_cast<double2*>(o1) = make_double2(c0[0] + c[r][0], c0[1] + c[r][1]);
+                *reinterpret_cast<double2*>(o1 + 2) = make_double2(c0[2] + c[r][2], c0[3] + c[r][3]);
+                *reinterpret_cast<double2*>(o2) = make_double2(s2 * d[r][0], s2 * d[r][1]);
+                *reinterpret_cast<double2*>(o2 + 2) = make_double2(s2 * d[r][2], s2 * d[r][3]);
             }
         }
     } else {
-        W1MG_FOR2(k, j, Mp, Np) {
+        W1MG_FOR2(k, j, Mp, Nr) {
             int kr = k;
             kr -= (kr >= N) ? N : 0;
             kr -= (kr >= N) ? N : 0;
             int ix = kr;
-            double a0 = 0.0, a1 = 0.0;
-            const double* bj = B + j;
+            double c = 0.0, d = 0.0;
+            const double* b1 = B1 + j;
+            const double* b2 = B2 + j;
             int t = 0;
-            for (; t + 1 < K; t += 2) {
-                const double w0 = tab[ix];
+            for (; t < K2; ++t) {
+                const double cw = lds(tab + ix), sw = lds(ts + ix);
                 ix += kr;
                 ix -= (ix >= N) ? N : 0;
-                const double w1 = tab[ix];
-                ix += kr;
-                ix -= (ix >= N) ? N : 0;
-                a0 = fma(w0, bj[t * ldb], a0);
-                a1 = fma(w1, bj[(t + 1) * ldb], a1);
+                c = fma(cw, lds(b1 + t * ldb), c);
+                d = fma(sw, lds(b2 + t * ldb), d);
             }
-            if (t < K) a0 = fma(tab[ix], bj[t * ldb], a0);
-            C[k * ldc + j] = (C0 ? C0[j] : 0.0) + sgn * (a0 + a1);
+            if (t < K1) c = fma(lds(tab + ix), lds(b1 + t * ldb), c);
+            C1[k * ldc + j] = (C0 ? lds(C0 + j) : 0.0) + c;
+            C2[k * ldc + j] = s2 * d;
         }
     }
 }
@@ -243,8 +270,7 @@ __device__ __noinline__ void dct2_vectors(const DctPlan& p, int NV, int xs, doub
     // stage 1: A[k1][j] = X0 + sum cos S - i sum sin D, k1 < H1
     double* ReA = Q;
     double* ImA = Q + p.H1p * NpA;
-    tgemm(p.tw1, N1, 1.0, p.H1p, T1 + E1, SA, NpA, NpA, ReA, NpA, X0);
-    tgemm(p.tw1 + N1, N1, -1.0, p.H1p, T1, DA, NpA, NpA, ImA, NpA, nullptr);
+    tgemm2(p.tw1, N1, p.H1p, T1 + E1, T1, SA, DA, NpA, NpA, NA, ReA, ImA, NpA, X0, -1.0);
     __syncthreads();
     const int NB = NV * H1, NpB = round4(NB), W2 = 2 * NpB;
     double* Cp = Q;
@@ -288,8 +314,7 @@ __device__ __noinline__ void dct2_vectors(const DctPlan& p, int NV, int xs, doub
             }
         }
         __syncthreads();
-        tgemm(p.tw2, N2, 1.0, p.H2p, T2 + E2, SB, W2, W2, Cp, W2, A0);
-        tgemm(p.tw2 + N2, N2, 1.0, p.H2p, T2, DB, W2, W2, Sn, W2, nullptr);
+        tgemm2(p.tw2, N2, p.H2p, T2 + E2, T2, SB, DB, W2, W2, W2, Cp, Sn, W2, A0, 1.0);
         __syncthreads();
     }
     // V[k1, k2] = Cp - i Sn (k2 < H2), V[k1, N2 - k2] = Cp + i Sn; V[m-k] = conj V[k];
@@ -393,8 +418,7 @@ __device__ __noinline__ void dct3_vectors(const DctPlan& p, int NV, int xs, doub
         __syncthreads();
         double* Cp = Q;
         double* Sn = Q + p.H2p * W2;
-        tgemm(p.tw2, N2, 1.0, p.H2p, T2 + E2, SB, W2, W2, Cp, W2, A0);
-        tgemm(p.tw2 + N2, N2, 1.0, p.H2p, T2, DB, W2, W2, Sn, W2, nullptr);
+        tgemm2(p.tw2, N2, p.H2p, T2 + E2, T2, SB, DB, W2, W2, W2, Cp, Sn, W2, A0, 1.0);
         __syncthreads();
         // b[k1][n2] = Cp + i Sn (n2 < H2), b[k1][N2 - n2] = Cp - i Sn -> stage 1 inputs
         // (vector j = n2 NV + v)
@@ -426,8 +450,7 @@ __device__ __noinline__ void dct3_vectors(const DctPlan& p, int NV, int xs, doub
     // stage 1 (inverse, over k1): w[n1] = b0 + 2 (P - Q), w[N1 - n1] = b0 + 2 (P + Q)
     double* PP = Q;
     double* QQ = Q + p.H1p * NpA;
-    tgemm(p.tw1, N1, 1.0, p.H1p, T1 + E1, BR, NpA, NpA, PP, NpA, nullptr);
-    tgemm(p.tw1 + N1, N1, 1.0, p.H1p, T1, BI, NpA, NpA, QQ, NpA, nullptr);
+    tgemm2(p.tw1, N1, p.H1p, T1 + E1, T1, BR, BI, NpA, NpA, NA, PP, QQ, NpA, nullptr, 1.0);
     __syncthreads();
     // un-reorder: n = (N2 n1 + N1 n2) mod m -> y at idxA[n2][n1] (the forward
     // input map); r = n2 N1 + n1
