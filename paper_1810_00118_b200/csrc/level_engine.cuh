@@ -493,6 +493,9 @@ bool resident_ok(const Level& lv) {
 // the cluster engine wherever it fits (tests).
 // PDHG levels with m = n+1 <= 65 run level-resident (pdhg_engine.cuh)
 int g_pdhg_small = 1;
+// one-pair PDHG levels above that run level-persistent (pdhg_persist.cuh:
+// all iterations in one cooperative launch): 1 = on (default), 0 = off
+int g_pdhg_persist = 1;
 
 // cluster-size rule (W1MG_CLUSTER_PICK): 1 = fewest node passes per phase
 // (default), 0 = powers of two with >= 8 rows per CTA

@@ -12,6 +12,7 @@
 #include "pdhg_kernels.cuh"
 #include "pdhg_small.cuh"
 #include "dct_kernels.cuh"
+#include "pdhg_persist.cuh"
 
 namespace {
 
@@ -197,6 +198,9 @@ void dct_kernel_attrs() {
     CK(cudaFuncSetAttribute(dct_rows_inv_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     CK(cudaFuncSetAttribute(dct_rows_inv_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     CK(cudaFuncSetAttribute(dct_rows_inv_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(pdhg_persist_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(pdhg_persist_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(pdhg_persist_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     done |= 1ull << (dev & 63);
 }
 
@@ -346,6 +350,53 @@ void pdhg_iteration(w1mg_ctx* c, const PLevel& lv, int q) {
     CK(cudaGetLastError());
 }
 
+// Level-persistent PDHG for one pair (pdhg_persist.cuh): every iteration of
+// the level in one cooperative launch (g_pdhg_persist, level_engine.cuh).
+
+template <int Q>
+bool launch_pdhg_persist_q(w1mg_ctx* c, const PLevel& lv) {
+    const DctPlan& p = lv.dp;
+    const int m = p.m;
+    int R = 1;
+    while (R < 16 && (m + R - 1) / R > c->num_sms) R <<= 1;
+    const size_t smem = dct_smem_bytes(p, R);
+    if (smem > kDctSmemMax) return false;
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdhg_persist_kernel<Q>, 256, smem));
+    if (occ < 1) return false;
+    const int chunks = (m + R - 1) / R;
+    const int G = std::min(chunks, c->num_sms * occ);
+    const bool fresh = c->bufs.find("persist.bar") == c->bufs.end();
+    unsigned* bar = c->get<unsigned>("persist.bar", 2);
+    int* err = c->get<int>("persist.err", 1);
+    if (fresh) CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), c->stream));
+    CK(cudaMemsetAsync(bar, 0, sizeof(unsigned), c->stream));  // arrivals (gen keeps counting)
+    CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
+    GridBar gb{bar, bar + 1, err};
+    double* part = c->get<double>("persist.part", (size_t)3 * G);
+    const double scale = 1.0 / (4.0 * double(m) * double(m));  // poisson.cpp:93
+    SweepArgs a = lv.args;
+    const DctPlan* pp = &p;
+    const double* lam = lv.lam;
+    void* args[] = {(void*)&a, (void*)pp, (void*)&lam, (void*)&R, (void*)&R, (void*)&scale,
+                    (void*)&gb, (void*)&part};
+    CK(cudaLaunchCooperativeKernel((const void*)pdhg_persist_kernel<Q>, dim3(G), dim3(256), args,
+                                   smem, c->stream));
+    ++c->launches;
+    int herr = 0;
+    CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (herr) fail(W1MG_ECUDA, "level-persistent PDHG: grid barrier timed out");
+    return true;
+}
+
+bool launch_pdhg_persist(w1mg_ctx* c, const PLevel& lv, int q) {
+    if (!g_pdhg_persist || lv.B != 1) return false;
+    if (q == 0) return launch_pdhg_persist_q<0>(c, lv);
+    if (q == 1) return launch_pdhg_persist_q<1>(c, lv);
+    return launch_pdhg_persist_q<2>(c, lv);
+}
+
 // small levels: one launch per level, one CTA per pair (pdhg_small.cuh);
 // W1MG_PDHG_SMALL = 1 (default, m <= 33), 2 (m <= 65), 0 (streaming only)
 // (g_pdhg_small, level_engine.cuh)
@@ -382,6 +433,7 @@ void run_pdhg_iters(w1mg_ctx* c, const PLevel& lv, int q, long max_iters) {
         else launch_pdhg_small<2>(c, lv);
         return;
     }
+    if (launch_pdhg_persist(c, lv, q)) return;
     constexpr int K = 8;
     if (max_iters < K) {
         for (long k = 0; k < max_iters; ++k) pdhg_iteration(c, lv, q);

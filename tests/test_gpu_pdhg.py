@@ -67,17 +67,20 @@ def test_project_affine(n):
     assert _rel(again.x_edges, out.x_edges) <= 1e-10
 
 
-@pytest.fixture(params=["streaming", "resident"])
+@pytest.fixture(params=["streaming", "persistent", "resident"])
 def pdhg_engine(request):
     """streaming: 3-launch iteration (row DCT-II + pre, column DCT-II /
-    divide / DCT-III, row DCT-III + post); resident: one CTA per pair for
-    m <= 65."""
+    divide / DCT-III, row DCT-III + post); persistent: every iteration of a
+    one-pair level in one cooperative launch (pdhg_persist.cuh); resident:
+    one CTA per pair for m <= 65, persistent above."""
     from paper_1810_00118_b200 import _lib
 
     L = _lib.lib()
     L.w1mg_set_pdhg_small(2 if request.param == "resident" else 0)
+    L.w1mg_set_option(b"pdhg_persist", 0 if request.param == "streaming" else 1)
     yield request.param
     L.w1mg_set_pdhg_small(1)
+    L.w1mg_set_option(b"pdhg_persist", 1)
 
 
 @pytest.mark.parametrize("n", [31, 32, 64, 128, 256])
