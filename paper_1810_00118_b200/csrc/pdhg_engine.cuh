@@ -378,8 +378,13 @@ bool launch_pdhg_persist_q(w1mg_ctx* c, const PLevel& lv) {
     SweepArgs a = lv.args;
     const DctPlan* pp = &p;
     const double* lam = lv.lam;
+    unsigned long long* stamps = nullptr;
+    if (std::getenv("W1MG_PERSIST_STAMPS")) {
+        stamps = c->get<unsigned long long>("persist.stamps", 640);
+        CK(cudaMemsetAsync(stamps, 0, 640 * 8, c->stream));
+    }
     void* args[] = {(void*)&a, (void*)pp, (void*)&lam, (void*)&R, (void*)&R, (void*)&scale,
-                    (void*)&gb, (void*)&part};
+                    (void*)&gb, (void*)&part, (void*)&stamps};
     CK(cudaLaunchCooperativeKernel((const void*)pdhg_persist_kernel<Q>, dim3(G), dim3(256), args,
                                    smem, c->stream));
     ++c->launches;
@@ -387,6 +392,21 @@ bool launch_pdhg_persist_q(w1mg_ctx* c, const PLevel& lv) {
     CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (herr) fail(W1MG_ECUDA, "level-persistent PDHG: grid barrier timed out");
+    if (stamps) {  // per-phase ns of iterations 8..63: A, bar, B, bar, C, bar, D, bar
+        std::vector<unsigned long long> h(640);
+        CK(cudaMemcpy(h.data(), stamps, 640 * 8, cudaMemcpyDeviceToHost));
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int cnt = 0;
+        for (int it = 8; it < 63; ++it) {
+            if (!h[(it + 1) * 10]) break;
+            for (int q = 0; q < 8; ++q) acc[q] += double(h[it * 10 + q + 1] - h[it * 10 + q]);
+            ++cnt;
+        }
+        if (cnt)
+            std::fprintf(stderr, "persist m=%d G=%d R=%d ns: A %.0f bar %.0f B %.0f bar %.0f C %.0f bar %.0f D %.0f bar %.0f\n",
+                         m, G, R, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
+                         acc[4] / cnt, acc[5] / cnt, acc[6] / cnt, acc[7] / cnt);
+    }
     return true;
 }
 

@@ -97,7 +97,8 @@ __device__ __forceinline__ double pdhg_rhs_cg(const SweepArgs& a, int i, int j) 
 template <int QN>
 __global__ void __launch_bounds__(256, 1)
 pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict__ lambda, int Rr,
-                    int Rc, double scale, GridBar gb, double* __restrict__ part) {
+                    int Rc, double scale, GridBar gb, double* __restrict__ part,
+                    unsigned long long* __restrict__ stamps) {
     __shared__ uint64_t bar;
     __shared__ int s_ok;
     __shared__ int s_stop;
@@ -125,7 +126,14 @@ pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict
     double* psi = pslot_w(a, 0, P_PSI);
     const int nrc = (m + Rr - 1) / Rr, ncc = (m + Rc - 1) / Rc;
     const double mu = a.mu, tau = a.tau, ih = a.ih;
-    for (;;) {
+    long iter = 0;
+    // diagnostics (W1MG_PERSIST_STAMPS): CTA 0 stamps the end of every phase
+    // and barrier of the first 64 iterations
+    auto stamp = [&](int q) {
+        if (stamps && blockIdx.x == 0 && threadIdx.x == 0 && iter < 64) stamps[iter * 10 + q] = gtimer();
+    };
+    for (;; ++iter) {
+        stamp(0);
         // ---- A: rows, pre step + DCT-II
         for (int c = blockIdx.x; c < nrc; c += gridDim.x) {
             const int j0 = c * Rr;
@@ -140,7 +148,9 @@ pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict
             }
             __syncthreads();
         }
+        stamp(1);
         if (!grid_barrier(gb, gen, &s_ok)) return;
+        stamp(2);
         // ---- B: columns, DCT-II, divide, DCT-III (X rows = columns, stride m)
         for (int c = blockIdx.x; c < ncc; c += gridDim.x) {
             const int c0 = c * Rc;
@@ -163,7 +173,9 @@ pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict
             }
             __syncthreads();
         }
+        stamp(3);
         if (!grid_barrier(gb, gen, &s_ok)) return;
+        stamp(4);
         // ---- C: rows, DCT-III -> psi
         for (int c = blockIdx.x; c < nrc; c += gridDim.x) {
             const int j0 = c * Rr;
@@ -178,7 +190,9 @@ pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict
             }
             __syncthreads();
         }
+        stamp(5);
         if (!grid_barrier(gb, gen, &s_ok)) return;
+        stamp(6);
         // ---- D: post step on the CTA's rows + Eq. 12 partial sums
         double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
         for (int c = blockIdx.x; c < nrc; c += gridDim.x) {
@@ -256,7 +270,9 @@ pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict
             part[blockIdx.x * 3 + 1] = t1;
             part[blockIdx.x * 3 + 2] = t2;
         }
+        stamp(7);
         if (!grid_barrier(gb, gen, &s_ok)) return;
+        stamp(8);
         // ---- E: Eq. 12 and the stop rule, identical in every CTA (the sweep
         // count is tracked locally, so no CTA reads what CTA 0 records)
         if (threadIdx.x == 0) {
