@@ -366,11 +366,9 @@ bool launch_pdhg_persist_q(w1mg_ctx* c, const PLevel& lv) {
     if (occ < 1) return false;
     const int chunks = (m + R - 1) / R;
     const int G = std::min(chunks, c->num_sms * occ);
-    const bool fresh = c->bufs.find("persist.bar") == c->bufs.end();
     unsigned* bar = c->get<unsigned>("persist.bar", 2);
     int* err = c->get<int>("persist.err", 1);
-    if (fresh) CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), c->stream));
-    CK(cudaMemsetAsync(bar, 0, sizeof(unsigned), c->stream));  // arrivals (gen keeps counting)
+    CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), c->stream));  // arrival counter
     CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
     GridBar gb{bar, bar + 1, err};
     double* part = c->get<double>("persist.part", (size_t)3 * G);

@@ -27,8 +27,8 @@
 namespace w1mg_dev {
 
 struct GridBar {
-    unsigned* count;  // arrivals of the current barrier
-    unsigned* gen;    // barrier generation (monotone across launches)
+    unsigned* count;  // arrivals, monotone across barriers and launches
+    unsigned* gen;    // unused slot (kept zero)
     int* err;         // set on a barrier timeout: every CTA leaves
 };
 
@@ -44,22 +44,21 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// Sense-by-generation grid barrier (all CTAs co-resident: cooperative
-// launch).  Returns false when the barrier timed out (2 s): the caller
-// leaves the kernel; the host then fails loudly.
-__device__ __forceinline__ bool grid_barrier(const GridBar& gb, unsigned& gen, int* s_ok) {
+// Grid barrier over a monotone arrival counter (all CTAs co-resident:
+// cooperative launch): barrier number q completes when the counter reaches
+// base + q * gridDim.x.  One release-add per CTA and acquire polling -- no
+// reset, no second atomic on the critical path.  `target` is the running
+// target (thread 0 only).  Returns false when the barrier timed out (2 s):
+// the caller leaves the kernel; the host then fails loudly.
+__device__ __forceinline__ bool grid_barrier(const GridBar& gb, unsigned& target, int* s_ok) {
     __syncthreads();
     if (threadIdx.x == 0) {
         int ok = 1;
-        __threadfence();
-        const unsigned arrived = atomicAdd(gb.count, 1u);
-        if (arrived == gridDim.x - 1) {
-            atomicExch(gb.count, 0u);
-            __threadfence();
-            atomicAdd(gb.gen, 1u);
-        } else {
+        target += gridDim.x;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gb.count) : "memory");
+        if ((int)(ld_acquire_u32(gb.count) - target) < 0) {
             const unsigned long long t0 = gtimer();
-            while (ld_acquire_u32(gb.gen) == gen) {
+            while ((int)(ld_acquire_u32(gb.count) - target) < 0) {
                 if (*(volatile int*)gb.err || gtimer() - t0 > 2000000000ull) {
                     atomicExch(gb.err, 1);
                     ok = 0;
@@ -69,9 +68,30 @@ __device__ __forceinline__ bool grid_barrier(const GridBar& gb, unsigned& gen, i
         }
         *s_ok = ok;
     }
-    ++gen;
     __syncthreads();
     return *s_ok != 0;
+}
+
+// Batched gather: st(a, b, ld(a, b)) for a < NA, b < NB, U loads per thread
+// in flight before any is used (L2 latency, not issue, bounds the load
+// phases of a one-pair level).
+template <int U, class Ld, class St>
+__device__ __forceinline__ void gather2(int NA, int NB, Ld ld, St st) {
+    const int tot = NA * NB;
+    for (int e0 = threadIdx.x; e0 < tot; e0 += U * blockDim.x) {
+        double x[U];
+        int ia[U], ib[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * blockDim.x;
+            ia[u] = e / NB;
+            ib[u] = e - ia[u] * NB;
+            x[u] = (e < tot) ? ld(ia[u], ib[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (e0 + u * (int)blockDim.x < tot) st(ia[u], ib[u], x[u]);
+    }
 }
 
 // pdhg_rhs with L2 loads (rows written by other CTAs earlier in the launch)
@@ -114,13 +134,9 @@ pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict
     const int NV = Rr > Rc ? Rr : Rc;
     // tables once per level (one bulk copy); no rows through the barrier
     DctSmem d = dct_begin(g, NV, nullptr, L, 0, 0, &bar);
+    // the arrival counter is zeroed by the host before the launch
     unsigned gen = 0;
-    if (threadIdx.x == 0) gen = ld_acquire_u32(gb.gen);
     dct_wait(&bar);
-    __shared__ unsigned s_gen;
-    if (threadIdx.x == 0) s_gen = gen;
-    __syncthreads();
-    gen = s_gen;
     const int xs = d.xs;
     double* T = pslot_w(a, 0, P_T);
     double* psi = pslot_w(a, 0, P_PSI);
@@ -137,10 +153,9 @@ pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict
         // ---- A: rows, pre step + DCT-II
         for (int c = blockIdx.x; c < nrc; c += gridDim.x) {
             const int j0 = c * Rr;
-            W1MG_FOR2(v, i, Rr, m) {
-                const int j = j0 + v;
-                d.X[v * xs + i] = (j < m) ? pdhg_rhs_cg(a, i, j) : 0.0;
-            }
+            gather2<4>(
+                Rr, m, [&](int v, int i) { return (j0 + v < m) ? pdhg_rhs_cg(a, i, j0 + v) : 0.0; },
+                [&](int v, int i, double x) { d.X[v * xs + i] = x; });
             __syncthreads();
             dct2_vectors(d.p, Rr, xs, d.X, d.P, d.Q);
             W1MG_FOR2(v, i, Rr, m) {
@@ -154,9 +169,9 @@ pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict
         // ---- B: columns, DCT-II, divide, DCT-III (X rows = columns, stride m)
         for (int c = blockIdx.x; c < ncc; c += gridDim.x) {
             const int c0 = c * Rc;
-            W1MG_FOR2(j, v, m, Rc) {
-                d.X[v * m + j] = (c0 + v < m) ? __ldcg(T + L.at(c0 + v, j)) : 0.0;
-            }
+            gather2<8>(
+                m, Rc, [&](int j, int v) { return (c0 + v < m) ? __ldcg(T + L.at(c0 + v, j)) : 0.0; },
+                [&](int j, int v, double x) { d.X[v * m + j] = x; });
             __syncthreads();
             dct2_vectors(d.p, Rc, m, d.X, d.P, d.Q);
             W1MG_FOR2(v, k2, Rc, m) {
@@ -179,10 +194,9 @@ pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict
         // ---- C: rows, DCT-III -> psi
         for (int c = blockIdx.x; c < nrc; c += gridDim.x) {
             const int j0 = c * Rr;
-            W1MG_FOR2(v, i, Rr, m) {
-                const int j = j0 + v;
-                d.X[v * xs + i] = (j < m) ? __ldcg(T + L.at(i, j)) : 0.0;
-            }
+            gather2<8>(
+                Rr, m, [&](int v, int i) { return (j0 + v < m) ? __ldcg(T + L.at(i, j0 + v)) : 0.0; },
+                [&](int v, int i, double x) { d.X[v * xs + i] = x; });
             __syncthreads();
             dct3_vectors(d.p, Rr, xs, d.X, d.P, d.Q);
             W1MG_FOR2(v, i, Rr, m) {
