@@ -362,7 +362,7 @@ bool launch_pdhg_persist_q(w1mg_ctx* c, const PLevel& lv) {
     const size_t smem = dct_smem_bytes(p, R);
     if (smem > kDctSmemMax) return false;
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdhg_persist_kernel<Q>, 256, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdhg_persist_kernel<Q>, kPersistThreads, smem));
     if (occ < 1) return false;
     const int chunks = (m + R - 1) / R;
     const int G = std::min(chunks, c->num_sms * occ);
@@ -383,8 +383,8 @@ bool launch_pdhg_persist_q(w1mg_ctx* c, const PLevel& lv) {
     }
     void* args[] = {(void*)&a, (void*)pp, (void*)&lam, (void*)&R, (void*)&R, (void*)&scale,
                     (void*)&gb, (void*)&part, (void*)&stamps};
-    CK(cudaLaunchCooperativeKernel((const void*)pdhg_persist_kernel<Q>, dim3(G), dim3(256), args,
-                                   smem, c->stream));
+    CK(cudaLaunchCooperativeKernel((const void*)pdhg_persist_kernel<Q>, dim3(G),
+                                   dim3(kPersistThreads), args, smem, c->stream));
     ++c->launches;
     int herr = 0;
     CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));

@@ -114,15 +114,17 @@ __device__ __forceinline__ double pdhg_rhs_cg(const SweepArgs& a, int i, int j) 
 
 // One pair (b = 0), all iterations of the level.  Rr rows / Rc columns per
 // chunk (powers of two); chunk c of a phase is done by CTA c mod gridDim.
+constexpr int kPersistThreads = 512;  // 16 warps per SM: the phases are latency chains
+
 template <int QN>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kPersistThreads, 1)
 pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict__ lambda, int Rr,
                     int Rc, double scale, GridBar gb, double* __restrict__ part,
                     unsigned long long* __restrict__ stamps) {
     __shared__ uint64_t bar;
     __shared__ int s_ok;
     __shared__ int s_stop;
-    __shared__ double red[8][3];
+    __shared__ double red[kPersistThreads / 32][3];
     PairCtl* ctl = a.ctl;
     if (*(volatile int*)&ctl->done) return;
     // read before the first barrier, i.e. before CTA 0 records anything
