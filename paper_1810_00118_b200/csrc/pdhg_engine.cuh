@@ -357,13 +357,18 @@ template <int Q>
 bool launch_pdhg_persist_q(w1mg_ctx* c, const PLevel& lv) {
     const DctPlan& p = lv.dp;
     const int m = p.m;
-    int R = 1;
-    while (R < 16 && (m + R - 1) / R > c->num_sms) R <<= 1;
-    const size_t smem = dct_smem_bytes(p, R);
-    if (smem > kDctSmemMax) return false;
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdhg_persist_kernel<Q>, kPersistThreads, smem));
-    if (occ < 1) return false;
+    // vectors per chunk: the fewest whose chunks fit co-resident (two CTAs per
+    // SM where the shared memory allows)
+    int R = 1, occ = 0;
+    size_t smem = 0;
+    for (;; R <<= 1) {
+        if (R > 16) return false;
+        smem = dct_smem_bytes(p, R);
+        if (smem > kDctSmemMax) return false;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdhg_persist_kernel<Q>,
+                                                         kPersistThreads, smem));
+        if (occ >= 1 && (m + R - 1) / R <= c->num_sms * std::min(occ, 2)) break;
+    }
     const int chunks = (m + R - 1) / R;
     const int G = std::min(chunks, c->num_sms * occ);
     unsigned* bar = c->get<unsigned>("persist.bar", 2);
