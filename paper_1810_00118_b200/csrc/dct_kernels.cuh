@@ -158,6 +158,7 @@ __device__ __noinline__ void tgemm2(const double* tab, int N, int Mp, int K1, in
                 for (int q = 0; q < 4; ++q) c[r][q] = d[r][q] = 0.0;
             const double* b1 = B1 + 4 * tj;
             const double* b2 = B2 + 4 * tj;
+#pragma unroll 2
             for (int t = 0; t < K1; ++t) {
                 const bool two = t < K2;
                 const double2 x01 = lds2(b1 + t * ldb), x23 = lds2(b1 + t * ldb + 2);
@@ -207,7 +208,35 @@ __device__ __noinline__ void tgemm2(const double* tab, int N, int Mp, int K1, in
             double c = 0.0, d = 0.0;
             const double* b1 = B1 + j;
             const double* b2 = B2 + j;
+            // four steps per trip: the index walk and 16 independent shared
+            // loads issue before the FMAs, two accumulator pairs
+            double c1 = 0.0, d1 = 0.0;
             int t = 0;
+            for (; t + 3 < K2; t += 4) {
+                int i4[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    i4[u] = ix;
+                    ix += kr;
+                    ix -= (ix >= N) ? N : 0;
+                }
+                double cw[4], sw[4], x1[4], x2[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    cw[u] = lds(tab + i4[u]);
+                    sw[u] = lds(ts + i4[u]);
+                    x1[u] = lds(b1 + (t + u) * ldb);
+                    x2[u] = lds(b2 + (t + u) * ldb);
+                }
+                c = fma(cw[0], x1[0], c);
+                d = fma(sw[0], x2[0], d);
+                c1 = fma(cw[1], x1[1], c1);
+                d1 = fma(sw[1], x2[1], d1);
+                c = fma(cw[2], x1[2], c);
+                d = fma(sw[2], x2[2], d);
+                c1 = fma(cw[3], x1[3], c1);
+                d1 = fma(sw[3], x2[3], d1);
+            }
             for (; t < K2; ++t) {
                 const double cw = lds(tab + ix), sw = lds(ts + ix);
                 ix += kr;
@@ -216,6 +245,8 @@ __device__ __noinline__ void tgemm2(const double* tab, int N, int Mp, int K1, in
                 d = fma(sw, lds(b2 + t * ldb), d);
             }
             if (t < K1) c = fma(lds(tab + ix), lds(b1 + t * ldb), c);
+            c += c1;
+            d += d1;
             C1[k * ldc + j] = (C0 ? lds(C0 + j) : 0.0) + c;
             C2[k * ldc + j] = s2 * d;
         }

@@ -367,7 +367,7 @@ bool launch_pdhg_persist_q(w1mg_ctx* c, const PLevel& lv) {
         if (smem > kDctSmemMax) return false;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdhg_persist_kernel<Q>,
                                                          kPersistThreads, smem));
-        if (occ >= 1 && (m + R - 1) / R <= c->num_sms * std::min(occ, 2)) break;
+        if (occ >= 1 && (m + R - 1) / R <= c->num_sms) break;
     }
     const int chunks = (m + R - 1) / R;
     const int G = std::min(chunks, c->num_sms * occ);

@@ -114,13 +114,13 @@ __device__ __forceinline__ double pdhg_rhs_cg(const SweepArgs& a, int i, int j) 
 
 // One pair (b = 0), all iterations of the level.  Rr rows / Rc columns per
 // chunk (powers of two); chunk c of a phase is done by CTA c mod gridDim.
-// 256 threads, two CTAs per SM when their shared memory fits: the phases are
-// latency chains, so two CTAs per SM (each with half the vectors) interleave
-// (512 threads in one CTA measured slower: 65^2 3.8 vs 3.2 us per row phase)
+// 256 threads, one CTA per SM (measured: 512 threads in one CTA 65^2 row
+// phase 3.8 vs 3.2 us; two 256-thread CTAs per SM with half the vectors each:
+// no faster per phase and 2-3x slower barriers)
 constexpr int kPersistThreads = 256;
 
 template <int QN>
-__global__ void __launch_bounds__(kPersistThreads, 2)
+__global__ void __launch_bounds__(kPersistThreads, 1)
 pdhg_persist_kernel(const SweepArgs a, const DctPlan g, const double* __restrict__ lambda, int Rr,
                     int Rc, double scale, GridBar gb, double* __restrict__ part,
                     unsigned long long* __restrict__ stamps) {
