@@ -571,7 +571,7 @@ def main(argv=None):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            trj = json.load(f)
+            trj = json.load(f).get(args.numerics, {})
     flops_ns = trj.get("fp64_flops_per_node_sweep")
     inst_ns = trj.get("fp64_inst_per_node_sweep")
     tr = trj.get("dram_bytes_per_launch")

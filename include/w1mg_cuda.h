@@ -266,9 +266,12 @@ int w1mg_slab_cp_run(w1mg_ctx* ctx, w1mg_slab_comm* comm, int n, int nslabs, con
                      double mu, double tau, double tol, long max_iters, double* mx, double* my,
                      double* phi, double* fpr_hist, long hist_cap, w1mg_cp_report* rep);
 
-/* Config-5 cascade on one large grid: levels 0..L-2 replicated on every rank,
- * the finest level row-slab partitioned (comm == NULL: `nslabs` slabs emulated
- * on one device).  Outputs: the finest level's owned rows; stats: all levels. */
+/* Config-5 cascade on one large grid: levels with n >= the "slab_min_n"
+ * option (default 1024) and the finest level are row-slab partitioned, the
+ * coarser ones replicated on every rank (comm == NULL: `nslabs` slabs
+ * emulated on one device).  After a partitioned level its slabs are gathered
+ * back (NCCL broadcast of each owner's rows) to prolong into the next.
+ * Outputs: the finest level's owned rows; stats: all levels. */
 int w1mg_ml_slab_cp_run(w1mg_ctx* ctx, w1mg_slab_comm* comm, int nslabs, int n_finest,
                         const double* rho_levels, const w1mg_ml_params* prm, double* mx,
                         double* my, double* phi, w1mg_level_stats* stats, w1mg_cp_report* rep);

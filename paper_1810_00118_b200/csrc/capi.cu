@@ -72,6 +72,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_PDL")) g_pdl = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_FAST")) g_fast = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_PDHG_PERSIST")) g_pdhg_persist = std::atoi(v) != 0;
+        if (const char* v = std::getenv("W1MG_SLAB_MIN_N")) g_slab_min_n = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
             const int w = std::atoi(v);
@@ -600,6 +601,7 @@ int w1mg_set_option(const char* name, long value) {
     const std::string k(name);
     const int v = (int)value;
     if (k == "pdhg_persist" && (v == 0 || v == 1)) g_pdhg_persist = v;
+    else if (k == "slab_min_n" && v >= 1) g_slab_min_n = v;
     else if (k == "pdhg_small" && v >= 0 && v <= 2) g_pdhg_small = v;
     else if (k == "cluster_pick" && (v == 0 || v == 1)) g_cluster_pick = v;
     else if (k == "compact") g_compact = v != 0;

@@ -117,8 +117,30 @@ double inner_h(const FluxField& a, const FluxField& b) {
 
 double norm_L2(const ScalarField& a) { return std::sqrt(inner_h(a, a)); }
 double norm_L2(const FluxField& a) { return std::sqrt(inner_h(a, a)); }
-double norm_plain(const ScalarField& a) { return std::sqrt(inner_h(a, a)) / a.grid.h; }
-double norm_plain(const FluxField& a) { return std::sqrt(inner_h(a, a)) / a.grid.h; }
+// norm_plain (grid.cpp:117-128): the unweighted Euclidean norm -- a host
+// Neumaier sum in the reference's order (O(V) utility, not the solve path),
+// so the bits match the reference exactly (sqrt(inner_h)/h would round
+// through the h^2 scaling).
+namespace {
+double neumaier_sq(const std::vector<double>& v, double& s, double& c) {
+    for (double x : v) {
+        const double y = x * x, t = s + y;
+        if (std::fabs(s) >= std::fabs(y)) c += (s - t) + y;
+        else c += (y - t) + s;
+        s = t;
+    }
+    return s + c;
+}
+}  // namespace
+double norm_plain(const ScalarField& a) {
+    double s = 0.0, c = 0.0;
+    return std::sqrt(neumaier_sq(a.values, s, c));
+}
+double norm_plain(const FluxField& a) {
+    double s = 0.0, c = 0.0;
+    neumaier_sq(a.x_edges, s, c);
+    return std::sqrt(neumaier_sq(a.y_edges, s, c));
+}
 
 double operator_norm_bound(const GridSpec& grid) { return 2.0 * std::sqrt(2.0) / grid.h; }
 

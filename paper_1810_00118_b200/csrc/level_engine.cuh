@@ -493,6 +493,9 @@ bool resident_ok(const Level& lv) {
 // the cluster engine wherever it fits (tests).
 // PDHG levels with m = n+1 <= 65 run level-resident (pdhg_engine.cuh)
 int g_pdhg_small = 1;
+// levels of a config-5 cascade with n >= g_slab_min_n are row-slab
+// partitioned (the finest always); option "slab_min_n" / W1MG_SLAB_MIN_N
+int g_slab_min_n = 1024;
 // one-pair PDHG levels above that run level-persistent (pdhg_persist.cuh:
 // all iterations in one cooperative launch): 1 = on (default), 0 = off
 int g_pdhg_persist = 1;

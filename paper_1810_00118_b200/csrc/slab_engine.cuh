@@ -233,9 +233,9 @@ SlabSet make_slabs(w1mg_ctx* c, const std::string& tag, int n, int R, w1mg_slab_
     s.red = c->get<double>(tag + ".red", 3 * nloc);
     s.sums = c->get<double>(tag + ".sums", 3);
     s.ndone = c->get<int>(tag + ".ndone_all", 1);
-    s.peer = comm ? (comm->peer_n > 0) : (g_slab_peer != 0);
-    if (comm && s.peer && comm->peer_n != n)
-        fail(W1MG_EINVAL, "slab comm peer memory was enabled for another grid size");
+    // peer transport where this rank's arena is laid out for this grid size;
+    // other partitioned levels of a cascade use the NCCL transport
+    s.peer = comm ? (comm->peer_n == n) : (g_slab_peer != 0);
     for (int q = 0; q < nloc; ++q) {
         const int r = comm ? comm->rank : q;
         const bool first = comm ? (r == 0) : (q == 0);
@@ -475,6 +475,39 @@ void slab_load_from_level(w1mg_ctx* c, SlabSet& s, const Level& full) {
     }
 }
 
+// After a partitioned level: every slab's owned rows of the latest state
+// (phi, m_x, m_y at parity `cur`) back into the whole-grid level F (parity 0,
+// F's control block cur = 0) -- on a communicator each rank stores its rows
+// and the row blocks are broadcast from their owners (one NCCL group), so
+// every rank holds the full level for the next prolongation.
+void slab_store_to_level(w1mg_ctx* c, SlabSet& s, Level& F, int cur) {
+    const int n = s.n;
+    const size_t row_bytes = (size_t)F.L.pitch * 8;
+    const int src_slot[3] = {PHI0 + cur, MX0 + cur, MY0 + cur};
+    const int dst_slot[3] = {PHI0, MX0, MY0};
+    for (auto& lv : s.lv) {
+        const int r0 = lv.args.jlo, r1 = std::min(lv.args.jhi, n + 1);
+        for (int q = 0; q < 3; ++q)
+            CK(cudaMemcpy2DAsync(slot_ptr(F, 0, dst_slot[q]) + F.L.at(0, r0), row_bytes,
+                                 slot_ptr(lv, 0, src_slot[q]) + lv.L.at(0, r0), row_bytes,
+                                 row_bytes, r1 - r0, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    if (s.comm && s.comm->world > 1) {
+        check_nccl(ncclGroupStart(), "group start");
+        for (int r = 0; r < s.comm->world; ++r) {
+            const int r0 = s.bounds[r], r1 = std::min(s.bounds[r + 1], n + 1);
+            for (int q = 0; q < 3; ++q) {
+                double* p = slot_ptr(F, 0, dst_slot[q]) + F.L.at(0, r0);
+                check_nccl(ncclBroadcast(p, p, (size_t)(r1 - r0) * F.L.pitch, ncclDouble, r,
+                                         s.comm->comm, c->stream),
+                           "broadcast level rows");
+            }
+        }
+        check_nccl(ncclGroupEnd(), "group end");
+    }
+    CK(cudaMemsetAsync(&F.ctl->cur, 0, sizeof(int), c->stream));
+}
+
 }  // namespace
 
 extern "C" {
@@ -498,55 +531,74 @@ int w1mg_ml_slab_cp_run(w1mg_ctx* c, w1mg_slab_comm* comm, int nslabs, int n_fin
             put_nodes(c, L, 0, RHO, rho_levels + off, cudaMemcpyDefault);
             off += (size_t)(L.n + 1) * (L.n + 1);
         }
-        // replicated coarse cascade
-        std::vector<Level> coarse(lv.begin(), lv.end() - 1);
-        w1mg_ml_params pc = *prm;
-        pc.levels = levels - 1;
+        // levels 0 .. p0-1 replicated (identical on every rank), p0 .. L-1
+        // row-slab partitioned: every level with n >= g_slab_min_n, and the
+        // finest in any case
+        int p0 = levels - 1;
+        while (p0 > 0 && lv[p0 - 1].n >= g_slab_min_n) --p0;
         long* it = c->get<long>("mlsl.iters", levels);
         double* ff = c->get<double>("mlsl.fpr", levels);
         double* tl = c->get<double>("mlsl.tol", levels);
         std::vector<double> secs;
-        run_cascade(c, coarse, pc, it, ff, tl, &secs);
-        // finest: prolong into the whole-grid level, then cut into slabs
-        Level& F = lv.back();
-        dim3 blk(32, 8);
-        prolong_kernel<<<node_grid(F.n, 1, blk), blk, 0, c->stream>>>(
-            coarse.back().base, coarse.back().L, coarse.back().ctl, F.base, F.L);
-        ++c->launches;
-        CK(cudaGetLastError());
-        double tol = (prm->rel_tol > 0 || !prm->eps) ? 0.0 : prm->eps[levels - 1];
-        if (prm->rel_tol > 0) {
-            double* rs = c->get<double>("mlsl.rho_sq", 1);
-            const double h = 1.0 / F.n;
-            reduce_pairs(c, FSlotSq{F.base, F.L, RHO}, F.n + 1, F.n + 1, 1, h * h, 1.0, rs);
-            double hrs = 0.0;
-            CK(cudaMemcpyAsync(&hrs, rs, 8, cudaMemcpyDeviceToHost, c->stream));
+        std::vector<long> hit(levels, 0);
+        std::vector<double> hff(levels, 0.0), htl(levels, 0.0), hsec(levels, 0.0);
+        if (p0 > 0) {
+            std::vector<Level> coarse(lv.begin(), lv.begin() + p0);
+            w1mg_ml_params pc = *prm;
+            pc.levels = p0;
+            run_cascade(c, coarse, pc, it, ff, tl, &secs);
+            CK(cudaMemcpyAsync(hit.data(), it, p0 * sizeof(long), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(hff.data(), ff, p0 * 8, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(htl.data(), tl, p0 * 8, cudaMemcpyDeviceToHost, c->stream));
             CK(cudaStreamSynchronize(c->stream));
-            tol = (prm->rel_tol * F.args.tau) * hrs;  // as init_ctl_kernel
+            for (int l = 0; l < p0; ++l) hsec[l] = secs[l];
         }
-        const double step = w1mg_cp_step_size(F.n, prm->step_mode);
-        SlabSet s = make_slabs(c, "mlsl.slab", F.n, nslabs, comm, step, step, nullptr, 0);
-        slab_load_from_level(c, s, F);
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
-        CK(cudaEventRecord(e0, c->stream));
-        slab_run(c, s, prm->pnorm, tol, prm->max_iters);
-        CK(cudaEventRecord(e1, c->stream));
-        PairCtl hc;
-        CK(cudaMemcpyAsync(&hc, s.ctl, sizeof(PairCtl), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        slab_after_run(s, hc);
-        std::vector<long> hit(levels - 1);
-        std::vector<double> hff(levels - 1), htl(levels - 1);
-        CK(cudaMemcpyAsync(hit.data(), it, (levels - 1) * sizeof(long), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(hff.data(), ff, (levels - 1) * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(htl.data(), tl, (levels - 1) * 8, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+        SlabSet s;
+        PairCtl hc{};
+        double tol = 0.0;
         float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, e0, e1));
+        dim3 blk(32, 8);
+        for (int l = p0; l < levels; ++l) {
+            Level& F = lv[l];
+            if (l > 0) {  // prolong the (whole, gathered) coarser level into F
+                prolong_kernel<<<node_grid(F.n, 1, blk), blk, 0, c->stream>>>(
+                    lv[l - 1].base, lv[l - 1].L, lv[l - 1].ctl, F.base, F.L);
+                ++c->launches;
+                CK(cudaGetLastError());
+            }
+            tol = (prm->rel_tol > 0 || !prm->eps) ? 0.0 : prm->eps[l];
+            if (prm->rel_tol > 0) {
+                double* rs = c->get<double>("mlsl.rho_sq", 1);
+                const double h = 1.0 / F.n;
+                reduce_pairs(c, FSlotSq{F.base, F.L, RHO}, F.n + 1, F.n + 1, 1, h * h, 1.0, rs);
+                double hrs = 0.0;
+                CK(cudaMemcpyAsync(&hrs, rs, 8, cudaMemcpyDeviceToHost, c->stream));
+                CK(cudaStreamSynchronize(c->stream));
+                tol = (prm->rel_tol * F.args.tau) * hrs;  // as init_ctl_kernel
+            }
+            const double step = w1mg_cp_step_size(F.n, prm->step_mode);
+            s = make_slabs(c, "mlsl.slab" + std::to_string(l), F.n, nslabs, comm, step, step,
+                           nullptr, 0);
+            slab_load_from_level(c, s, F);
+            CK(cudaEventRecord(e0, c->stream));
+            slab_run(c, s, prm->pnorm, tol, prm->max_iters);
+            CK(cudaEventRecord(e1, c->stream));
+            CK(cudaMemcpyAsync(&hc, s.ctl, sizeof(PairCtl), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            slab_after_run(s, hc);
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            hit[l] = hc.it;
+            hff[l] = hc.fpr;
+            htl[l] = tol;
+            hsec[l] = ms * 1e-3;
+            if (l + 1 < levels) slab_store_to_level(c, s, F, hc.cur);
+        }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+        Level& F = lv.back();
         // W1 over owned rows (+ sum over ranks)
         double w1 = 0.0, du = 0.0;
         double* vals = c->get<double>("mlsl.vals", 2 * s.lv.size());
@@ -582,14 +634,13 @@ int w1mg_ml_slab_cp_run(w1mg_ctx* c, w1mg_slab_comm* comm, int nslabs, int n_fin
             w1 = loc[0];
             du = loc[1];
         }
-        long total = hc.it;
-        double tsec = ms * 1e-3;
-        for (int l = 0; l < levels - 1; ++l) {
+        long total = 0;
+        double tsec = 0.0;
+        for (int l = 0; l < levels; ++l) {
             total += hit[l];
-            tsec += secs[l];
-            if (stats) stats[l] = {1.0 / lv[l].n, htl[l], hit[l], hff[l], secs[l]};
+            tsec += hsec[l];
+            if (stats) stats[l] = {1.0 / lv[l].n, htl[l], hit[l], hff[l], hsec[l]};
         }
-        if (stats) stats[levels - 1] = {1.0 / F.n, tol, hc.it, hc.fpr, ms * 1e-3};
         if (rep) {
             rep->distance = w1;
             rep->dual_value = du;

@@ -170,8 +170,17 @@ def norm_L2(a) -> float:
 
 
 def norm_plain(a) -> float:
-    h = a.grid.h
-    return math.sqrt(inner_h(a, a) / h / h)
+    """Unweighted Euclidean norm (grid.cpp:117-128): Neumaier sum of squares
+    in the reference's order on the host (a utility, not the solve path)."""
+    arrs = [a.values] if isinstance(a, ScalarField) else [a.x_edges, a.y_edges]
+    s = c = 0.0
+    for arr in arrs:
+        for x in np.ravel(arr).tolist():
+            y = x * x
+            t = s + y
+            c += (s - t) + y if abs(s) >= abs(y) else (y - t) + s
+            s = t
+    return math.sqrt(s + c)
 
 
 def operator_norm_bound(grid: GridSpec) -> float:
@@ -645,9 +654,10 @@ def ml_pdhg_run(rho_levels: list, p: PNorm = PNorm.p2, rel_tol: float = 1e-5, ep
 def ml_slab_run(rho_levels: list, nslabs: int = 2, comm=None, p: PNorm = PNorm.p2,
                 rel_tol: float = 1e-5, eps=None, max_iters: int = 5_000_000,
                 step_mode: StepMode = StepMode.practical) -> SolveReport:
-    """Config-5 cascade: coarse levels replicated, the finest level cut into
-    row slabs (emulated on one device when comm is None, else this rank's slab
-    of an NCCL decomposition; the returned finest fields hold the owned rows)."""
+    """Config-5 cascade: levels with n >= the "slab_min_n" option (default
+    1024) and the finest level cut into row slabs, coarser levels replicated
+    (emulated on one device when comm is None, else this rank's slab of an
+    NCCL decomposition; the returned finest fields hold the owned rows)."""
     levels = len(rho_levels)
     nf = rho_levels[-1].shape[0] - 1
     flat = np.ascontiguousarray(np.concatenate([np.ravel(r) for r in rho_levels]))

@@ -105,6 +105,35 @@ def test_ml_slab_cascade_bit_exact(oracle, nslabs, transport):
     assert [l.iters for l in rep.levels] == [30] * 4
 
 
+@pytest.mark.parametrize("min_n", [128, 64])
+@pytest.mark.parametrize("nslabs", [2, 5])
+def test_ml_slab_cascade_partitions_every_large_level(oracle, nslabs, min_n, transport):
+    """Every level with n >= slab_min_n is row-slab partitioned (SURVEY 8e:
+    'the finest levels'), the slabs of one level gathered back to prolong
+    into the next: still bit-exact at fixed sweeps, and converged W1 / sweeps
+    as the oracle cascade."""
+    from paper_1810_00118_b200 import _lib
+
+    L = _lib.lib()
+    assert L.w1mg_set_option(b"slab_min_n", min_n) == _lib.W1MG_OK
+    try:
+        img0, img1 = instances.config5_images(m=256)
+        rhos = instances.ml_sources(img0, img1, 3)  # 64, 128, 256
+        eps = [-1.0] * 3
+        rep = w1mg.ml_slab_run(rhos, nslabs=nslabs, eps=eps, max_iters=25)
+        ref = oracle.ml_cp_run(rhos, p=1, eps=eps, max_iters=25)
+        assert np.array_equal(rep.potential.values, ref.phi)
+        assert np.array_equal(rep.flux.x_edges, ref.mx)
+        assert np.array_equal(rep.flux.y_edges, ref.my)
+        assert [l.iters for l in rep.levels] == [25] * 3
+        rep = w1mg.ml_slab_run(rhos, nslabs=nslabs, rel_tol=1e-5)
+        ref = oracle.ml_cp_run(rhos, p=1, rel_tol=1e-5)
+        assert abs(rep.distance - ref.distance) <= 1e-4 * ref.distance
+        assert all(abs(a.iters - b) <= 1 for a, b in zip(rep.levels, ref.level_iters))
+    finally:
+        L.w1mg_set_option(b"slab_min_n", 1024)
+
+
 def test_ml_slab_cascade_converged(oracle, transport):
     import time
 

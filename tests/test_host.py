@@ -179,3 +179,24 @@ print("ok", r)
              for r in range(2)]
     outs = [p.communicate(timeout=300)[0] for p in procs]
     assert all(p.returncode == 0 for p in procs), outs
+
+
+def test_norm_plain_matches_reference_order():
+    """norm_plain (grid.cpp:117-128) is the unweighted Neumaier norm, bit for
+    bit (round 1 computed sqrt(inner_h)/h, which rounds through h^2)."""
+    import math
+
+    import numpy as np
+
+    from paper_1810_00118_b200 import w1mg
+
+    rng = np.random.default_rng(9)
+    g = w1mg.GridSpec(7)
+    phi = w1mg.ScalarField(g, rng.standard_normal((8, 8)))
+    s = c = 0.0
+    for x in phi.values.ravel().tolist():
+        y = x * x
+        t = s + y
+        c += (s - t) + y if abs(s) >= abs(y) else (y - t) + s
+        s = t
+    assert w1mg.norm_plain(phi) == math.sqrt(s + c)
