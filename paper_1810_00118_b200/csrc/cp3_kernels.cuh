@@ -345,8 +345,7 @@ constexpr int kWarps3 = 4;
 constexpr int tmap3_smem(int nw) { return nw * (kStagesT * kBoxRows * kStageBytes + kStagesT * 8); }
 
 template <int PN>
-__global__ void __launch_bounds__(kWarps3 * 32, 5)
-cp_sweep3_tmap_kernel(const SweepArgs a, const int parity, const __grid_constant__ CUtensorMap tm,
+__device__ __forceinline__ void cp_sweep3_tmap_body(const SweepArgs& a, const int parity, const CUtensorMap& tm,
                       const int pdl_early) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (pdl_early) asm volatile("griddepcontrol.launch_dependents;");
@@ -375,6 +374,21 @@ cp_sweep3_tmap_kernel(const SweepArgs a, const int parity, const __grid_constant
         else march3<PN, false>(a, pair, parity, cx, j0, j1, lane, ring, bars, acc, &tm);
     }
     finish_sweep3<kWarps3>(a, pair, parity, acc);
+}
+
+template <int PN>
+__global__ void __launch_bounds__(kWarps3 * 32, 5)
+cp_sweep3_tmap_kernel(const SweepArgs a, const int parity, const __grid_constant__ CUtensorMap tm,
+                      const int pdl_early) {
+    cp_sweep3_tmap_body<PN>(a, parity, tm, pdl_early);
+}
+
+// the same at six CTAs per SM (<= 80 registers; option "occ3" = 6, A/B)
+template <int PN>
+__global__ void __launch_bounds__(kWarps3 * 32, 6)
+cp_sweep3_tmap6_kernel(const SweepArgs a, const int parity, const __grid_constant__ CUtensorMap tm,
+                       const int pdl_early) {
+    cp_sweep3_tmap_body<PN>(a, parity, tm, pdl_early);
 }
 
 }  // namespace w1mg_dev
