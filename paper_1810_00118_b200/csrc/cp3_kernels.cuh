@@ -383,12 +383,5 @@ cp_sweep3_tmap_kernel(const SweepArgs a, const int parity, const __grid_constant
     cp_sweep3_tmap_body<PN>(a, parity, tm, pdl_early);
 }
 
-// the same at six CTAs per SM (<= 80 registers; option "occ3" = 6, A/B)
-template <int PN>
-__global__ void __launch_bounds__(kWarps3 * 32, 6)
-cp_sweep3_tmap6_kernel(const SweepArgs a, const int parity, const __grid_constant__ CUtensorMap tm,
-                       const int pdl_early) {
-    cp_sweep3_tmap_body<PN>(a, parity, tm, pdl_early);
-}
 
 }  // namespace w1mg_dev
