@@ -351,11 +351,16 @@ bool two_sweep(const Level& lv) {
 // kernel is as fast or faster (512^2 x256 367 vs 369 us, 256^2 x1024 422 vs
 // 386 us per sweep); batched 256^2 and the big one-pair grids stay on two
 // sweeps
+// In tolerance mode (fewer FP64 instructions per node) the three-sweep pass
+// also wins on batched 128^2 / 256^2 levels (fast-mode probe, 1024 pairs:
+// 256^2 0.339 vs 0.361 ms, 128^2 0.100 vs 0.114 ms per sweep; 256 pairs of
+// 256^2 0.090 vs 0.099 ms), so auto uses it for every batched level n >= 96.
 bool three_sweep(const Level& lv) {
     if (lv.slab || !lv.has_tmap || lv.n < 96) return false;
+    const int batched_min = g_fast ? 96 : 384;
     return g_sweep_variant == kTma3 ||
            (g_sweep_variant == kAuto && ((lv.B == 1 && lv.n >= 192 && lv.n <= 384) ||
-                                         (lv.B > 1 && lv.n >= 384)));
+                                         (lv.B > 1 && lv.n >= batched_min)));
 }
 // sweeps one streaming launch performs on this level
 int sweeps_per_launch(const Level& lv) { return three_sweep(lv) ? 3 : two_sweep(lv) ? 2 : 1; }
