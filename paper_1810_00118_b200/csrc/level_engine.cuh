@@ -538,6 +538,10 @@ int cluster_size(const Level& lv, int num_sms) {
         while (C * 2 <= 16 && (long)lv.B * C * 2 <= num_sms && (lv.n + 1) / (C * 2) >= 8) C *= 2;
     }
     if (g_resident == 1 && (C == 1 || lv.n > 128)) return 0;
+    // big batches of 128^2 pairs stream instead: 1024 config-4 pairs, 128^2
+    // level 0.93 s per step streaming (three sweeps per pass) vs 1.57 s on
+    // 4-CTA clusters (bench A/B, tools/gpu/r2s.sh)
+    if (g_resident == 1 && lv.n > 64 && (long)lv.B * C > 2L * num_sms) return 0;
     return C;
 }
 
