@@ -140,55 +140,7 @@ __device__ __noinline__ void tgemm2(const double* tab, int N, int Mp, int K1, in
                                     double* C1, double* C2, int ldc, const double* C0, double s2) {
     const int Nt = Np >> 2, Mt = Mp >> 2;
     const double* ts = tab + N;
-    // tile shape by the per-thread serial work of one step (instructions):
-    // 4x4 ~44, 2x2 ~14, 1x1 ~9, times the rounds of tiles over the block
-    const int bd = blockDim.x;
-    const int Nr2 = (Nr + 1) >> 1;
-    const long w4 = (long)((Mt * Nt + bd - 1) / bd) * 44;
-    const long w2 = (long)(((Mp >> 1) * Nr2 + bd - 1) / bd) * 14;
-    const long w1 = (long)((Mp * Nr + bd - 1) / bd) * 9;
-    if (w2 < w4 && w2 <= w1) {
-        W1MG_FOR2(ti, tj, Mp >> 1, Nr2) {
-            int kr[2], ix[2];
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                int k = 2 * ti + r;
-                k -= (k >= N) ? N : 0;
-                k -= (k >= N) ? N : 0;
-                kr[r] = k;
-                ix[r] = k;
-            }
-            double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-            const double* b1 = B1 + 2 * tj;
-            const double* b2 = B2 + 2 * tj;
-#pragma unroll 2
-            for (int t = 0; t < K1; ++t) {
-                const double2 x = lds2(b1 + t * ldb);
-                const double2 y = (t < K2) ? lds2(b2 + t * ldb) : make_double2(0.0, 0.0);
-#pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const double cw = lds(tab + ix[r]), sw = lds(ts + ix[r]);
-                    ix[r] += kr[r];
-                    ix[r] -= (ix[r] >= N) ? N : 0;
-                    c[r][0] = fma(cw, x.x, c[r][0]);
-                    c[r][1] = fma(cw, x.y, c[r][1]);
-                    d[r][0] = fma(sw, y.x, d[r][0]);
-                    d[r][1] = fma(sw, y.y, d[r][1]);
-                }
-            }
-            double2 z = make_double2(0.0, 0.0);
-            if (C0) z = lds2(C0 + 2 * tj);
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                double* o1 = C1 + (2 * ti + r) * ldc + 2 * tj;
-                double* o2 = C2 + (2 * ti + r) * ldc + 2 * tj;
-                *reinterpret_cast<double2*>(o1) = make_double2(z.x + c[r][0], z.y + c[r][1]);
-                *reinterpret_cast<double2*>(o2) = make_double2(s2 * d[r][0], s2 * d[r][1]);
-            }
-        }
-        return;
-    }
-    if (w4 <= w1) {
+    if (4 * Mt * Nt >= (int)blockDim.x) {
         W1MG_FOR2(ti, tj, Mt, Nt) {
             int kr[4], ix[4];
 #pragma unroll
