@@ -71,6 +71,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_WARPS_PER_SM")) g_warps_per_sm = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_PDL")) g_pdl = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_FAST")) g_fast = std::atoi(v) != 0;
+        if (const char* v = std::getenv("W1MG_OCC3")) g_occ3 = std::atoi(v) == 4 ? 4 : 5;
         if (const char* v = std::getenv("W1MG_PDHG_PERSIST")) g_pdhg_persist = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_SLAB_MIN_N")) g_slab_min_n = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
@@ -609,6 +610,7 @@ int w1mg_set_option(const char* name, long value) {
     else if (k == "warps_per_sm" && v >= 1) g_warps_per_sm = v;
     else if (k == "pdl" && (v == 0 || v == 1)) g_pdl = v;
     else if (k == "fast" && (v == 0 || v == 1)) g_fast = v;
+    else if (k == "occ3" && (v == 4 || v == 5)) g_occ3 = v;
     else if (k == "tmap_nw" && (v == 0 || v == 2 || v == 4 || v == 8)) g_tmap_nw = v;
     else return W1MG_EINVAL;
     return W1MG_OK;

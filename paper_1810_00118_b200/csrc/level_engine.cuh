@@ -308,6 +308,9 @@ void launch_pdl(K kernel, dim3 grid, dim3 blk, int smem, cudaStream_t s, const S
 // (PN = 3: FMA-contracted node arithmetic and the rsqrt shrink of
 // device_common.cuh; fields within 1e-9 of the reference at fixed sweeps)
 int g_fast = 0;
+// CTAs per SM of the tolerance-mode three-sweep kernel: 5 (<= 96 registers,
+// default) or 4 (<= 128), option "occ3" (A/B)
+int g_occ3 = 5;
 int stream_pn(int pn) { return (g_fast && pn == 1) ? 3 : pn; }
 
 template <int NW, bool U>
@@ -372,11 +375,14 @@ void launch_sweep3(const Level& lv, int pn, int parity, cudaStream_t s) {
     const long blocks = (long)lv.grid3.x * lv.grid3.y;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const int early = (g_pdl && 2 * blocks <= (long)nsm * 5) ? 1 : 0;
+    const int early = (g_pdl && 2 * blocks <= (long)nsm * g_occ3) ? 1 : 0;
     switch (pn) {
         case 0: launch_pdl(cp_sweep3_tmap_kernel<0>, lv.grid3, blk, sm, s, lv.args3, parity, lv.tmap, early); break;
         case 1: launch_pdl(cp_sweep3_tmap_kernel<1>, lv.grid3, blk, sm, s, lv.args3, parity, lv.tmap, early); break;
-        case 3: launch_pdl(cp_sweep3_tmap_kernel<3>, lv.grid3, blk, sm, s, lv.args3, parity, lv.tmap, early); break;
+        case 3:
+            if (g_occ3 == 4) launch_pdl(cp_sweep3_tmap4_kernel<3>, lv.grid3, blk, sm, s, lv.args3, parity, lv.tmap, early);
+            else launch_pdl(cp_sweep3_tmap_kernel<3>, lv.grid3, blk, sm, s, lv.args3, parity, lv.tmap, early);
+            break;
         default: launch_pdl(cp_sweep3_tmap_kernel<2>, lv.grid3, blk, sm, s, lv.args3, parity, lv.tmap, early); break;
     }
 }
@@ -420,7 +426,7 @@ cudaGraphExec_t sweep_graph(w1mg_ctx* c, const Level& lv, int pn, int K) {
            std::to_string(lv.grid3.x) + ":B" +
            std::to_string(lv.B) + ":v" +
            std::to_string(g_sweep_variant) + ":nw" + std::to_string(lv.tmap_nw) + ":pdl" +
-           std::to_string(g_pdl) + ":f" + std::to_string(g_fast);
+           std::to_string(g_pdl) + ":f" + std::to_string(g_fast) + ":o" + std::to_string(g_occ3);
     auto it = c->graphs.find(key);
     if (it != c->graphs.end()) return it->second;
     cudaGraph_t g;
