@@ -73,6 +73,7 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_FAST")) g_fast = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_OCC3")) g_occ3 = std::atoi(v) == 4 ? 4 : 5;
         if (const char* v = std::getenv("W1MG_PDHG_PERSIST")) g_pdhg_persist = std::atoi(v) != 0;
+        if (const char* v = std::getenv("W1MG_PDHG_RS")) g_pdhg_rs = std::atoi(v);
         if (const char* v = std::getenv("W1MG_SLAB_MIN_N")) g_slab_min_n = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
@@ -602,6 +603,7 @@ int w1mg_set_option(const char* name, long value) {
     const std::string k(name);
     const int v = (int)value;
     if (k == "pdhg_persist" && (v == 0 || v == 1)) g_pdhg_persist = v;
+    else if (k == "pdhg_rs" && v >= 0 && v <= 3) g_pdhg_rs = v;
     else if (k == "slab_min_n" && v >= 1) g_slab_min_n = v;
     else if (k == "pdhg_small" && v >= 0 && v <= 2) g_pdhg_small = v;
     else if (k == "cluster_pick" && (v == 0 || v == 1)) g_cluster_pick = v;

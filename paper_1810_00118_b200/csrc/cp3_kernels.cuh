@@ -176,8 +176,8 @@ __device__ __forceinline__ void march3(const SweepArgs& a, int pair, int parity,
         uyA = uy;
         dyA = dy;
     }
-    // C's stores go four rows below A: running pointers
-    const long o0 = L.at(i, rA0) - 4L * P;
+    // C's stores go two rows below A: running pointers
+    const long o0 = L.at(i, rA0) - 2L * P;
     double* __restrict__ wph = phw + o0;
     double* __restrict__ wmx = mxw + o0;
     double* __restrict__ wmy = myw + o0;
@@ -185,16 +185,10 @@ __device__ __forceinline__ void march3(const SweepArgs& a, int pair, int parity,
     double pc = in ? ring[sh + lane] : 0.0;  // phi^k(i, rA), phi^k(i+1, rA)
     double pr = hx ? ring[sh + lane + 1] : 0.0;
 
-    // B trails A by TWO rows and C trails B by two: in one step the three
-    // sweeps read only results of earlier steps, so their dependency chains
-    // interleave (a one-row lag chained A -> B -> C inside every step).
-    // B state: A's outputs of the last two rows; C state: B's outputs of the
-    // last two rows; rho of the last four rows.
-    double fA_prev = 0.0, mxA_prev = 0.0, myA_prev = 0.0;
-    double fA_prev2 = 0.0, mxA_prev2 = 0.0, myA_prev2 = 0.0;
-    double fB_prev = 0.0, mxB_prev = 0.0, myB_prev = 0.0;
-    double fB_prev2 = 0.0, mxB_prev2 = 0.0, myB_prev2 = 0.0;
-    double r_prev = 0.0, r_prev2 = 0.0, r_prev3 = 0.0, r_prev4 = 0.0;
+    // B state: A's outputs of the previous row, rho of the previous row;
+    // C state: B's outputs of the previous row, rho two rows back
+    double fA_prev = 0.0, mxA_prev = 0.0, myA_prev = 0.0, r_prev = 0.0;
+    double fB_prev = 0.0, mxB_prev = 0.0, myB_prev = 0.0, r_prev2 = 0.0;
     double uyB = 0.0, dyB = 0.0, uyC = 0.0, dyC = 0.0;
 
     // mode: 0 = rows tested at run time, 3 = middle step (A, B, C rows all
@@ -203,7 +197,7 @@ __device__ __forceinline__ void march3(const SweepArgs& a, int pair, int parity,
     auto step = [&](const int t, auto mode, auto par) {
         constexpr int kMode = decltype(mode)::value;
         constexpr int kPar = decltype(par)::value;
-        const int rA = rA0 + t, rB = rA - 2, rC = rA - 4;
+        const int rA = rA0 + t, rB = rA - 1, rC = rA - 2;
         double fA = 0.0, uxA = 0.0, uyAn = 0.0, dxA = 0.0, dyAn = 0.0, r = 0.0;
         double pu = 0.0, pur = 0.0;
         if (kMode == 3 || kInt || rA <= rA1) {
@@ -249,21 +243,21 @@ __device__ __forceinline__ void march3(const SweepArgs& a, int pair, int parity,
             uyA = uyAn;
             dyA = dyAn;
         }
-        // ---- sweep B at row rB (inputs: A's rows rB and rB + 1, steps t-2, t-1)
+        // ---- sweep B at row rB (inputs: A's rows rB and rB + 1)
         double fB = 0.0, uxB = 0.0, uyBn = 0.0;
         if (kMode == 3 || (rB >= rA0 && rB <= rB1)) {
             const bool hyB = kInt || (in && (rB < n));
-            const double prB = __shfl_down_sync(0xffffffffu, fA_prev2, 1);
-            const double puB = hyB ? fA_prev : 0.0;
+            const double prB = __shfl_down_sync(0xffffffffu, fA_prev, 1);
+            const double puB = hyB ? fA : 0.0;
             double dx, dy;
-            node_flux<PN>(hx, hyB, fA_prev2, hx ? prB : 0.0, puB, mxA_prev2, myA_prev2, mu, zt, ih,
+            node_flux<PN>(hx, hyB, fA_prev, hx ? prB : 0.0, puB, mxA_prev, myA_prev, mu, zt, ih,
                           uxB, uyBn, dx, dy);
             const double uxl = __shfl_up_sync(0xffffffffu, uxB, 1);
             const double dxl = __shfl_up_sync(0xffffffffu, dx, 1);
             double divd;
             const double d =
-                phi_delta<PN>(uxB, uxl, uyBn, uyB, dx, dxl, dy, dyB, r_prev2, ih, tau, divd);
-            fB = fA_prev2 + d;
+                phi_delta<PN>(uxB, uxl, uyBn, uyB, dx, dxl, dy, dyB, r_prev, ih, tau, divd);
+            fB = fA_prev + d;
             if (kMode == 3 || (own && rB >= j0 && rB < j1)) {
                 acc[3] = __fma_rn(dy, dy, __fma_rn(dx, dx, acc[3]));
                 acc[4] = __fma_rn(d, d, acc[4]);
@@ -272,21 +266,21 @@ __device__ __forceinline__ void march3(const SweepArgs& a, int pair, int parity,
             uyB = uyBn;
             dyB = dy;
         }
-        // ---- sweep C at row rC (inputs: B's rows rC and rC + 1, steps t-2, t-1)
+        // ---- sweep C at row rC (inputs: B's rows rC and rC + 1)
         if (kMode == 3 || rC >= rA0) {
             const bool hyC = kInt || (in && (rC < n));
-            const double prC = __shfl_down_sync(0xffffffffu, fB_prev2, 1);
-            const double puC = hyC ? fB_prev : 0.0;
+            const double prC = __shfl_down_sync(0xffffffffu, fB_prev, 1);
+            const double puC = hyC ? fB : 0.0;
             double ux, uy, dx, dy;
-            node_flux<PN>(hx, hyC, fB_prev2, hx ? prC : 0.0, puC, mxB_prev2, myB_prev2, mu, zt, ih,
-                          ux, uy, dx, dy);
+            node_flux<PN>(hx, hyC, fB_prev, hx ? prC : 0.0, puC, mxB_prev, myB_prev, mu, zt, ih, ux,
+                          uy, dx, dy);
             const double uxl = __shfl_up_sync(0xffffffffu, ux, 1);
             const double dxl = __shfl_up_sync(0xffffffffu, dx, 1);
             double divd;
             const double d =
-                phi_delta<PN>(ux, uxl, uy, uyC, dx, dxl, dy, dyC, r_prev4, ih, tau, divd);
+                phi_delta<PN>(ux, uxl, uy, uyC, dx, dxl, dy, dyC, r_prev2, ih, tau, divd);
             if (own && (kMode == 3 || rC >= j0)) {  // rC < j1 always
-                *wph = fB_prev2 + d;
+                *wph = fB_prev + d;
                 if (hx) *wmx = ux;
                 if (hyC) *wmy = uy;
             }
@@ -298,21 +292,13 @@ __device__ __forceinline__ void march3(const SweepArgs& a, int pair, int parity,
             uyC = uy;
             dyC = dy;
         }
-        fB_prev2 = fB_prev;
-        mxB_prev2 = mxB_prev;
-        myB_prev2 = myB_prev;
         fB_prev = fB;
         mxB_prev = uxB;
         myB_prev = uyBn;
-        fA_prev2 = fA_prev;
-        mxA_prev2 = mxA_prev;
-        myA_prev2 = myA_prev;
+        r_prev2 = r_prev;
         fA_prev = fA;
         mxA_prev = uxA;
         myA_prev = uyAn;
-        r_prev4 = r_prev3;
-        r_prev3 = r_prev2;
-        r_prev2 = r_prev;
         r_prev = r;
         pc = pu;
         pr = pur;
@@ -327,9 +313,9 @@ __device__ __forceinline__ void march3(const SweepArgs& a, int pair, int parity,
     using PE = std::integral_constant<int, 0>;
     using PO = std::integral_constant<int, 1>;
     using PR = std::integral_constant<int, 2>;
-    const int T = j1 + 3 - rA0;  // last step: C at row j1 - 1
+    const int T = j1 + 1 - rA0;  // last step: C at row j1 - 1
     // middle steps: A row < j1 and C row >= j0
-    const int tm0 = j0 + 4 - rA0, tm1 = j1 - rA0;
+    const int tm0 = j0 + 2 - rA0, tm1 = j1 - rA0;
     int t = 0;
     for (; t < tm0 && t <= T; ++t, next_row()) step(t, M0{}, PR{});
     if (t < tm1 && (t & 1)) {
@@ -404,6 +390,5 @@ cp_sweep3_tmap4_kernel(const SweepArgs a, const int parity, const __grid_constan
                        const int pdl_early) {
     cp_sweep3_tmap_body<PN>(a, parity, tm, pdl_early);
 }
-
 
 }  // namespace w1mg_dev

@@ -13,6 +13,7 @@
 #include "pdhg_small.cuh"
 #include "dct_kernels.cuh"
 #include "pdhg_persist.cuh"
+#include "pdhg_rs.cuh"
 
 namespace {
 
@@ -420,6 +421,141 @@ bool launch_pdhg_persist(w1mg_ctx* c, const PLevel& lv, int q) {
     return launch_pdhg_persist_q<2>(c, lv);
 }
 
+// Row-resident level-persistent PDHG for one pair (pdhg_rs.cuh): rows of the
+// state in shared memory for the whole level, two grid barriers per
+// iteration, register-stationary dense DCT for m <= 129 (odd), prime-factor
+// transforms above.  g_pdhg_rs (level_engine.cuh): 0 off, 1 auto, 2 forces
+// the prime-factor transforms (A/B), 3 also replaces the one-CTA small kernel.
+
+struct RsTables {
+    const double* cosq;
+    const double* lamq;
+};
+
+// cos(pi j / 2m), j < 4m (host long double) and lambda in position order
+RsTables rs_tables(w1mg_ctx* c, int n, bool dense) {
+    const int m = n + 1, h = (m - 1) / 2;
+    const std::string kc = "rs.cosq." + std::to_string(m);
+    const std::string kl = std::string(dense ? "rs.lamq.d." : "rs.lamq.n.") + std::to_string(m);
+    const bool fc = c->bufs.find(kc) == c->bufs.end(), fl = c->bufs.find(kl) == c->bufs.end();
+    double* dc = c->get<double>(kc, (size_t)4 * m);
+    double* dl = c->get<double>(kl, m);
+    if (fc) {
+        std::vector<double> hc((size_t)4 * m);
+        const long double pi = 3.141592653589793238462643383279502884L;
+        for (int j = 0; j < 4 * m; ++j) hc[j] = (double)cosl(pi * (long double)j / (2.0L * m));
+        CK(cudaMemcpy(dc, hc.data(), hc.size() * 8, cudaMemcpyHostToDevice));
+    }
+    if (fl) {
+        std::vector<double> hl(m);
+        const double hh = 1.0 / n;
+        const double inv_h2 = 1.0 / (hh * hh);
+        auto lam = [&](int k) { return (2.0 - 2.0 * std::cos(M_PI * k / m)) * inv_h2; };  // poisson.cpp:28-30
+        for (int pos = 0; pos < m; ++pos) {
+            int k = pos;
+            if (dense) k = pos < h ? 2 * pos + 2 : (pos < 2 * h ? 2 * (pos - h) + 1 : 0);
+            hl[pos] = lam(k);
+        }
+        CK(cudaMemcpy(dl, hl.data(), hl.size() * 8, cudaMemcpyHostToDevice));
+    }
+    return RsTables{dc, dl};
+}
+
+template <int Q, int TS>
+bool launch_pdhg_rs_qt(w1mg_ctx* c, const PLevel& lv, int R) {
+    const DctPlan& p = lv.dp;
+    const int m = p.m, G = (m + R - 1) / R, ms = m + 1;
+    const size_t smem = rs_smem_doubles(p, R, TS) * sizeof(double);
+    if (smem > kDctSmemMax || G > c->num_sms) return false;
+    static unsigned long long attr = 0;  // per device
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!(attr >> (dev & 63) & 1ull)) {
+        CK(cudaFuncSetAttribute(pdhg_rs_kernel<Q, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kDctSmemMax));
+        attr |= 1ull << (dev & 63);
+    }
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdhg_rs_kernel<Q, TS>, kRsThreads, smem));
+    if (occ < 1) return false;
+    const RsTables tb = rs_tables(c, lv.n, TS > 0);
+    RsArgs ra{};
+    ra.m = m;
+    ra.h = (m - 1) / 2;
+    ra.R = R;
+    ra.G = G;
+    ra.HP = 16 * TS;
+    ra.posDC = TS > 0 ? 2 * ra.h : 0;
+    ra.halo_x = TS > 0 ? 0 : 1;
+    ra.cosq = tb.cosq;
+    ra.lamq = tb.lamq;
+    ra.scale = 1.0 / (4.0 * double(m) * double(m));  // poisson.cpp:93
+    ra.vyb = c->get<double>("rs.vyb", (size_t)G * ms);
+    ra.psb = c->get<double>("rs.psb", (size_t)G * ms);
+    ra.flag = c->get<unsigned>("rs.flag", (size_t)2 * G);
+    ra.part = c->get<double>("rs.part", (size_t)3 * G);
+    CK(cudaMemsetAsync(ra.flag, 0, sizeof(unsigned) * 2 * G, c->stream));
+    unsigned* bar = c->get<unsigned>("persist.bar", 2);
+    int* err = c->get<int>("persist.err", 1);
+    CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), c->stream));
+    CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
+    GridBar gb{bar, bar + 1, err};
+    ra.stamps = nullptr;
+    if (std::getenv("W1MG_PERSIST_STAMPS")) {
+        ra.stamps = c->get<unsigned long long>("persist.stamps", 640);
+        CK(cudaMemsetAsync(ra.stamps, 0, 640 * 8, c->stream));
+    }
+    SweepArgs a = lv.args;
+    DctPlan pp = p;
+    void* args[] = {(void*)&a, (void*)&pp, (void*)&ra, (void*)&gb};
+    CK(cudaLaunchCooperativeKernel((const void*)pdhg_rs_kernel<Q, TS>, dim3(G), dim3(kRsThreads), args,
+                                   smem, c->stream));
+    ++c->launches;
+    int herr = 0;
+    CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (herr) fail(W1MG_ECUDA, "row-resident PDHG: grid barrier timed out");
+    if (ra.stamps) {  // per-phase ns of iterations 8..62: A, bar, B, bar, C, D
+        std::vector<unsigned long long> h(640);
+        CK(cudaMemcpy(h.data(), ra.stamps, 640 * 8, cudaMemcpyDeviceToHost));
+        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+        int cnt = 0;
+        for (int it = 8; it < 62; ++it) {
+            if (!h[(it + 1) * 10]) break;
+            for (int q = 0; q < 6; ++q) acc[q] += double(h[it * 10 + q + 1] - h[it * 10 + q]);
+            acc[6] += double(h[(it + 1) * 10] - h[it * 10]);
+            ++cnt;
+        }
+        if (cnt)
+            std::fprintf(stderr, "rs m=%d G=%d R=%d TS=%d ns: A %.0f bar %.0f B %.0f bar %.0f C %.0f D %.0f | iter %.0f\n",
+                         m, G, R, TS, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
+                         acc[4] / cnt, acc[5] / cnt, acc[6] / cnt);
+    }
+    return true;
+}
+
+template <int Q>
+bool launch_pdhg_rs_q(w1mg_ctx* c, const PLevel& lv) {
+    const int m = lv.n + 1, h = (m - 1) / 2;
+    int R = (m + c->num_sms - 1) / c->num_sms;
+    if ((m & 1) && h <= 64 && g_pdhg_rs != 2) {
+        if (h <= 16) return launch_pdhg_rs_qt<Q, 1>(c, lv, R);
+        if (h <= 32) return launch_pdhg_rs_qt<Q, 2>(c, lv, R);
+        return launch_pdhg_rs_qt<Q, 4>(c, lv, R);
+    }
+    int Rp = 1;
+    while (Rp < R) Rp <<= 1;  // the prime-factor transforms split vectors by shifts
+    if (Rp > 16) return false;
+    return launch_pdhg_rs_qt<Q, 0>(c, lv, Rp);
+}
+
+bool launch_pdhg_rs(w1mg_ctx* c, const PLevel& lv, int q) {
+    if (!g_pdhg_rs || lv.B != 1) return false;
+    if (q == 0) return launch_pdhg_rs_q<0>(c, lv);
+    if (q == 1) return launch_pdhg_rs_q<1>(c, lv);
+    return launch_pdhg_rs_q<2>(c, lv);
+}
+
 // small levels: one launch per level, one CTA per pair (pdhg_small.cuh);
 // W1MG_PDHG_SMALL = 1 (default, m <= 33), 2 (m <= 65), 0 (streaming only)
 // (g_pdhg_small, level_engine.cuh)
@@ -449,6 +585,7 @@ void launch_pdhg_small(w1mg_ctx* c, const PLevel& lv) {
 // watches the done counter one graph behind, like run_sweeps).
 void run_pdhg_iters(w1mg_ctx* c, const PLevel& lv, int q, long max_iters) {
     if (max_iters <= 0) return;
+    if (g_pdhg_rs == 3 && launch_pdhg_rs(c, lv, q)) return;
     if ((g_pdhg_small == 1 && lv.n + 1 <= kPdhgSmallAutoM) ||
         (g_pdhg_small == 2 && lv.n + 1 <= kPdhgSmallMaxM)) {
         if (q == 0) launch_pdhg_small<0>(c, lv);
@@ -456,6 +593,7 @@ void run_pdhg_iters(w1mg_ctx* c, const PLevel& lv, int q, long max_iters) {
         else launch_pdhg_small<2>(c, lv);
         return;
     }
+    if (launch_pdhg_rs(c, lv, q)) return;
     if (launch_pdhg_persist(c, lv, q)) return;
     constexpr int K = 8;
     if (max_iters < K) {

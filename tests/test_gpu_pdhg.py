@@ -67,23 +67,30 @@ def test_project_affine(n):
     assert _rel(again.x_edges, out.x_edges) <= 1e-10
 
 
-@pytest.fixture(params=["streaming", "persistent", "resident"])
+@pytest.fixture(params=["streaming", "persistent", "resident", "rowres", "rowres_pfa", "auto"])
 def pdhg_engine(request):
     """streaming: 3-launch iteration (row DCT-II + pre, column DCT-II /
     divide / DCT-III, row DCT-III + post); persistent: every iteration of a
     one-pair level in one cooperative launch (pdhg_persist.cuh); resident:
-    one CTA per pair for m <= 65, persistent above."""
+    one CTA per pair for m <= 65, persistent above; rowres: the row-resident
+    persistent engine (pdhg_rs.cuh) at every size, dense register-stationary
+    DCT for odd m <= 129; rowres_pfa: the same with the prime-factor
+    transforms everywhere; auto: the defaults."""
     from paper_1810_00118_b200 import _lib
 
     L = _lib.lib()
-    L.w1mg_set_pdhg_small(2 if request.param == "resident" else 0)
-    L.w1mg_set_option(b"pdhg_persist", 0 if request.param == "streaming" else 1)
+    rs = {"rowres": 3, "rowres_pfa": 2, "auto": 1}.get(request.param, 0)
+    if request.param != "auto":
+        L.w1mg_set_pdhg_small(2 if request.param == "resident" else 0)
+        L.w1mg_set_option(b"pdhg_persist", 0 if request.param == "streaming" else 1)
+    L.w1mg_set_option(b"pdhg_rs", rs)
     yield request.param
     L.w1mg_set_pdhg_small(1)
     L.w1mg_set_option(b"pdhg_persist", 1)
+    L.w1mg_set_option(b"pdhg_rs", 1)
 
 
-@pytest.mark.parametrize("n", [31, 32, 64, 128, 256])
+@pytest.mark.parametrize("n", [31, 32, 48, 64, 100, 128, 256])
 @pytest.mark.parametrize("p", [0, 1, 2])
 def test_pdhg_fixed_iterations(p, n, pdhg_engine):
     rho = instances.config1_source(n)
