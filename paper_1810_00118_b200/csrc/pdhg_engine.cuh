@@ -14,6 +14,7 @@
 #include "dct_kernels.cuh"
 #include "pdhg_persist.cuh"
 #include "pdhg_rs.cuh"
+#include "pdhg_rs2.cuh"
 
 namespace {
 
@@ -461,6 +462,26 @@ RsTables rs_tables(w1mg_ctx* c, int n, bool dense) {
     return RsTables{dc, dl};
 }
 
+// per-phase ns of iterations 8..62 (CTA 0): A, barrier, B, barrier, C, D
+void rs_print_stamps(w1mg_ctx* c, const unsigned long long* stamps, int m, int G, int R, int TS) {
+    (void)c;
+    if (!stamps) return;
+    std::vector<unsigned long long> h(640);
+    CK(cudaMemcpy(h.data(), stamps, 640 * 8, cudaMemcpyDeviceToHost));
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    int cnt = 0;
+    for (int it = 8; it < 62; ++it) {
+        if (!h[(it + 1) * 10]) break;
+        for (int q = 0; q < 6; ++q) acc[q] += double(h[it * 10 + q + 1] - h[it * 10 + q]);
+        acc[6] += double(h[(it + 1) * 10] - h[it * 10]);
+        ++cnt;
+    }
+    if (cnt)
+        std::fprintf(stderr, "rs m=%d G=%d R=%d TS=%d ns: A %.0f bar %.0f B %.0f bar %.0f C %.0f D %.0f | iter %.0f\n",
+                     m, G, R, TS, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
+                     acc[4] / cnt, acc[5] / cnt, acc[6] / cnt);
+}
+
 template <int Q, int TS>
 bool launch_pdhg_rs_qt(w1mg_ctx* c, const PLevel& lv, int R) {
     const DctPlan& p = lv.dp;
@@ -515,22 +536,82 @@ bool launch_pdhg_rs_qt(w1mg_ctx* c, const PLevel& lv, int R) {
     CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (herr) fail(W1MG_ECUDA, "row-resident PDHG: grid barrier timed out");
-    if (ra.stamps) {  // per-phase ns of iterations 8..62: A, bar, B, bar, C, D
-        std::vector<unsigned long long> h(640);
-        CK(cudaMemcpy(h.data(), ra.stamps, 640 * 8, cudaMemcpyDeviceToHost));
-        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-        int cnt = 0;
-        for (int it = 8; it < 62; ++it) {
-            if (!h[(it + 1) * 10]) break;
-            for (int q = 0; q < 6; ++q) acc[q] += double(h[it * 10 + q + 1] - h[it * 10 + q]);
-            acc[6] += double(h[(it + 1) * 10] - h[it * 10]);
-            ++cnt;
-        }
-        if (cnt)
-            std::fprintf(stderr, "rs m=%d G=%d R=%d TS=%d ns: A %.0f bar %.0f B %.0f bar %.0f C %.0f D %.0f | iter %.0f\n",
-                         m, G, R, TS, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
-                         acc[4] / cnt, acc[5] / cnt, acc[6] / cnt);
+    rs_print_stamps(c, ra.stamps, m, G, R, TS);
+    return true;
+}
+
+// 129 < m <= 257 (odd): clusters of two CTAs share the register-stationary
+// DCT matrix (pdhg_rs2.cuh); cooperative launch of 2 x ceil(m / 2R) CTAs.
+template <int Q>
+bool launch_pdhg_rs2_q(w1mg_ctx* c, const PLevel& lv) {
+    const int m = lv.n + 1, h = (m - 1) / 2, ms = m + 1;
+    const int NC = c->num_sms / 2;
+    const int R = (m + 2 * NC - 1) / (2 * NC);
+    const int G = 2 * ((m + 2 * R - 1) / (2 * R));
+    const size_t smem = rs2_smem_doubles(m, R) * sizeof(double);
+    if (smem > kDctSmemMax) return false;
+    static unsigned long long attr = 0;  // per device
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!(attr >> (dev & 63) & 1ull)) {
+        CK(cudaFuncSetAttribute(pdhg_rs2_kernel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kDctSmemMax));
+        attr |= 1ull << (dev & 63);
     }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(kRsThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, pdhg_rs2_kernel<Q>, &cfg) != cudaSuccess ||
+        2 * nclusters < G) {
+        cudaGetLastError();
+        return false;
+    }
+    const RsTables tb = rs_tables(c, lv.n, true);
+    RsArgs ra{};
+    ra.m = m;
+    ra.h = h;
+    ra.R = R;
+    ra.G = G;
+    ra.HP = kRs2HP;
+    ra.posDC = 2 * h;
+    ra.halo_x = 0;
+    ra.cosq = tb.cosq;
+    ra.lamq = tb.lamq;
+    ra.scale = 1.0 / (4.0 * double(m) * double(m));  // poisson.cpp:93
+    ra.vyb = nullptr;
+    ra.psb = nullptr;
+    ra.flag = nullptr;
+    ra.part = c->get<double>("rs.part", (size_t)3 * G);
+    unsigned* bar = c->get<unsigned>("persist.bar", 2);
+    int* err = c->get<int>("persist.err", 1);
+    CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), c->stream));
+    CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
+    GridBar gb{bar, bar + 1, err};
+    ra.stamps = nullptr;
+    if (std::getenv("W1MG_PERSIST_STAMPS")) {
+        ra.stamps = c->get<unsigned long long>("persist.stamps", 640);
+        CK(cudaMemsetAsync(ra.stamps, 0, 640 * 8, c->stream));
+    }
+    (void)ms;
+    CK(cudaLaunchKernelEx(&cfg, pdhg_rs2_kernel<Q>, lv.args, ra, gb));
+    ++c->launches;
+    int herr = 0;
+    CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (herr) fail(W1MG_ECUDA, "row-resident PDHG (clusters): grid barrier timed out");
+    rs_print_stamps(c, ra.stamps, m, G, R, 8);
     return true;
 }
 
@@ -543,6 +624,7 @@ bool launch_pdhg_rs_q(w1mg_ctx* c, const PLevel& lv) {
         if (h <= 32) return launch_pdhg_rs_qt<Q, 2>(c, lv, R);
         return launch_pdhg_rs_qt<Q, 4>(c, lv, R);
     }
+    if ((m & 1) && h <= kRs2HP && g_pdhg_rs != 2 && launch_pdhg_rs2_q<Q>(c, lv)) return true;
     int Rp = 1;
     while (Rp < R) Rp <<= 1;  // the prime-factor transforms split vectors by shifts
     if (Rp > 16) return false;

@@ -90,7 +90,7 @@ def pdhg_engine(request):
     L.w1mg_set_option(b"pdhg_rs", 1)
 
 
-@pytest.mark.parametrize("n", [31, 32, 48, 64, 100, 128, 256])
+@pytest.mark.parametrize("n", [31, 32, 48, 64, 100, 128, 150, 256])
 @pytest.mark.parametrize("p", [0, 1, 2])
 def test_pdhg_fixed_iterations(p, n, pdhg_engine):
     rho = instances.config1_source(n)
