@@ -15,6 +15,7 @@
 #include "pdhg_persist.cuh"
 #include "pdhg_rs.cuh"
 #include "pdhg_rs2.cuh"
+#include "pdhg_rspf.cuh"
 
 namespace {
 
@@ -615,6 +616,67 @@ bool launch_pdhg_rs2_q(w1mg_ctx* c, const PLevel& lv) {
     return true;
 }
 
+// m = N1 N2 (odd coprime factors, pdhg_rspf.cuh; instantiated for 513 = 27 x
+// 19): register-stationary prime-factor transforms in the row-resident flow.
+template <int Q, class P>
+bool launch_pdhg_rspf_q(w1mg_ctx* c, const PLevel& lv) {
+    const int m = P::M;
+    const int R = (m + c->num_sms - 1) / c->num_sms, G = (m + R - 1) / R;
+    const size_t smem = rspf_smem_doubles<P>(R) * sizeof(double);
+    if (smem > kDctSmemMax || G > c->num_sms) return false;
+    static unsigned long long attr = 0;  // per device
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!(attr >> (dev & 63) & 1ull)) {
+        CK(cudaFuncSetAttribute(pdhg_rspf_kernel<Q, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kDctSmemMax));
+        attr |= 1ull << (dev & 63);
+    }
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdhg_rspf_kernel<Q, P>, kRsThreads, smem));
+    if (occ < 1) return false;
+    const std::string kt = "rspf.tab." + std::to_string(m);
+    const bool ft = c->bufs.find(kt) == c->bufs.end();
+    short* dtab = c->get<short>(kt, P::NTAB);
+    if (ft) {
+        std::vector<short> ht(P::NTAB);
+        rspf_tables<P>(ht.data());
+        CK(cudaMemcpy(dtab, ht.data(), ht.size() * sizeof(short), cudaMemcpyHostToDevice));
+    }
+    const RsTables tb = rs_tables(c, lv.n, false);
+    RsArgs ra{};
+    ra.m = m;
+    ra.h = (m - 1) / 2;
+    ra.R = R;
+    ra.G = G;
+    ra.posDC = 0;
+    ra.cosq = tb.cosq;
+    ra.lamq = tb.lamq;
+    ra.scale = 1.0 / (4.0 * double(m) * double(m));  // poisson.cpp:93
+    ra.part = c->get<double>("rs.part", (size_t)3 * G);
+    unsigned* bar = c->get<unsigned>("persist.bar", 2);
+    int* err = c->get<int>("persist.err", 1);
+    CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), c->stream));
+    CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
+    GridBar gb{bar, bar + 1, err};
+    if (std::getenv("W1MG_PERSIST_STAMPS")) {
+        ra.stamps = c->get<unsigned long long>("persist.stamps", 640);
+        CK(cudaMemsetAsync(ra.stamps, 0, 640 * 8, c->stream));
+    }
+    SweepArgs a = lv.args;
+    const short* ctab = dtab;
+    void* args[] = {(void*)&a, (void*)&ra, (void*)&ctab, (void*)&gb};
+    CK(cudaLaunchCooperativeKernel((const void*)pdhg_rspf_kernel<Q, P>, dim3(G), dim3(kRsThreads), args,
+                                   smem, c->stream));
+    ++c->launches;
+    int herr = 0;
+    CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (herr) fail(W1MG_ECUDA, "row-resident PDHG (prime-factor): grid barrier timed out");
+    rs_print_stamps(c, ra.stamps, m, G, R, -1);
+    return true;
+}
+
 template <int Q>
 bool launch_pdhg_rs_q(w1mg_ctx* c, const PLevel& lv) {
     const int m = lv.n + 1, h = (m - 1) / 2;
@@ -625,6 +687,7 @@ bool launch_pdhg_rs_q(w1mg_ctx* c, const PLevel& lv) {
         return launch_pdhg_rs_qt<Q, 4>(c, lv, R);
     }
     if ((m & 1) && h <= kRs2HP && g_pdhg_rs != 2 && launch_pdhg_rs2_q<Q>(c, lv)) return true;
+    if (m == 513 && g_pdhg_rs != 2 && launch_pdhg_rspf_q<Q, PfGeo<27, 19>>(c, lv)) return true;
     int Rp = 1;
     while (Rp < R) Rp <<= 1;  // the prime-factor transforms split vectors by shifts
     if (Rp > 16) return false;

@@ -106,6 +106,31 @@ def test_pdhg_fixed_iterations(p, n, pdhg_engine):
     np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-7)
 
 
+@pytest.mark.parametrize("rs", [0, 1])
+def test_pdhg_fixed_iterations_finest(rs):
+    """Config 3's finest level (m = 513 = 27 x 19): the register-stationary
+    prime-factor engine (pdhg_rspf.cuh, rs = 1) and the previous persistent
+    engine (rs = 0) against the numpy oracle."""
+    from paper_1810_00118_b200 import _lib
+
+    L = _lib.lib()
+    L.w1mg_set_option(b"pdhg_rs", rs)
+    try:
+        n = 512
+        rho = instances.config1_source(n)
+        prm = w1mg.SolverParams(p=w1mg.PNorm.p2, tolerance=-1.0, max_iters=100)
+        rep = w1mg.pdhg_run(_src(rho), prm)
+        ref = PO.pdhg_run(rho, p=1, tol=-1.0, max_iters=100)
+        assert rep.iterations == 100
+        assert _rel(rep.flux.x_edges, ref.mx) <= FIELD_TOL
+        assert _rel(rep.flux.y_edges, ref.my) <= FIELD_TOL
+        assert _rel(rep.dual_flux.x_edges, ref.px) <= FIELD_TOL
+        assert _rel(rep.potential.values, ref.phi) <= FIELD_TOL
+        np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-7)
+    finally:
+        L.w1mg_set_option(b"pdhg_rs", 1)
+
+
 def test_pdhg_converged_config1_like():
     """SURVEY finding 9: N=32, p=2 -> W1 = 0.5053635, recovered dual ~ +W1."""
     rho = instances.config1_source(32)
