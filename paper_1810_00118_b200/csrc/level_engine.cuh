@@ -510,8 +510,9 @@ int g_slab_min_n = 1024;
 // one-pair PDHG levels above that run level-persistent (pdhg_persist.cuh:
 // all iterations in one cooperative launch): 1 = on (default), 0 = off
 int g_pdhg_persist = 1;
-// ... row-resident (pdhg_rs.cuh) where it fits: 0 off, 1 auto (default), 2 the
-// prime-factor transforms at every size, 3 also instead of the one-CTA kernel
+// ... row-resident (pdhg_rs.cuh / pdhg_rs2.cuh / pdhg_rspf.cuh) where it fits:
+// 0 off, 1 auto (default), 2 the prime-factor transforms of dct_kernels.cuh
+// at every size (3 = 1, kept for scripts)
 int g_pdhg_rs = 1;
 
 // cluster-size rule (W1MG_CLUSTER_PICK): 1 = fewest node passes per phase

@@ -426,8 +426,10 @@ bool launch_pdhg_persist(w1mg_ctx* c, const PLevel& lv, int q) {
 // Row-resident level-persistent PDHG for one pair (pdhg_rs.cuh): rows of the
 // state in shared memory for the whole level, two grid barriers per
 // iteration, register-stationary dense DCT for m <= 129 (odd), prime-factor
-// transforms above.  g_pdhg_rs (level_engine.cuh): 0 off, 1 auto, 2 forces
-// the prime-factor transforms (A/B), 3 also replaces the one-CTA small kernel.
+// transforms above.  g_pdhg_rs (level_engine.cuh): 0 off, 1 auto (every
+// one-pair level, also instead of the one-CTA small kernel: 7.4 vs 12 us per
+// iteration at 33^2), 2 forces the prime-factor transforms of
+// dct_kernels.cuh (A/B).
 
 struct RsTables {
     const double* cosq;
@@ -463,24 +465,34 @@ RsTables rs_tables(w1mg_ctx* c, int n, bool dense) {
     return RsTables{dc, dl};
 }
 
-// per-phase ns of iterations 8..62 (CTA 0): A, barrier, B, barrier, C, D
+// ns between consecutive time stamps of CTA 0 (iterations 8..62 averaged);
+// the stamps in use are listed in the kernels (0 = iteration start)
 void rs_print_stamps(w1mg_ctx* c, const unsigned long long* stamps, int m, int G, int R, int TS) {
     (void)c;
     if (!stamps) return;
-    std::vector<unsigned long long> h(640);
-    CK(cudaMemcpy(h.data(), stamps, 640 * 8, cudaMemcpyDeviceToHost));
-    double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    const int NS = kRsStampSlots;
+    std::vector<unsigned long long> h((size_t)64 * NS);
+    CK(cudaMemcpy(h.data(), stamps, h.size() * 8, cudaMemcpyDeviceToHost));
+    std::vector<double> acc(NS, 0.0);
+    double tot = 0.0;
     int cnt = 0;
     for (int it = 8; it < 62; ++it) {
-        if (!h[(it + 1) * 10]) break;
-        for (int q = 0; q < 6; ++q) acc[q] += double(h[it * 10 + q + 1] - h[it * 10 + q]);
-        acc[6] += double(h[(it + 1) * 10] - h[it * 10]);
+        if (!h[(size_t)(it + 1) * NS]) break;
+        unsigned long long prev = h[(size_t)it * NS];
+        for (int q = 1; q < NS; ++q) {
+            const unsigned long long t = h[(size_t)it * NS + q];
+            if (!t) continue;
+            acc[q] += double(t - prev);
+            prev = t;
+        }
+        tot += double(h[(size_t)(it + 1) * NS] - h[(size_t)it * NS]);
         ++cnt;
     }
-    if (cnt)
-        std::fprintf(stderr, "rs m=%d G=%d R=%d TS=%d ns: A %.0f bar %.0f B %.0f bar %.0f C %.0f D %.0f | iter %.0f\n",
-                     m, G, R, TS, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
-                     acc[4] / cnt, acc[5] / cnt, acc[6] / cnt);
+    if (!cnt) return;
+    std::fprintf(stderr, "rs m=%d G=%d R=%d TS=%d ns:", m, G, R, TS);
+    for (int q = 1; q < NS; ++q)
+        if (acc[q] > 0.0) std::fprintf(stderr, " [%d] %.0f", q, acc[q] / cnt);
+    std::fprintf(stderr, " | iter %.0f\n", tot / cnt);
 }
 
 template <int Q, int TS>
@@ -524,8 +536,8 @@ bool launch_pdhg_rs_qt(w1mg_ctx* c, const PLevel& lv, int R) {
     GridBar gb{bar, bar + 1, err};
     ra.stamps = nullptr;
     if (std::getenv("W1MG_PERSIST_STAMPS")) {
-        ra.stamps = c->get<unsigned long long>("persist.stamps", 640);
-        CK(cudaMemsetAsync(ra.stamps, 0, 640 * 8, c->stream));
+        ra.stamps = c->get<unsigned long long>("rs.stamps", 64 * kRsStampSlots);
+        CK(cudaMemsetAsync(ra.stamps, 0, 64 * kRsStampSlots * 8, c->stream));
     }
     SweepArgs a = lv.args;
     DctPlan pp = p;
@@ -550,7 +562,7 @@ bool launch_pdhg_rs2_q(w1mg_ctx* c, const PLevel& lv) {
     const int R = (m + 2 * NC - 1) / (2 * NC);
     const int G = 2 * ((m + 2 * R - 1) / (2 * R));
     const size_t smem = rs2_smem_doubles(m, R) * sizeof(double);
-    if (smem > kDctSmemMax) return false;
+    if (smem > kDctSmemMax || 2 * R + 2 > kRs2NV) return false;
     static unsigned long long attr = 0;  // per device
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -602,8 +614,8 @@ bool launch_pdhg_rs2_q(w1mg_ctx* c, const PLevel& lv) {
     GridBar gb{bar, bar + 1, err};
     ra.stamps = nullptr;
     if (std::getenv("W1MG_PERSIST_STAMPS")) {
-        ra.stamps = c->get<unsigned long long>("persist.stamps", 640);
-        CK(cudaMemsetAsync(ra.stamps, 0, 640 * 8, c->stream));
+        ra.stamps = c->get<unsigned long long>("rs.stamps", 64 * kRsStampSlots);
+        CK(cudaMemsetAsync(ra.stamps, 0, 64 * kRsStampSlots * 8, c->stream));
     }
     (void)ms;
     CK(cudaLaunchKernelEx(&cfg, pdhg_rs2_kernel<Q>, lv.args, ra, gb));
@@ -623,7 +635,7 @@ bool launch_pdhg_rspf_q(w1mg_ctx* c, const PLevel& lv) {
     const int m = P::M;
     const int R = (m + c->num_sms - 1) / c->num_sms, G = (m + R - 1) / R;
     const size_t smem = rspf_smem_doubles<P>(R) * sizeof(double);
-    if (smem > kDctSmemMax || G > c->num_sms) return false;
+    if (smem > kDctSmemMax || G > c->num_sms || R * m > 5 * kRsThreads) return false;
     static unsigned long long attr = 0;  // per device
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -660,8 +672,8 @@ bool launch_pdhg_rspf_q(w1mg_ctx* c, const PLevel& lv) {
     CK(cudaMemsetAsync(err, 0, sizeof(int), c->stream));
     GridBar gb{bar, bar + 1, err};
     if (std::getenv("W1MG_PERSIST_STAMPS")) {
-        ra.stamps = c->get<unsigned long long>("persist.stamps", 640);
-        CK(cudaMemsetAsync(ra.stamps, 0, 640 * 8, c->stream));
+        ra.stamps = c->get<unsigned long long>("rs.stamps", 64 * kRsStampSlots);
+        CK(cudaMemsetAsync(ra.stamps, 0, 64 * kRsStampSlots * 8, c->stream));
     }
     SweepArgs a = lv.args;
     const short* ctab = dtab;
@@ -730,7 +742,7 @@ void launch_pdhg_small(w1mg_ctx* c, const PLevel& lv) {
 // watches the done counter one graph behind, like run_sweeps).
 void run_pdhg_iters(w1mg_ctx* c, const PLevel& lv, int q, long max_iters) {
     if (max_iters <= 0) return;
-    if (g_pdhg_rs == 3 && launch_pdhg_rs(c, lv, q)) return;
+    if (g_pdhg_rs && launch_pdhg_rs(c, lv, q)) return;  // one pair: row-resident persistent engine
     if ((g_pdhg_small == 1 && lv.n + 1 <= kPdhgSmallAutoM) ||
         (g_pdhg_small == 2 && lv.n + 1 <= kPdhgSmallMaxM)) {
         if (q == 0) launch_pdhg_small<0>(c, lv);
@@ -738,7 +750,6 @@ void run_pdhg_iters(w1mg_ctx* c, const PLevel& lv, int q, long max_iters) {
         else launch_pdhg_small<2>(c, lv);
         return;
     }
-    if (launch_pdhg_rs(c, lv, q)) return;
     if (launch_pdhg_persist(c, lv, q)) return;
     constexpr int K = 8;
     if (max_iters < K) {

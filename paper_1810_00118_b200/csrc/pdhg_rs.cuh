@@ -48,6 +48,7 @@
 namespace w1mg_dev {
 
 constexpr int kRsThreads = 512;
+constexpr int kRsStampSlots = 24;  // diagnostics: time stamps per iteration (CTA 0)
 
 struct RsArgs {
     int m, h, R, G;       // m = 2h+1 nodes per side, R rows (columns) per CTA, G CTAs
@@ -335,7 +336,7 @@ pdhg_rs_kernel(const SweepArgs a, const DctPlan g, const RsArgs ra, GridBar gb) 
     unsigned gen = 0;
     long iter = 0;
     auto stamp = [&](int q) {
-        if (ra.stamps && c == 0 && tid == 0 && iter < 64) ra.stamps[iter * 10 + q] = gtimer();
+        if (ra.stamps && c == 0 && tid == 0 && iter < 64) ra.stamps[iter * kRsStampSlots + q] = gtimer();
     };
     auto flush_state = [&]() {
         const int gs[6] = {P_MX, P_MY, P_PX, P_PY, P_BX, P_BY};

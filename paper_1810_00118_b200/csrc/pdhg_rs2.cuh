@@ -17,11 +17,19 @@
 //            O_i (odd part) for all the cluster's vectors and stores them
 //            into the shared memory of the CTA that owns the vector; one
 //            cluster barrier, then y_i = E_i + O_i, y_{m-1-i} = E_i - O_i.
-// Thread (warp wq, lane): rows q = 16 r + wq (r < 8), columns i = 32 s + lane
-// (s < 4).  The DCT-II sums over i run in registers and end in a 9-shuffle
-// butterfly inside the warp (no shared-memory exchange, no second phase); the
-// DCT-III sums over q leave 16 per-warp partials per output, summed through
-// shared memory.
+// The products run on the FP64 tensor cores (mma.sync.m8n8k4.f64: 256 FMAs per
+// warp instruction, the N = 8 columns are the cluster's vectors), because the
+// scalar form was issue-bound (a 9-shuffle butterfly per vector and warp for
+// the DCT-II, a shared-memory partial exchange for the DCT-III):
+//   DCT-II   warp wq owns the rows q = 8 wq .. 8 wq + 7 of its half; its A
+//            fragments c(q, 4 it + lane % 4), it < 32, stay in REGISTERS for
+//            the whole level; the B fragments are the folded vectors (shared
+//            memory); the accumulators are the finished outputs;
+//   DCT-III  warp wq owns the outputs i = 8 wq .. 8 wq + 7; the A fragments of
+//            the transposed matrix c(4 qt + lane % 4, i) are staged once per
+//            level in shared memory in fragment order (conflict-free loads).
+// The rank-one terms (constant mode, middle sample) are one more row of ones /
+// alternating signs on warp 0.
 //
 // The iteration structure, the shadow row, the deferred stop rule and the
 // plane/position conventions are those of pdhg_rs.cuh (reference semantics:
@@ -32,35 +40,23 @@
 
 namespace w1mg_dev {
 
-constexpr int kRs2KB = 8, kRs2IB = 4, kRs2HP = 128;  // rows / columns per thread, padded half
+constexpr int kRs2HP = 128;   // padded half size: h <= 128
+constexpr int kRs2HS = 132;   // row stride of the folded / spectral vectors (conflict-free B fragments)
+constexpr int kRs2NV = 8;     // rows of the vector buffers = the N of the MMA
 
-// 8 per-lane values -> the sum over the 32 lanes of value r = 4 b4 + 2 b3 + b2
-// (b = bits of the lane index), replicated over the lane's low two bits.
-__device__ __forceinline__ double rs2_butterfly(const double (&v)[8], int lane) {
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-    double u[4], t[2];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const double send = b4 ? v[j] : v[j + 4], keep = b4 ? v[j + 4] : v[j];
-        u[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const double send = b3 ? u[j] : u[j + 2], keep = b3 ? u[j + 2] : u[j];
-        t[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    const double send = b2 ? t[0] : t[1], keep = b2 ? t[1] : t[0];
-    double w = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    w += __shfl_xor_sync(0xffffffffu, w, 2);
-    w += __shfl_xor_sync(0xffffffffu, w, 1);
-    return w;
+// D (8 x 8) += A (8 x 4, row) B (4 x 8, col), fp64: lane holds A[lane/4][lane%4],
+// B[lane%4][lane/4], D[lane/4][2 (lane%4) + {0, 1}]
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
 }
 
 // Dynamic shared memory (doubles)
 __host__ __device__ inline size_t rs2_smem_doubles(int m, int R) {
-    const int ms = m + 1, hs = (m - 1) / 2 + 2;
-    return (size_t)ms * (1 + 7 * (R + 1) + (R + 2)) + (size_t)hs * ((2 * R + 2) + 2 * R + 2 * (R + 2)) +
-           (size_t)(2 * R + 2) * (kRs2HP + 1) * 17 + 8;
+    const int ms = m + 1;
+    return (size_t)ms * (1 + 7 * (R + 1) + (R + 2)) + (size_t)kRs2HS * (2 * kRs2NV + 2 * (R + 2)) +
+           (size_t)16 * 32 * 32 + 8;
 }
 
 template <int QN>
@@ -77,7 +73,8 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
     const long max_it = ctl->max_it;
     const double tol = ctl->tol;
     const int m = ra.m, n = m - 1, h = ra.h, R = ra.R, G = (int)gridDim.x;
-    const int ms = m + 1, hs = h + 2, tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    const int ms = m + 1, tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
+    constexpr int hs = kRs2HS;
     const int c = blockIdx.x, e = (int)cluster.block_rank(), base = (c >> 1) * 2 * R;
     const int j0 = base + e * R, nr = max(0, min(R, m - j0));
     const int sh = (nr > 0 && j0 > 0) ? 1 : 0;
@@ -87,36 +84,34 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
     const int VCc = jhi - jlo + 1;                           // rows of the row DCT-III (phase C)
     const Layout L = a.L;
     const double mu = a.mu, tau = a.tau, ih = a.ih, scale = ra.scale;
-    constexpr int PS = (kRs2HP + 1) * 17;
 
     double* lam = rs_sm;
     double* st = lam + ms;
     double* X = st + (size_t)S_N * (R + 1) * ms;
-    double* F = X + (size_t)(R + 2) * ms;        // [2R+2][hs] transform inputs of this half
-    double* FY = F + (size_t)(2 * R + 2) * hs;   // [2R][hs] divided spectrum of this half
-    double* EO = FY + (size_t)(2 * R) * hs;      // [R+2][2][hs] E / O of the vectors this CTA owns
-    double* P3 = EO + (size_t)(R + 2) * 2 * hs;  // [2R+2][PS] DCT-III partials
+    double* F = X + (size_t)(R + 2) * ms;        // [8][hs] transform inputs of this half
+    double* FY = F + (size_t)kRs2NV * hs;        // [8][hs] divided spectrum of this half
+    double* EO = FY + (size_t)kRs2NV * hs;       // [R+2][2][hs] E / O of the vectors this CTA owns
+    double* A3 = EO + (size_t)(R + 2) * 2 * hs;  // [16][32][32] DCT-III A fragments
     double* Fr[2] = {cluster.map_shared_rank(F, 0), cluster.map_shared_rank(F, 1)};
     double* EOr[2] = {cluster.map_shared_rank(EO, 0), cluster.map_shared_rank(EO, 1)};
     auto S = [&](int slot, int sv) { return st + ((size_t)slot * (R + 1) + sv) * ms; };
 
-    // coefficients of this CTA's half: rows q = 16 r + wq, columns i = 32 s + lane
-    double cf[kRs2KB][kRs2IB];
+    // coefficients of this CTA's half c(q, i) = cos(pi k (2i+1) / 2m), k = 2q+2 / 2q+1
+    auto coef = [&](int q, int i) {
+        const int kk = e ? 2 * q + 1 : 2 * q + 2;
+        return (q < h && i < h) ? __ldg(ra.cosq + (kk * (2 * i + 1)) % (4 * m)) : 0.0;
+    };
+    const int fr = lane >> 2, fc = lane & 3;  // fragment row / column of this lane
+    double cfa[32];                           // DCT-II A fragments: rows 8 wq + fr, columns 4 it + fc
 #pragma unroll
-    for (int r = 0; r < kRs2KB; ++r) {
-        const int q = 16 * r + wq, kk = e ? 2 * q + 1 : 2 * q + 2;
-#pragma unroll
-        for (int s = 0; s < kRs2IB; ++s) {
-            const int i = 32 * s + lane;
-            cf[r][s] = (q < h && i < h) ? __ldg(ra.cosq + (kk * (2 * i + 1)) % (4 * m)) : 0.0;
-        }
-    }
+    for (int it = 0; it < 32; ++it) cfa[it] = coef(8 * wq + fr, 4 * it + fc);
+    for (int qt = 0; qt < 32; ++qt)           // DCT-III: A[i = 8 wq + fr][q = 4 qt + fc]
+        A3[(wq * 32 + qt) * 32 + lane] = coef(4 * qt + fc, 8 * wq + fr);
 
     for (int x = tid; x < m; x += kRsThreads) lam[x] = ra.lamq[x];
     for (int x = tid; x < S_N * (R + 1) * ms; x += kRsThreads) st[x] = 0.0;
     for (int x = tid; x < (R + 2) * ms; x += kRsThreads) X[x] = 0.0;
-    for (int x = tid; x < (2 * R + 2) * hs; x += kRsThreads) F[x] = 0.0;
-    for (int x = tid; x < 2 * R * hs; x += kRsThreads) FY[x] = 0.0;
+    for (int x = tid; x < 2 * kRs2NV * hs; x += kRsThreads) F[x] = 0.0;  // F and FY
     __syncthreads();
     {
         const int gs[S_N] = {P_MX, P_MY, P_PX, P_PY, P_BX, P_BY, P_RHO};
@@ -133,7 +128,7 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
     unsigned gen = 0;
     long iter = 0;
     auto stamp = [&](int q) {
-        if (ra.stamps && c == 0 && tid == 0 && iter < 64) ra.stamps[iter * 10 + q] = gtimer();
+        if (ra.stamps && c == 0 && tid == 0 && iter < 64) ra.stamps[iter * kRsStampSlots + q] = gtimer();
     };
 
     // fold the CTA's nr vectors X[v] and hand s to rank 0, d to rank 1
@@ -152,36 +147,39 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             }
         }
     };
-    // this half of the DCT-II of the cluster's vectors F[w], w < V: out(w, pos, X_k)
+    // this half of the DCT-II of the cluster's vectors F[w], w < V <= 8: out(w, pos, X_k)
     auto dct2_half = [&](int V, auto out) {
-        for (int w = 0; w < V; ++w) {
-            const double* f = F + w * hs;
-            double in[kRs2IB];
+        const double* fb = F + fr * hs + fc;  // B[k = fc][n = fr] = F[vector fr][4 it + fc]
+        double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-            for (int s = 0; s < kRs2IB; ++s) {
-                const int i = 32 * s + lane;
-                in[s] = (i < h) ? f[i] : 0.0;
-            }
-            double acc[kRs2KB];
+        for (int it = 0; it < 32; ++it) {
+            dmma884(d0, d1, cfa[it], fb[4 * it]);
+            if ((it & 7) == 7) asm volatile("" ::: "memory");  // loads in batches of 8 (registers)
+        }
+        const int q = 8 * wq + fr;
 #pragma unroll
-            for (int r = 0; r < kRs2KB; ++r) {
-                double t = 0.0;
+        for (int cc = 0; cc < 2; ++cc) {
+            const int w = 2 * fc + cc;
+            const double sum = cc ? d1 : d0;
+            if (w < V && q < h) {
+                if (e) {
+                    out(w, h + q, 2.0 * sum);
+                } else {
+                    const double xh = F[w * hs + h];
+                    out(w, q, 2.0 * (sum + ((q & 1) ? xh : -xh)));  // cos(pi k / 2), k = 2q+2
+                }
+            }
+        }
+        if (e == 0 && wq == 0) {  // constant mode: a row of ones
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll 8
+            for (int it = 0; it < 32; ++it) dmma884(c0, c1, (4 * it + fc < h) ? 1.0 : 0.0, fb[4 * it]);
+            if (fr == 0) {
 #pragma unroll
-                for (int s = 0; s < kRs2IB; ++s) t = fma(cf[r][s], in[s], t);
-                acc[r] = t;
-            }
-            const double sum = rs2_butterfly(acc, lane);
-            const int r = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-            const int q = 16 * r + wq;
-            const double xh = e ? 0.0 : f[h];
-            if ((lane & 3) == 0 && q < h) {
-                if (e) out(w, h + q, 2.0 * sum);
-                else out(w, q, 2.0 * (sum + ((q & 1) ? xh : -xh)));  // cos(pi k / 2), k = 2q+2
-            }
-            if (e == 0 && wq == 0) {  // constant mode: plain sum of the symmetric part
-                double dc = (in[0] + in[1]) + (in[2] + in[3]);
-                dc = warp_sum(dc);
-                if (lane == 0) out(w, 2 * h, 2.0 * (dc + xh));
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int w = 2 * fc + cc;
+                    if (w < V) out(w, 2 * h, 2.0 * ((cc ? c1 : c0) + F[w * hs + h]));
+                }
             }
         }
     };
@@ -189,36 +187,32 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
     // constant mode at [h] on rank 0): E (rank 0) or O (rank 1) -> send(w, i, val),
     // i <= h (i = h: the middle sample, rank 0 only)
     auto dct3_half = [&](int V, const double* src, auto send) {
-        for (int w = 0; w < V; ++w) {
-            const double* y = src + w * hs;
-            double in[kRs2KB];
+        const double* yb = src + fr * hs + fc;  // B[k = fc][n = fr] = src[vector fr][4 qt + fc]
+        const double* a3 = A3 + (wq * 32) * 32 + lane;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll 8
+        for (int qt = 0; qt < 32; ++qt) dmma884(d0, d1, a3[qt * 32], yb[4 * qt]);
+        const int i = 8 * wq + fr;
 #pragma unroll
-            for (int r = 0; r < kRs2KB; ++r) {
-                const int q = 16 * r + wq;
-                in[r] = (q < h) ? y[q] : 0.0;
-            }
-            double* p = P3 + (size_t)w * PS + lane * 17 + wq;
-#pragma unroll
-            for (int s = 0; s < kRs2IB; ++s) {
-                double t = 0.0;
-#pragma unroll
-                for (int r = 0; r < kRs2KB; ++r) t = fma(cf[r][s], in[r], t);
-                p[s * 32 * 17] = t;
-            }
-            if (e == 0 && lane == 0) {  // middle sample: sum of X_k cos(pi k / 2), k even
-                double mp = 0.0;
-#pragma unroll
-                for (int r = 0; r < kRs2KB; ++r) mp += ((16 * r + wq) & 1) ? in[r] : -in[r];
-                P3[(size_t)w * PS + kRs2HP * 17 + wq] = mp;
-            }
+        for (int cc = 0; cc < 2; ++cc) {
+            const int w = 2 * fc + cc;
+            const double sum = cc ? d1 : d0;
+            if (w < V && i < h) send(w, i, e ? 2.0 * sum : src[w * hs + h] + 2.0 * sum);
         }
-        __syncthreads();
-        const int per = e ? h : h + 1;
-        for (int x = tid; x < V * per; x += kRsThreads) {
-            int w, i;
-            rs_split(x, per, w, i);
-            const double sum = rs_sum16(P3 + (size_t)w * PS + (i < h ? i : kRs2HP) * 17);
-            send(w, i, e ? 2.0 * sum : src[w * hs + h] + 2.0 * sum);
+        if (e == 0 && wq == 0) {  // middle sample: sum of X_k cos(pi k / 2), k = 2q+2
+            double c0 = 0.0, c1 = 0.0;
+#pragma unroll 8
+            for (int qt = 0; qt < 32; ++qt) {
+                const int q = 4 * qt + fc;
+                dmma884(c0, c1, (q < h) ? ((q & 1) ? 1.0 : -1.0) : 0.0, yb[4 * qt]);
+            }
+            if (fr == 0) {
+#pragma unroll
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int w = 2 * fc + cc;
+                    if (w < V) send(w, h, src[w * hs + h] + 2.0 * (cc ? c1 : c0));
+                }
+            }
         }
     };
     // y of the owned vector x from its E / O rows: out(i, y_i)
@@ -252,12 +246,14 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             X[v * ms + i] = div - S(S_RHO, sv)[i];
         }
         __syncthreads();
+        stamp(1);
         fold_send();
         cluster.sync();
-        dct2_half(VC, [&](int w, int pos, double val) { T1[L.at(base + w, pos)] = val; });
-        stamp(1);
-        if (!grid_barrier(gb, gen, &s_ok)) return;
         stamp(2);
+        dct2_half(VC, [&](int w, int pos, double val) { T1[L.at(base + w, pos)] = val; });
+        stamp(11);
+        if (!grid_barrier(gb, gen, &s_ok)) return;
+        stamp(12);
         double pt0 = 0.0, pt1 = 0.0, pt2 = 0.0;  // Eq. 12 partials of the previous iteration
         if (iter > 0 && tid < G) {
             pt0 = __ldcg(ra.part + 3 * tid + 0);
@@ -272,21 +268,26 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             X[v * ms + j] = __ldcg(T1 + L.at(j, j0 + v));
         }
         __syncthreads();
+        stamp(5);
         fold_send();
         cluster.sync();
+        stamp(6);
         dct2_half(VC, [&](int w, int pos, double val) {
             const int p1 = base + w;
             const double y = (p1 == 2 * h && pos == 2 * h) ? 0.0 : val / (lam[p1] + lam[pos]);
             FY[w * hs + (pos == 2 * h ? h : (e ? pos - h : pos))] = y;
         });
         __syncthreads();
+        stamp(7);
         dct3_half(VC, FY, [&](int w, int i, double val) {
             const int o = w / R;  // owner rank of column base + w
             EOr[o][((size_t)(2 * (w - o * R)) + e) * hs + i] = val;
         });
         cluster.sync();
+        stamp(8);
         for (int v = 0; v < nr; ++v)
             combine(v, [&](int j, double val) { T2[L.at(j0 + v, j)] = val; });
+        stamp(9);
         // ---- stop rule of the previous iteration (identical in every CTA)
         if (iter > 0) {
             pt0 = warp_sum(pt0);
@@ -334,9 +335,9 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
                 return;
             }
         }
-        stamp(3);
+        stamp(11);
         if (!grid_barrier(gb, gen, &s_ok)) return;
-        stamp(4);
+        stamp(12);
         // ---- C: rows jlo .. jhi of T2 (the cluster's rows, the shadow row
         // below and the halo row above): DCT-III along i; afterwards X row x
         // holds psi = y / (4 m^2) (poisson.cpp:93) of row j0 - sh + x
@@ -350,6 +351,7 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             }
         }
         __syncthreads();
+        stamp(13);
         dct3_half(VCc, F, [&](int w, int i, double val) {
             const int jj = jlo + w;
 #pragma unroll
@@ -362,10 +364,11 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             }
         });
         cluster.sync();
+        stamp(14);
         for (int x = 0; x < sh + nr + hl; ++x)
             combine(x, [&](int i, double val) { X[x * ms + i] = scale * val; });
         __syncthreads();
-        stamp(5);
+        stamp(16);
         // ---- D: post step (pdhg_post_kernel's arithmetic) on the shadow and
         // owned rows; Eq. 12 partial sums over the owned rows only
         double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
@@ -437,7 +440,7 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             ra.part[c * 3 + 1] = t1;
             ra.part[c * 3 + 2] = t2;
         }
-        stamp(6);
+        stamp(17);
     }
 }
 

@@ -50,7 +50,7 @@ struct PfGeo {
     static constexpr int NU = 32 / H2;          // columns per warp in the N2 stage
     static constexpr int NI0 = H1 * N2;         // items of the W build
     static constexpr int NTAB = M + N2 * N1P + N1 * N2 + 2 * NI0;  // shorts
-    static_assert((N1 & 1) && (N2 & 1) && N1 <= 32 && NU >= 1, "factor sizes");
+    static_assert((N1 & 1) && (N2 & 1) && N1 <= 32 && NU >= 1 && (T1 & 1), "factor sizes");
 };
 
 // host + device: doubles of dynamic shared memory for R rows per CTA
@@ -121,7 +121,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
     const short* crtk = idxg + N2 * N1P;
     const short* i0k = crtk + N1 * N2;
     const short* i0d = i0k + P::NI0;
-    auto S = [&](int slot, int sv) { return st + ((size_t)slot * (R + 1) + sv) * ms; };
+    auto S = [&](int slot, int sv) { return st + (slot * (R + 1) + sv) * ms; };
     const double* rho = pslot(a, 0, P_RHO);
 
     // ---- twiddles in registers
@@ -171,11 +171,20 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
         for (int col = warp; col < V * N2; col += kRsThreads / 32) {
             int v, n2;
             rs_split(col, N2, v, n2);
-            const double* g = GBf + v * P::GB + n2 * N1P;
+            // the column as 16-byte pairs e[a] = (g[2a], g[2a+1]); t and N1 - t meet
+            // from both ends: two pairs feed two steps
+            const double2* g2 = reinterpret_cast<const double2*>(GBf + v * P::GB + n2 * N1P);
             const double sgn = isre ? 1.0 : -1.0;
-            double acc = isre ? g[0] : 0.0;
+            double2 lo = g2[0], hi = g2[(N1 - 1) / 2];
+            double acc = isre ? lo.x : 0.0;
+            acc = fma(cw1[0], fma(sgn, hi.x, lo.y), acc);  // t = 1: g[1], g[N1-1]
 #pragma unroll
-            for (int t = 1; t <= T1; ++t) acc = fma(cw1[t - 1], fma(sgn, g[N1 - t], g[t]), acc);
+            for (int aa = 1; aa <= (T1 - 1) / 2; ++aa) {
+                lo = g2[aa];                    // g[2aa], g[2aa+1]
+                hi = g2[(N1 - 1) / 2 - aa];     // g[N1-1-2aa], g[N1-2aa]
+                acc = fma(cw1[2 * aa - 1], fma(sgn, hi.y, lo.x), acc);  // t = 2aa
+                acc = fma(cw1[2 * aa], fma(sgn, hi.x, lo.y), acc);      // t = 2aa+1
+            }
             double* o = A2 + v * AS + k1l * 2 * N2P + (isre ? 0 : N2P) + n2;
             if (lane < N1) *o = acc;
             if (lane == 0) o[N2P] = 0.0;  // Im A[0] = 0
@@ -259,10 +268,18 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
             int v, n2;
             rs_split(col, N2, v, n2);
             const double* br = GBf + v * P::GB + n2 * 2 * K1P;
-            const double* src = isre ? br : br + K1P;
+            const double2* s2p = reinterpret_cast<const double2*>(isre ? br : br + K1P);
             double acc = 0.0;
+            {
+                const double2 e0 = s2p[0];
+                acc = cw1[0] * e0.y;  // t = 1
 #pragma unroll
-            for (int t = 1; t <= T1; ++t) acc = fma(cw1[t - 1], src[t], acc);
+                for (int aa = 1; aa <= (T1 - 1) / 2; ++aa) {
+                    const double2 ee = s2p[aa];
+                    acc = fma(cw1[2 * aa - 1], ee.x, acc);
+                    acc = fma(cw1[2 * aa], ee.y, acc);
+                }
+            }
             const int peer = isre ? lane + T1 : lane - T1;
             const double oth = __shfl_sync(0xffffffffu, acc, peer & 31);
             const double b0 = br[0];
@@ -287,32 +304,49 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
     unsigned gen = 0;
     long iter = 0;
     auto stamp = [&](int q) {
-        if (ra.stamps && c == 0 && tid == 0 && iter < 64) ra.stamps[iter * 10 + q] = gtimer();
+        if (ra.stamps && c == 0 && tid == 0 && iter < 64) ra.stamps[iter * kRsStampSlots + q] = gtimer();
     };
 
     for (;; ++iter) {
         stamp(0);
         // ---- A: r = A v - rho on the owned rows (poisson.cpp:113-115), DCT-II along i -> T1
-        for (int x = tid; x < nr * m; x += kRsThreads) {
-            int v, i;
-            rs_split(x, m, v, i);
-            const int j = j0 + v, sv = v + 1;
-            const double* mx = S(0, sv);
-            const double* bx = S(4, sv);
-            const double r_ = (i < n) ? mx[i] - mu * bx[i] : 0.0;
-            const double l_ = (i > 0) ? mx[i - 1] - mu * bx[i - 1] : 0.0;
-            const double a_ = (j < n) ? S(1, sv)[i] - mu * S(5, sv)[i] : 0.0;
-            const double b_ = (j > 0) ? S(1, sv - 1)[i] - mu * S(5, sv - 1)[i] : 0.0;
-            const double div = (r_ - l_) * ih + (a_ - b_) * ih;
-            GBf[v * P::GB + ginv[i]] = div - __ldg(rho + L.at(i, j));
+        {
+            constexpr int NIT = 5;  // items per thread (R m <= 5 x 512 checked by the host)
+            double rr[NIT];
+#pragma unroll
+            for (int t = 0; t < NIT; ++t) {  // rho first: independent read-only loads
+                const int x = tid + t * kRsThreads;
+                int v, i;
+                rs_split(x, m, v, i);
+                rr[t] = (x < nr * m) ? __ldg(rho + L.at(i, j0 + v)) : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < NIT; ++t) {
+                const int x = tid + t * kRsThreads;
+                if (x < nr * m) {
+                    int v, i;
+                    rs_split(x, m, v, i);
+                    const int j = j0 + v, sv = v + 1;
+                    const double* mx = S(0, sv);
+                    const double* bx = S(4, sv);
+                    const double r_ = (i < n) ? mx[i] - mu * bx[i] : 0.0;
+                    const double l_ = (i > 0) ? mx[i - 1] - mu * bx[i - 1] : 0.0;
+                    const double a_ = (j < n) ? S(1, sv)[i] - mu * S(5, sv)[i] : 0.0;
+                    const double b_ = (j > 0) ? S(1, sv - 1)[i] - mu * S(5, sv - 1)[i] : 0.0;
+                    const double div = (r_ - l_) * ih + (a_ - b_) * ih;
+                    GBf[v * P::GB + ginv[i]] = div - rr[t];
+                }
+            }
         }
         __syncthreads();
+        stamp(1);
         stage1_fwd(nr);
         __syncthreads();
-        stage2_fwd(nr, [&](int v, int kk, double val) { T1p[L.at(j0 + v, kk)] = val; });
-        stamp(1);
-        if (!grid_barrier(gb, gen, &s_ok)) return;
         stamp(2);
+        stage2_fwd(nr, [&](int v, int kk, double val) { T1p[L.at(j0 + v, kk)] = val; });
+        stamp(11);
+        if (!grid_barrier(gb, gen, &s_ok)) return;
+        stamp(12);
         double pt0 = 0.0, pt1 = 0.0, pt2 = 0.0;  // Eq. 12 partials of the previous iteration
         if (iter > 0 && tid < G) {
             pt0 = __ldcg(ra.part + 3 * tid + 0);
@@ -327,18 +361,24 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
             GBf[v * P::GB + ginv[j]] = __ldcg(T1p + L.at(j, j0 + v));
         }
         __syncthreads();
+        stamp(5);
         stage1_fwd(nr);
         __syncthreads();
+        stamp(6);
         stage2_fwd(nr, [&](int v, int kk, double val) {
             const int p1 = j0 + v;
             X[v * ms + kk] = (p1 == 0 && kk == 0) ? 0.0 : val / (lam[p1] + lam[kk]);
         });
         __syncthreads();
+        stamp(7);
         build_w(nr);
         __syncthreads();
+        stamp(8);
         stage2_inv(nr);
         __syncthreads();
+        stamp(9);
         stage1_inv(nr, [&](int v, int j, double val) { T2p[L.at(j0 + v, j)] = val; });
+        stamp(10);
         // ---- stop rule of the previous iteration (identical in every CTA)
         if (iter > 0) {
             pt0 = warp_sum(pt0);
@@ -385,9 +425,9 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
                 return;
             }
         }
-        stamp(3);
+        stamp(11);
         if (!grid_barrier(gb, gen, &s_ok)) return;
-        stamp(4);
+        stamp(12);
         // ---- C: rows j0-sh .. j0+nr-1+hl of T2: DCT-III along i; afterwards X
         // row w holds psi = y / (4 m^2) (poisson.cpp:93) of row j0 - sh + w
         const int nh = sh + nr + hl;
@@ -397,13 +437,16 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
             X[w * ms + kk] = __ldcg(T2p + L.at(kk, j0 - sh + w));
         }
         __syncthreads();
+        stamp(13);
         build_w(nh);
         __syncthreads();
+        stamp(14);
         stage2_inv(nh);
         __syncthreads();
+        stamp(15);
         stage1_inv(nh, [&](int w, int i, double val) { X[w * ms + i] = scale * val; });
         __syncthreads();
-        stamp(5);
+        stamp(16);
         // ---- D: post step (pdhg_post_kernel's arithmetic) on the shadow and
         // owned rows; Eq. 12 partial sums over the owned rows only
         double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
@@ -475,7 +518,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
             ra.part[c * 3 + 1] = t1;
             ra.part[c * 3 + 2] = t2;
         }
-        stamp(6);
+        stamp(17);
     }
 }
 

@@ -106,6 +106,22 @@ def test_pdhg_fixed_iterations(p, n, pdhg_engine):
     np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-7)
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8, 9, 17])
+def test_pdhg_tiny_grids(n, pdhg_engine):
+    """Every engine on grids of a few nodes (m = 2 ... 18: one or two CTAs,
+    even and odd m, h = (m-1)/2 below one thread tile)."""
+    rng = np.random.default_rng(n)
+    rho = instances.make_source(rng.random((n + 1, n + 1)) + 0.1, rng.random((n + 1, n + 1)) + 0.1, n)
+    prm = w1mg.SolverParams(p=w1mg.PNorm.p2, tolerance=-1.0, max_iters=50)
+    rep = w1mg.pdhg_run(_src(rho), prm)
+    ref = PO.pdhg_run(rho, p=1, tol=-1.0, max_iters=50)
+    assert rep.iterations == 50
+    assert _rel(rep.flux.x_edges, ref.mx) <= FIELD_TOL
+    assert _rel(rep.flux.y_edges, ref.my) <= FIELD_TOL
+    assert _rel(rep.dual_flux.x_edges, ref.px) <= FIELD_TOL
+    np.testing.assert_allclose(rep.residual_history, ref.residual_history, rtol=1e-7, atol=1e-300)
+
+
 @pytest.mark.parametrize("rs", [0, 1])
 def test_pdhg_fixed_iterations_finest(rs):
     """Config 3's finest level (m = 513 = 27 x 19): the register-stationary
