@@ -171,9 +171,12 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             }
         }
         if (e == 0 && wq == 0) {  // constant mode: a row of ones
-            double c0 = 0.0, c1 = 0.0;
+            double ca[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // independent chains
 #pragma unroll 8
-            for (int it = 0; it < 32; ++it) dmma884(c0, c1, (4 * it + fc < h) ? 1.0 : 0.0, fb[4 * it]);
+            for (int it = 0; it < 32; ++it)
+                dmma884(ca[it & 3][0], ca[it & 3][1], (4 * it + fc < h) ? 1.0 : 0.0, fb[4 * it]);
+            const double c0 = (ca[0][0] + ca[1][0]) + (ca[2][0] + ca[3][0]);
+            const double c1 = (ca[0][1] + ca[1][1]) + (ca[2][1] + ca[3][1]);
             if (fr == 0) {
 #pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {
@@ -200,12 +203,14 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             if (w < V && i < h) send(w, i, e ? 2.0 * sum : src[w * hs + h] + 2.0 * sum);
         }
         if (e == 0 && wq == 0) {  // middle sample: sum of X_k cos(pi k / 2), k = 2q+2
-            double c0 = 0.0, c1 = 0.0;
+            double ca[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll 8
             for (int qt = 0; qt < 32; ++qt) {
                 const int q = 4 * qt + fc;
-                dmma884(c0, c1, (q < h) ? ((q & 1) ? 1.0 : -1.0) : 0.0, yb[4 * qt]);
+                dmma884(ca[qt & 3][0], ca[qt & 3][1], (q < h) ? ((q & 1) ? 1.0 : -1.0) : 0.0, yb[4 * qt]);
             }
+            const double c0 = (ca[0][0] + ca[1][0]) + (ca[2][0] + ca[3][0]);
+            const double c1 = (ca[0][1] + ca[1][1]) + (ca[2][1] + ca[3][1]);
             if (fr == 0) {
 #pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {
@@ -262,15 +267,21 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
         }
         // ---- B: columns pos1 = base + w: DCT-II along j, divide by lambda_k1 +
         // lambda_k2 (poisson.cpp:84-89), DCT-III along j -> T2
-        for (int x = tid; x < nr * m; x += kRsThreads) {
-            int v, j;
-            rs_split(x, m, v, j);
-            X[v * ms + j] = __ldcg(T1 + L.at(j, j0 + v));
+        // every CTA reads all the cluster's columns and folds them into its own
+        // half (s on rank 0, d on rank 1): no exchange, no cluster barrier here
+        for (int x = tid; x < VC * (h + 1); x += kRsThreads) {
+            int w, i;
+            rs_split(x, h + 1, w, i);
+            const double* col = T1 + L.at(0, base + w);
+            if (i < h) {
+                const double p = __ldcg(col + i), q = __ldcg(col + m - 1 - i);
+                F[w * hs + i] = e ? p - q : p + q;
+            } else if (e == 0) {
+                F[w * hs + h] = __ldcg(col + h);
+            }
         }
         __syncthreads();
         stamp(5);
-        fold_send();
-        cluster.sync();
         stamp(6);
         dct2_half(VC, [&](int w, int pos, double val) {
             const int p1 = base + w;

@@ -310,33 +310,19 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
     for (;; ++iter) {
         stamp(0);
         // ---- A: r = A v - rho on the owned rows (poisson.cpp:113-115), DCT-II along i -> T1
-        {
-            constexpr int NIT = 5;  // items per thread (R m <= 5 x 512 checked by the host)
-            double rr[NIT];
-#pragma unroll
-            for (int t = 0; t < NIT; ++t) {  // rho first: independent read-only loads
-                const int x = tid + t * kRsThreads;
-                int v, i;
-                rs_split(x, m, v, i);
-                rr[t] = (x < nr * m) ? __ldg(rho + L.at(i, j0 + v)) : 0.0;
-            }
-#pragma unroll
-            for (int t = 0; t < NIT; ++t) {
-                const int x = tid + t * kRsThreads;
-                if (x < nr * m) {
-                    int v, i;
-                    rs_split(x, m, v, i);
-                    const int j = j0 + v, sv = v + 1;
-                    const double* mx = S(0, sv);
-                    const double* bx = S(4, sv);
-                    const double r_ = (i < n) ? mx[i] - mu * bx[i] : 0.0;
-                    const double l_ = (i > 0) ? mx[i - 1] - mu * bx[i - 1] : 0.0;
-                    const double a_ = (j < n) ? S(1, sv)[i] - mu * S(5, sv)[i] : 0.0;
-                    const double b_ = (j > 0) ? S(1, sv - 1)[i] - mu * S(5, sv - 1)[i] : 0.0;
-                    const double div = (r_ - l_) * ih + (a_ - b_) * ih;
-                    GBf[v * P::GB + ginv[i]] = div - rr[t];
-                }
-            }
+        for (int x = tid; x < nr * m; x += kRsThreads) {
+            int v, i;
+            rs_split(x, m, v, i);
+            const int j = j0 + v, sv = v + 1;
+            const double rr = __ldg(rho + L.at(i, j));
+            const double* mx = S(0, sv);
+            const double* bx = S(4, sv);
+            const double r_ = (i < n) ? mx[i] - mu * bx[i] : 0.0;
+            const double l_ = (i > 0) ? mx[i - 1] - mu * bx[i - 1] : 0.0;
+            const double a_ = (j < n) ? S(1, sv)[i] - mu * S(5, sv)[i] : 0.0;
+            const double b_ = (j > 0) ? S(1, sv - 1)[i] - mu * S(5, sv - 1)[i] : 0.0;
+            const double div = (r_ - l_) * ih + (a_ - b_) * ih;
+            GBf[v * P::GB + ginv[i]] = div - rr;
         }
         __syncthreads();
         stamp(1);
