@@ -603,7 +603,7 @@ int w1mg_set_option(const char* name, long value) {
     const std::string k(name);
     const int v = (int)value;
     if (k == "pdhg_persist" && (v == 0 || v == 1)) g_pdhg_persist = v;
-    else if (k == "pdhg_rs" && v >= 0 && v <= 3) g_pdhg_rs = v;
+    else if (k == "pdhg_rs" && v >= 0 && v <= 4) g_pdhg_rs = v;
     else if (k == "slab_min_n" && v >= 1) g_slab_min_n = v;
     else if (k == "pdhg_small" && v >= 0 && v <= 2) g_pdhg_small = v;
     else if (k == "cluster_pick" && (v == 0 || v == 1)) g_cluster_pick = v;

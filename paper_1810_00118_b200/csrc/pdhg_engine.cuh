@@ -698,7 +698,8 @@ bool launch_pdhg_rs_q(w1mg_ctx* c, const PLevel& lv) {
         if (h <= 32) return launch_pdhg_rs_qt<Q, 2>(c, lv, R);
         return launch_pdhg_rs_qt<Q, 4>(c, lv, R);
     }
-    if ((m & 1) && h <= kRs2HP && g_pdhg_rs != 2 && launch_pdhg_rs2_q<Q>(c, lv)) return true;
+    // (4: no cluster launches -- ncu cannot replay a cooperative cluster launch)
+    if ((m & 1) && h <= kRs2HP && g_pdhg_rs != 2 && g_pdhg_rs != 4 && launch_pdhg_rs2_q<Q>(c, lv)) return true;
     if (m == 513 && g_pdhg_rs != 2 && launch_pdhg_rspf_q<Q, PfGeo<27, 19>>(c, lv)) return true;
     int Rp = 1;
     while (Rp < R) Rp <<= 1;  // the prime-factor transforms split vectors by shifts
