@@ -500,7 +500,7 @@ bool launch_pdhg_rs_qt(w1mg_ctx* c, const PLevel& lv, int R) {
     const DctPlan& p = lv.dp;
     const int m = p.m, G = (m + R - 1) / R, ms = m + 1;
     const size_t smem = rs_smem_doubles(p, R, TS) * sizeof(double);
-    if (smem > kDctSmemMax || G > c->num_sms) return false;
+    if (smem > kDctSmemMax || G + 1 > c->num_sms) return false;  // + the reducer CTA
     static unsigned long long attr = 0;  // per device
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -528,6 +528,8 @@ bool launch_pdhg_rs_qt(w1mg_ctx* c, const PLevel& lv, int R) {
     ra.psb = c->get<double>("rs.psb", (size_t)G * ms);
     ra.flag = c->get<unsigned>("rs.flag", (size_t)2 * G);
     ra.part = c->get<double>("rs.part", (size_t)3 * G);
+    ra.dec = c->get<int>("rs.dec", 2);
+    CK(cudaMemsetAsync(ra.dec, 0, 2 * sizeof(int), c->stream));
     CK(cudaMemsetAsync(ra.flag, 0, sizeof(unsigned) * 2 * G, c->stream));
     unsigned* bar = c->get<unsigned>("persist.bar", 2);
     int* err = c->get<int>("persist.err", 1);
@@ -542,7 +544,7 @@ bool launch_pdhg_rs_qt(w1mg_ctx* c, const PLevel& lv, int R) {
     SweepArgs a = lv.args;
     DctPlan pp = p;
     void* args[] = {(void*)&a, (void*)&pp, (void*)&ra, (void*)&gb};
-    CK(cudaLaunchCooperativeKernel((const void*)pdhg_rs_kernel<Q, TS>, dim3(G), dim3(kRsThreads), args,
+    CK(cudaLaunchCooperativeKernel((const void*)pdhg_rs_kernel<Q, TS>, dim3(G + 1), dim3(kRsThreads), args,
                                    smem, c->stream));
     ++c->launches;
     int herr = 0;
@@ -558,7 +560,7 @@ bool launch_pdhg_rs_qt(w1mg_ctx* c, const PLevel& lv, int R) {
 template <int Q>
 bool launch_pdhg_rs2_q(w1mg_ctx* c, const PLevel& lv) {
     const int m = lv.n + 1, h = (m - 1) / 2, ms = m + 1;
-    const int NC = c->num_sms / 2;
+    const int NC = c->num_sms / 2 - 1;  // one cluster for the reducer
     const int R = (m + 2 * NC - 1) / (2 * NC);
     const int G = 2 * ((m + 2 * R - 1) / (2 * R));
     const size_t smem = rs2_smem_doubles(m, R) * sizeof(double);
@@ -572,7 +574,7 @@ bool launch_pdhg_rs2_q(w1mg_ctx* c, const PLevel& lv) {
         attr |= 1ull << (dev & 63);
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(G);
+    cfg.gridDim = dim3(G + 2);  // + the reducer cluster
     cfg.blockDim = dim3(kRsThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c->stream;
@@ -587,7 +589,7 @@ bool launch_pdhg_rs2_q(w1mg_ctx* c, const PLevel& lv) {
     cfg.numAttrs = 2;
     int nclusters = 0;
     if (cudaOccupancyMaxActiveClusters(&nclusters, pdhg_rs2_kernel<Q>, &cfg) != cudaSuccess ||
-        2 * nclusters < G) {
+        2 * nclusters < G + 2) {
         cudaGetLastError();
         return false;
     }
@@ -607,6 +609,8 @@ bool launch_pdhg_rs2_q(w1mg_ctx* c, const PLevel& lv) {
     ra.psb = nullptr;
     ra.flag = nullptr;
     ra.part = c->get<double>("rs.part", (size_t)3 * G);
+    ra.dec = c->get<int>("rs.dec", 2);
+    CK(cudaMemsetAsync(ra.dec, 0, 2 * sizeof(int), c->stream));
     unsigned* bar = c->get<unsigned>("persist.bar", 2);
     int* err = c->get<int>("persist.err", 1);
     CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), c->stream));
@@ -633,9 +637,9 @@ bool launch_pdhg_rs2_q(w1mg_ctx* c, const PLevel& lv) {
 template <int Q, class P>
 bool launch_pdhg_rspf_q(w1mg_ctx* c, const PLevel& lv) {
     const int m = P::M;
-    const int R = (m + c->num_sms - 1) / c->num_sms, G = (m + R - 1) / R;
+    const int R = (m + c->num_sms - 2) / (c->num_sms - 1), G = (m + R - 1) / R;  // one SM for the reducer
     const size_t smem = rspf_smem_doubles<P>(R) * sizeof(double);
-    if (smem > kDctSmemMax || G > c->num_sms || R * m > 5 * kRsThreads) return false;
+    if (smem > kDctSmemMax || G + 1 > c->num_sms) return false;
     static unsigned long long attr = 0;  // per device
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -666,6 +670,8 @@ bool launch_pdhg_rspf_q(w1mg_ctx* c, const PLevel& lv) {
     ra.lamq = tb.lamq;
     ra.scale = 1.0 / (4.0 * double(m) * double(m));  // poisson.cpp:93
     ra.part = c->get<double>("rs.part", (size_t)3 * G);
+    ra.dec = c->get<int>("rs.dec", 2);
+    CK(cudaMemsetAsync(ra.dec, 0, 2 * sizeof(int), c->stream));
     unsigned* bar = c->get<unsigned>("persist.bar", 2);
     int* err = c->get<int>("persist.err", 1);
     CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), c->stream));
@@ -678,7 +684,7 @@ bool launch_pdhg_rspf_q(w1mg_ctx* c, const PLevel& lv) {
     SweepArgs a = lv.args;
     const short* ctab = dtab;
     void* args[] = {(void*)&a, (void*)&ra, (void*)&ctab, (void*)&gb};
-    CK(cudaLaunchCooperativeKernel((const void*)pdhg_rspf_kernel<Q, P>, dim3(G), dim3(kRsThreads), args,
+    CK(cudaLaunchCooperativeKernel((const void*)pdhg_rspf_kernel<Q, P>, dim3(G + 1), dim3(kRsThreads), args,
                                    smem, c->stream));
     ++c->launches;
     int herr = 0;
@@ -692,7 +698,7 @@ bool launch_pdhg_rspf_q(w1mg_ctx* c, const PLevel& lv) {
 template <int Q>
 bool launch_pdhg_rs_q(w1mg_ctx* c, const PLevel& lv) {
     const int m = lv.n + 1, h = (m - 1) / 2;
-    int R = (m + c->num_sms - 1) / c->num_sms;
+    int R = (m + c->num_sms - 2) / (c->num_sms - 1);  // one SM for the reducer CTA
     if ((m & 1) && h <= 64 && g_pdhg_rs != 2) {
         if (h <= 16) return launch_pdhg_rs_qt<Q, 1>(c, lv, R);
         if (h <= 32) return launch_pdhg_rs_qt<Q, 2>(c, lv, R);

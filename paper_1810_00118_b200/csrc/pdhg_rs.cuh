@@ -51,7 +51,7 @@ constexpr int kRsThreads = 512;
 constexpr int kRsStampSlots = 24;  // diagnostics: time stamps per iteration (CTA 0)
 
 struct RsArgs {
-    int m, h, R, G;       // m = 2h+1 nodes per side, R rows (columns) per CTA, G CTAs
+    int m, h, R, G;       // m = 2h+1 nodes per side, R rows (columns) per CTA, G worker CTAs
     int HP;               // padded half size (16 TS)
     int posDC;            // spectral position of the constant mode
     int halo_x;           // 1: psi halo row from the neighbour CTA (prime-factor mode)
@@ -62,6 +62,7 @@ struct RsArgs {
     double* psb;          // [G][ms] psi of each CTA's first row
     unsigned* flag;       // [2][G] iteration stamps of vyb / psb
     double* part;         // [G][3] Eq. 12 partial sums
+    int* dec;             // [2] stop decision of the reducer CTA, by iteration parity
     unsigned long long* stamps;
 };
 
@@ -206,6 +207,92 @@ __device__ __forceinline__ void rs_dct3(const double (&c)[TS][TS], int V, int m,
     }
 }
 
+// The REDUCER CTA(s) (blockIdx.x >= ra.G; `active`: the one that works): the
+// Eq. 12 reduction and the stop rule (finalize_pair<true>'s) of iteration k
+// run here between the two grid barriers of iteration k+1 -- off the
+// workers' critical path, on an SM the level leaves idle.  It sums the
+// workers' partials in a fixed order, records the history and (on a stop) the
+// control block, and publishes the decision in dec[iteration parity]; the
+// workers read it after the second barrier.  The phases a worker runs before
+// it learns of a stop only write scratch planes.
+struct RsRed {  // by value: a reference would move the kernel's parameter block to local memory
+    PairCtl* ctl;
+    double h2, mu, tau;
+    double* hist;
+    long hist_cap;
+    int* ndone;
+    const double* part;
+    int* dec;
+    int G;
+};
+__device__ __forceinline__ RsRed rs_red_args(const SweepArgs& a, const RsArgs& ra) {
+    return RsRed{a.ctl, a.h2, a.mu, a.tau, a.hist, a.hist_cap, a.ndone, ra.part, ra.dec, ra.G};
+}
+__device__ __noinline__ void rs_reducer(const RsRed a, const GridBar gb, bool active) {
+    const RsRed& ra = a;
+    __shared__ int r_ok;
+    __shared__ int r_stop;
+    __shared__ double r_red[kRsThreads / 32][3];
+    PairCtl* ctl = a.ctl;
+    long k = ctl->it;
+    const long max_it = ctl->max_it;
+    const double tol = ctl->tol;
+    const int tid = threadIdx.x, W = ra.G;
+    unsigned gen = 0;
+    if (tid == 0) r_stop = 0;
+    for (long iter = 0;; ++iter) {
+        if (!grid_barrier(gb, gen, &r_ok)) return;
+        if (iter > 0 && active) {
+            double pt0 = 0.0, pt1 = 0.0, pt2 = 0.0;
+            if (tid < W) {
+                pt0 = __ldcg(ra.part + 3 * tid + 0);
+                pt1 = __ldcg(ra.part + 3 * tid + 1);
+                pt2 = __ldcg(ra.part + 3 * tid + 2);
+            }
+            pt0 = warp_sum(pt0);
+            pt1 = warp_sum(pt1);
+            pt2 = warp_sum(pt2);
+            if ((tid & 31) == 0) {
+                r_red[tid >> 5][0] = pt0;
+                r_red[tid >> 5][1] = pt1;
+                r_red[tid >> 5][2] = pt2;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+                for (int w = 0; w < (W + 31) / 32; ++w) {
+                    t0 += r_red[w][0];
+                    t1 += r_red[w][1];
+                    t2 += r_red[w][2];
+                }
+                const double fpr = a.h2 * (t0 / a.mu + t1 / a.tau + 2.0 * t2);  // Eq. 12
+                const bool finite = isfinite(fpr);
+                const bool stop = fpr < tol || k + 1 >= max_it || !finite;
+                r_stop = stop ? 1 : 0;
+                ra.dec[iter & 1] = stop ? 1 : 0;
+                if (a.hist && k < a.hist_cap) a.hist[k] = fpr;
+                if (stop) {
+                    ctl->it = k + 1;
+                    ctl->fpr = fpr;
+                    ctl->cur = 0;
+                    if (!finite) ctl->nonfinite = 1;
+                    ctl->done = 1;
+                    if (a.ndone) atomicAdd(a.ndone, 1);
+                    __threadfence();
+                }
+            }
+            ++k;
+        }
+        if (!grid_barrier(gb, gen, &r_ok)) return;  // (its __syncthreads orders r_stop)
+        if (iter > 0) {
+            // every reducer CTA leaves with the workers: the idle one reads the decision too
+            if (!active && tid == 0) r_stop = __ldcg(ra.dec + (iter & 1));
+            __syncthreads();
+            if (r_stop) return;
+        }
+    }
+}
+
 // Dynamic shared memory (doubles): lam[ms] | state 7 x (R+1) x ms (row 0: the
 // shadow row) | vyl[ms] | X (R+2) x ms | dense: Y (R+2) x ms, P (R+2) x ps |
 // prime-factor: tables, P, Q arenas of dct_arena(g, R)
@@ -241,11 +328,12 @@ pdhg_rs_kernel(const SweepArgs a, const DctPlan g, const RsArgs ra, GridBar gb) 
     __shared__ double red[kRsThreads / 32][3];
     PairCtl* ctl = a.ctl;
     if (*(volatile int*)&ctl->done) return;
-    long k = ctl->it;
-    const long max_it = ctl->max_it;
-    const double tol = ctl->tol;
+    if ((int)blockIdx.x >= ra.G) {  // reducer CTA(s): Eq. 12 sums and the stop rule
+        rs_reducer(rs_red_args(a, ra), gb, (int)blockIdx.x == ra.G);
+        return;
+    }
     constexpr bool kDense = TS > 0;
-    const int m = ra.m, n = m - 1, h = ra.h, R = ra.R, G = (int)gridDim.x, HP = ra.HP;
+    const int m = ra.m, n = m - 1, h = ra.h, R = ra.R, G = ra.G, HP = ra.HP;
     const int ms = m + 1, tid = threadIdx.x, c = blockIdx.x;
     const int j0 = c * R, nr = min(R, m - j0);  // owned rows [j0, j0 + nr)
     const int sh = (kDense && c > 0) ? 1 : 0;   // shadow row j0-1 kept
@@ -386,13 +474,6 @@ pdhg_rs_kernel(const SweepArgs a, const DctPlan g, const RsArgs ra, GridBar gb) 
         stamp(1);
         if (!grid_barrier(gb, gen, &s_ok)) return;
         stamp(2);
-        // Eq. 12 partials of the previous iteration: visible after this barrier
-        double pt0 = 0.0, pt1 = 0.0, pt2 = 0.0;
-        if (iter > 0 && tid < G) {
-            pt0 = __ldcg(ra.part + 3 * tid + 0);
-            pt1 = __ldcg(ra.part + 3 * tid + 1);
-            pt2 = __ldcg(ra.part + 3 * tid + 2);
-        }
         // ---- B: columns pos1 in [j0, j0+nr): DCT-II along j, divide by
         // lambda_k1 + lambda_k2 (poisson.cpp:84-89), DCT-III along j -> T2
         for (int e = tid; e < nr * m; e += kRsThreads) {
@@ -426,62 +507,26 @@ pdhg_rs_kernel(const SweepArgs a, const DctPlan g, const RsArgs ra, GridBar gb) 
                 T2[L.at(j0 + v, j)] = X[v * ms + j];
             }
         }
-        // ---- stop rule of the previous iteration (identical in every CTA;
-        // CTA 0 records the history, and the control block when it stops)
-        if (iter > 0) {
-            pt0 = warp_sum(pt0);
-            pt1 = warp_sum(pt1);
-            pt2 = warp_sum(pt2);
-            if ((tid & 31) == 0) {
-                red[tid >> 5][0] = pt0;
-                red[tid >> 5][1] = pt1;
-                red[tid >> 5][2] = pt2;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-                for (int w = 0; w < (G + 31) / 32; ++w) {
-                    t0 += red[w][0];
-                    t1 += red[w][1];
-                    t2 += red[w][2];
-                }
-                const double fpr = a.h2 * (t0 / a.mu + t1 / a.tau + 2.0 * t2);  // Eq. 12
-                const bool finite = isfinite(fpr);
-                const bool stop = fpr < tol || k + 1 >= max_it || !finite;
-                s_stop = stop ? 1 : 0;
-                if (c == 0) {
-                    if (a.hist && k < a.hist_cap) a.hist[k] = fpr;
-                    if (stop) {
-                        ctl->it = k + 1;
-                        ctl->fpr = fpr;
-                        ctl->cur = 0;
-                        if (!finite) ctl->nonfinite = 1;
-                        ctl->done = 1;
-                        if (a.ndone) atomicAdd(a.ndone, 1);
-                        __threadfence();
-                    }
-                }
-            }
-            __syncthreads();
-            ++k;
-            if (s_stop) {
-                flush_state();
-                return;
-            }
-        }
         stamp(3);
         if (!grid_barrier(gb, gen, &s_ok)) return;
         stamp(4);
         // ---- C: rows j0-sh .. j0+nr-1+hl of T2 (dense) / the owned rows
         // (prime-factor), DCT-III along i, psi = y / (4 m^2) (poisson.cpp:93);
         // afterwards X row w holds psi of row j0 - sh + w
+        int decv = 0;  // the reducer's decision: requested now, consumed after the row loads
+        if (iter > 0 && tid == 0) decv = __ldcg(ra.dec + (iter & 1));
         const int nh = kDense ? sh + nr + hl : nr;
         for (int e = tid; e < nh * m; e += kRsThreads) {
             int w, pos;
             rs_split(e, m, w, pos);
             Y[w * ms + pos] = __ldcg(T2 + L.at(pos, j0 - sh + w));
         }
+        if (tid == 0) s_stop = decv;
         __syncthreads();
+        if (iter > 0 && s_stop) {  // iteration iter-1 met the stop rule: its state is final
+                flush_state();
+            return;
+        }
         if constexpr (kDense) {
             rs_dct3<TS>(cf, nh, m, h, HP, Y, ms, P, ps,
                         [&](int w, int i, double val) { X[w * ms + i] = scale * val; });

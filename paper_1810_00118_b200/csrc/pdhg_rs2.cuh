@@ -69,10 +69,11 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
     cg::cluster_group cluster = cg::this_cluster();
     PairCtl* ctl = a.ctl;
     if (*(volatile int*)&ctl->done) return;  // uniform over the grid
-    long k = ctl->it;
-    const long max_it = ctl->max_it;
-    const double tol = ctl->tol;
-    const int m = ra.m, n = m - 1, h = ra.h, R = ra.R, G = (int)gridDim.x;
+    if ((int)blockIdx.x >= ra.G) {  // reducer cluster: Eq. 12 sums and the stop rule
+        rs_reducer(rs_red_args(a, ra), gb, (int)blockIdx.x == ra.G);
+        return;
+    }
+    const int m = ra.m, n = m - 1, h = ra.h, R = ra.R, G = ra.G;
     const int ms = m + 1, tid = threadIdx.x, lane = tid & 31, wq = tid >> 5;
     constexpr int hs = kRs2HS;
     const int c = blockIdx.x, e = (int)cluster.block_rank(), base = (c >> 1) * 2 * R;
@@ -259,12 +260,6 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
         stamp(11);
         if (!grid_barrier(gb, gen, &s_ok)) return;
         stamp(12);
-        double pt0 = 0.0, pt1 = 0.0, pt2 = 0.0;  // Eq. 12 partials of the previous iteration
-        if (iter > 0 && tid < G) {
-            pt0 = __ldcg(ra.part + 3 * tid + 0);
-            pt1 = __ldcg(ra.part + 3 * tid + 1);
-            pt2 = __ldcg(ra.part + 3 * tid + 2);
-        }
         // ---- B: columns pos1 = base + w: DCT-II along j, divide by lambda_k1 +
         // lambda_k2 (poisson.cpp:84-89), DCT-III along j -> T2
         // every CTA reads all the cluster's columns and folds them into its own
@@ -299,59 +294,14 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
         for (int v = 0; v < nr; ++v)
             combine(v, [&](int j, double val) { T2[L.at(j0 + v, j)] = val; });
         stamp(9);
-        // ---- stop rule of the previous iteration (identical in every CTA)
-        if (iter > 0) {
-            pt0 = warp_sum(pt0);
-            pt1 = warp_sum(pt1);
-            pt2 = warp_sum(pt2);
-            if (lane == 0) {
-                red[wq][0] = pt0;
-                red[wq][1] = pt1;
-                red[wq][2] = pt2;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-                for (int w = 0; w < (G + 31) / 32; ++w) {
-                    t0 += red[w][0];
-                    t1 += red[w][1];
-                    t2 += red[w][2];
-                }
-                const double fpr = a.h2 * (t0 / a.mu + t1 / a.tau + 2.0 * t2);  // Eq. 12
-                const bool finite = isfinite(fpr);
-                const bool stop = fpr < tol || k + 1 >= max_it || !finite;
-                s_stop = stop ? 1 : 0;
-                if (c == 0) {
-                    if (a.hist && k < a.hist_cap) a.hist[k] = fpr;
-                    if (stop) {
-                        ctl->it = k + 1;
-                        ctl->fpr = fpr;
-                        ctl->cur = 0;
-                        if (!finite) ctl->nonfinite = 1;
-                        ctl->done = 1;
-                        if (a.ndone) atomicAdd(a.ndone, 1);
-                        __threadfence();
-                    }
-                }
-            }
-            __syncthreads();
-            ++k;
-            if (s_stop) {
-                const int gs[6] = {P_MX, P_MY, P_PX, P_PY, P_BX, P_BY};
-                for (int x = tid; x < 6 * nr * m; x += kRsThreads) {
-                    const int sl = x / (nr * m), rem = x - sl * nr * m, v = rem / m, i = rem - v * m;
-                    pslot_w(a, 0, gs[sl])[L.at(i, j0 + v)] = S(sl, v + 1)[i];
-                }
-                cluster.sync();  // no CTA leaves while its partner may still store into it
-                return;
-            }
-        }
         stamp(11);
         if (!grid_barrier(gb, gen, &s_ok)) return;
         stamp(12);
         // ---- C: rows jlo .. jhi of T2 (the cluster's rows, the shadow row
         // below and the halo row above): DCT-III along i; afterwards X row x
         // holds psi = y / (4 m^2) (poisson.cpp:93) of row j0 - sh + x
+        int decv = 0;  // the reducer's decision: requested now, consumed after the row loads
+        if (iter > 0 && tid == 0) decv = __ldcg(ra.dec + (iter & 1));
         {
             const int per = e ? h : h + 1;
             for (int x = tid; x < VCc * per; x += kRsThreads) {
@@ -361,7 +311,17 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
                 F[w * hs + q] = __ldcg(T2 + L.at(pos, jlo + w));
             }
         }
+        if (tid == 0) s_stop = decv;
         __syncthreads();
+        if (iter > 0 && s_stop) {  // iteration iter-1 met the stop rule: its state is final
+                const int gs[6] = {P_MX, P_MY, P_PX, P_PY, P_BX, P_BY};
+                for (int x = tid; x < 6 * nr * m; x += kRsThreads) {
+                    const int sl = x / (nr * m), rem = x - sl * nr * m, v = rem / m, i = rem - v * m;
+                    pslot_w(a, 0, gs[sl])[L.at(i, j0 + v)] = S(sl, v + 1)[i];
+                }
+                cluster.sync();  // no CTA leaves while its partner may still store into it
+            return;
+        }
         stamp(13);
         dct3_half(VCc, F, [&](int w, int i, double val) {
             const int jj = jlo + w;
