@@ -18,9 +18,11 @@
 //     barrier).
 //   * Two grid barriers per iteration (after the row DCT-II and after the
 //     column phase) instead of four.  The Eq. 12 reduction and the stop rule
-//     of iteration k run after the first barrier of iteration k+1 (whose
-//     phases before the decision only write scratch planes), so they cost no
-//     barrier of their own.
+//     of iteration k run on a REDUCER CTA (one more CTA, on an SM the level
+//     leaves idle) between the two barriers of iteration k+1; the workers
+//     read its decision together with their row loads after the second
+//     barrier.  What a worker runs before it learns of a stop only writes
+//     scratch planes, so the reduction costs the workers nothing.
 //   * Both transposes are done by the STORES (scattered, fire-and-forget);
 //     every load of a phase is a contiguous row.
 //   * The length-m DCT-II / DCT-III of a vector is a dense product with the
