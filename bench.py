@@ -439,6 +439,7 @@ def config3_time_to_w1(reps=3):
             "device_s": min(dev), "e2e_s": min(wall), "W1": r.distance,
             "iters": [l.iters for l in r.levels],
             "level_s": [l.seconds for l in r.levels],
+            "us_per_iter": [1e6 * l.seconds / max(l.iters, 1) for l in r.levels],
             "us_per_iter_finest": 1e6 * r.levels[-1].seconds / max(r.levels[-1].iters, 1)}
 
 
