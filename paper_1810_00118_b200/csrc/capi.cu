@@ -74,6 +74,10 @@ int w1mg_ctx_create(int device, w1mg_ctx** out) {
         if (const char* v = std::getenv("W1MG_OCC3")) g_occ3 = std::atoi(v) == 4 ? 4 : 5;
         if (const char* v = std::getenv("W1MG_PDHG_PERSIST")) g_pdhg_persist = std::atoi(v) != 0;
         if (const char* v = std::getenv("W1MG_PDHG_RS")) g_pdhg_rs = std::atoi(v);
+        // Nsight Compute cannot replay the cooperative cluster launch of
+        // pdhg_rs2_kernel (LaunchFailed, then a sticky error): under the
+        // profiler the 257^2-class levels take the one-CTA-per-SM path
+        else if (std::getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") && g_pdhg_rs == 1) g_pdhg_rs = 4;
         if (const char* v = std::getenv("W1MG_SLAB_MIN_N")) g_slab_min_n = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_COMPACT_STEP")) g_compact_step = std::max(1, std::atoi(v));
         if (const char* v = std::getenv("W1MG_TMAP_NW")) {
