@@ -586,7 +586,9 @@ bool launch_pdhg_rs2_q(w1mg_ctx* c, const PLevel& lv) {
     at[1].id = cudaLaunchAttributeCooperative;
     at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    // W1MG_RS2_NOCOOP (profiling only): plain cluster launch -- ncu cannot replay
+    // the cooperative one; the CTAs of one wave are co-resident on an idle GPU
+    cfg.numAttrs = std::getenv("W1MG_RS2_NOCOOP") ? 1 : 2;
     int nclusters = 0;
     if (cudaOccupancyMaxActiveClusters(&nclusters, pdhg_rs2_kernel<Q>, &cfg) != cudaSuccess ||
         2 * nclusters < G + 2) {

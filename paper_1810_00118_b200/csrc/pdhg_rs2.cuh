@@ -28,8 +28,11 @@
 //   DCT-III  warp wq owns the outputs i = 8 wq .. 8 wq + 7; the A fragments of
 //            the transposed matrix c(4 qt + lane % 4, i) are staged once per
 //            level in shared memory in fragment order (conflict-free loads).
-// The rank-one terms (constant mode, middle sample) are one more row of ones /
-// alternating signs on warp 0.
+// The rank-one terms (constant mode: sum_i s_i; middle sample: sum_k X_k cos(pi
+// k / 2)) are summed by whoever PRODUCES the vector (the fold, the row / column
+// loads, the accumulators of the preceding DCT-II), one warp per vector, so
+// nothing follows the MMAs on the critical path (as a 17th MMA row tile on
+// warp 0 they cost ~0.8 us per iteration).
 //
 // The iteration structure, the shadow row, the deferred stop rule and the
 // plane/position conventions are those of pdhg_rs.cuh (reference semantics:
@@ -56,7 +59,7 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 __host__ __device__ inline size_t rs2_smem_doubles(int m, int R) {
     const int ms = m + 1;
     return (size_t)ms * (1 + 7 * (R + 1) + (R + 2)) + (size_t)kRs2HS * (2 * kRs2NV + 2 * (R + 2)) +
-           (size_t)16 * 32 * 32 + 8;
+           (size_t)16 * 32 * 32 + 16 * kRs2NV + 8;
 }
 
 template <int QN>
@@ -93,6 +96,7 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
     double* FY = F + (size_t)kRs2NV * hs;        // [8][hs] divided spectrum of this half
     double* EO = FY + (size_t)kRs2NV * hs;       // [R+2][2][hs] E / O of the vectors this CTA owns
     double* A3 = EO + (size_t)(R + 2) * 2 * hs;  // [16][32][32] DCT-III A fragments
+    double* altp = A3 + 16 * 32 * 32;            // [16][8] per-warp partial sums of the middle sample
     double* Fr[2] = {cluster.map_shared_rank(F, 0), cluster.map_shared_rank(F, 1)};
     double* EOr[2] = {cluster.map_shared_rank(EO, 0), cluster.map_shared_rank(EO, 1)};
     auto S = [&](int slot, int sv) { return st + ((size_t)slot * (R + 1) + sv) * ms; };
@@ -147,9 +151,23 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
                 Fr[0][w * hs + h] = xv[h];
             }
         }
+        // the constant mode needs sum_i s_i: one warp per owned vector sums it
+        // here (both ranks, off the path behind the cluster barrier)
+        if (wq >= 16 - nr) {
+            const int v = 15 - wq;
+            const double* xv = X + v * ms;
+            double ss = 0.0;
+            for (int i = lane; i < h; i += 32) ss += xv[i] + xv[m - 1 - i];
+            ss = warp_sum(ss);
+            if (lane == 0) Fr[0][(e * R + v) * hs + h + 1] = ss;
+        }
     };
-    // this half of the DCT-II of the cluster's vectors F[w], w < V <= 8: out(w, pos, X_k)
-    auto dct2_half = [&](int V, auto out) {
+    // this half of the DCT-II of the cluster's vectors F[w], w < V <= 8: out(w, pos,
+    // X_k) stores and returns the finished value.  F[w][h+1] holds sum_i s_i (rank
+    // 0).  alt: rank 0 also leaves, per warp and vector, the partial sum of
+    // y cos(pi k / 2) over its eight rows in altp[wq][w] (the middle sample of
+    // the DCT-III that follows).
+    auto dct2_half = [&](int V, bool alt, auto out) {
         const double* fb = F + fr * hs + fc;  // B[k = fc][n = fr] = F[vector fr][4 it + fc]
         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
@@ -158,38 +176,38 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             if ((it & 7) == 7) asm volatile("" ::: "memory");  // loads in batches of 8 (registers)
         }
         const int q = 8 * wq + fr;
+        double y[2] = {0.0, 0.0};
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
             const int w = 2 * fc + cc;
             const double sum = cc ? d1 : d0;
             if (w < V && q < h) {
                 if (e) {
-                    out(w, h + q, 2.0 * sum);
+                    y[cc] = out(w, h + q, 2.0 * sum);
                 } else {
                     const double xh = F[w * hs + h];
-                    out(w, q, 2.0 * (sum + ((q & 1) ? xh : -xh)));  // cos(pi k / 2), k = 2q+2
+                    y[cc] = out(w, q, 2.0 * (sum + ((q & 1) ? xh : -xh)));  // cos(pi k / 2), k = 2q+2
                 }
             }
         }
-        if (e == 0 && wq == 0) {  // constant mode: a row of ones
-            double ca[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};  // independent chains
-#pragma unroll 8
-            for (int it = 0; it < 32; ++it)
-                dmma884(ca[it & 3][0], ca[it & 3][1], (4 * it + fc < h) ? 1.0 : 0.0, fb[4 * it]);
-            const double c0 = (ca[0][0] + ca[1][0]) + (ca[2][0] + ca[3][0]);
-            const double c1 = (ca[0][1] + ca[1][1]) + (ca[2][1] + ca[3][1]);
-            if (fr == 0) {
+        if (e == 0) {
+            if (alt) {  // sum over the warp's rows (lanes with the same fc) of +-y
 #pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {
-                    const int w = 2 * fc + cc;
-                    if (w < V) out(w, 2 * h, 2.0 * ((cc ? c1 : c0) + F[w * hs + h]));
+                    double t = (q & 1) ? y[cc] : -y[cc];
+                    t += __shfl_xor_sync(0xffffffffu, t, 4);
+                    t += __shfl_xor_sync(0xffffffffu, t, 8);
+                    t += __shfl_xor_sync(0xffffffffu, t, 16);
+                    if (fr == 0) altp[wq * kRs2NV + 2 * fc + cc] = t;
                 }
             }
+            if (wq == 0 && lane < V)  // constant mode: 2 (sum_i s_i + x_h)
+                out(lane, 2 * h, 2.0 * (F[lane * hs + h + 1] + F[lane * hs + h]));
         }
     };
     // this half of the DCT-III of the spectra src[w] (own-half positions, the
     // constant mode at [h] on rank 0): E (rank 0) or O (rank 1) -> send(w, i, val),
-    // i <= h (i = h: the middle sample, rank 0 only)
+    // i < h (the middle sample i = h is sent by the producers of the spectra)
     auto dct3_half = [&](int V, const double* src, auto send) {
         const double* yb = src + fr * hs + fc;  // B[k = fc][n = fr] = src[vector fr][4 qt + fc]
         const double* a3 = A3 + (wq * 32) * 32 + lane;
@@ -202,23 +220,6 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             const int w = 2 * fc + cc;
             const double sum = cc ? d1 : d0;
             if (w < V && i < h) send(w, i, e ? 2.0 * sum : src[w * hs + h] + 2.0 * sum);
-        }
-        if (e == 0 && wq == 0) {  // middle sample: sum of X_k cos(pi k / 2), k = 2q+2
-            double ca[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll 8
-            for (int qt = 0; qt < 32; ++qt) {
-                const int q = 4 * qt + fc;
-                dmma884(ca[qt & 3][0], ca[qt & 3][1], (q < h) ? ((q & 1) ? 1.0 : -1.0) : 0.0, yb[4 * qt]);
-            }
-            const double c0 = (ca[0][0] + ca[1][0]) + (ca[2][0] + ca[3][0]);
-            const double c1 = (ca[0][1] + ca[1][1]) + (ca[2][1] + ca[3][1]);
-            if (fr == 0) {
-#pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
-                    const int w = 2 * fc + cc;
-                    if (w < V) send(w, h, src[w * hs + h] + 2.0 * (cc ? c1 : c0));
-                }
-            }
         }
     };
     // y of the owned vector x from its E / O rows: out(i, y_i)
@@ -256,7 +257,10 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
         fold_send();
         cluster.sync();
         stamp(2);
-        dct2_half(VC, [&](int w, int pos, double val) { T1[L.at(base + w, pos)] = val; });
+        dct2_half(VC, false, [&](int w, int pos, double val) {
+            T1[L.at(base + w, pos)] = val;
+            return val;
+        });
         stamp(11);
         if (!grid_barrier(gb, gen, &s_ok)) return;
         stamp(12);
@@ -264,31 +268,44 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
         // lambda_k2 (poisson.cpp:84-89), DCT-III along j -> T2
         // every CTA reads all the cluster's columns and folds them into its own
         // half (s on rank 0, d on rank 1): no exchange, no cluster barrier here
-        for (int x = tid; x < VC * (h + 1); x += kRsThreads) {
-            int w, i;
-            rs_split(x, h + 1, w, i);
+        if (wq < VC) {  // warp wq takes column base + wq (all its loads in flight together)
+            const int w = wq;
             const double* col = T1 + L.at(0, base + w);
-            if (i < h) {
+            double ss = 0.0;
+            for (int i = lane; i < h; i += 32) {
                 const double p = __ldcg(col + i), q = __ldcg(col + m - 1 - i);
                 F[w * hs + i] = e ? p - q : p + q;
-            } else if (e == 0) {
-                F[w * hs + h] = __ldcg(col + h);
+                ss += p + q;
+            }
+            if (e == 0) {
+                ss = warp_sum(ss);
+                if (lane == 0) {
+                    F[w * hs + h] = __ldcg(col + h);
+                    F[w * hs + h + 1] = ss;
+                }
             }
         }
         __syncthreads();
         stamp(5);
         stamp(6);
-        dct2_half(VC, [&](int w, int pos, double val) {
+        dct2_half(VC, true, [&](int w, int pos, double val) {
             const int p1 = base + w;
             const double y = (p1 == 2 * h && pos == 2 * h) ? 0.0 : val / (lam[p1] + lam[pos]);
             FY[w * hs + (pos == 2 * h ? h : (e ? pos - h : pos))] = y;
+            return y;
         });
         __syncthreads();
         stamp(7);
-        dct3_half(VC, FY, [&](int w, int i, double val) {
+        auto send_b = [&](int w, int i, double val) {
             const int o = w / R;  // owner rank of column base + w
             EOr[o][((size_t)(2 * (w - o * R)) + e) * hs + i] = val;
-        });
+        };
+        if (e == 0 && tid < VC) {  // middle sample: constant mode + 2 sum_k y_k cos(pi k / 2)
+            double t = 0.0;
+            for (int w2 = 0; w2 < 16; ++w2) t += altp[w2 * kRs2NV + tid];
+            send_b(tid, h, FY[tid * hs + h] + 2.0 * t);
+        }
+        dct3_half(VC, FY, send_b);
         cluster.sync();
         stamp(8);
         for (int v = 0; v < nr; ++v)
@@ -302,13 +319,33 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
         // holds psi = y / (4 m^2) (poisson.cpp:93) of row j0 - sh + x
         int decv = 0;  // the reducer's decision: requested now, consumed after the row loads
         if (iter > 0 && tid == 0) decv = __ldcg(ra.dec + (iter & 1));
-        {
-            const int per = e ? h : h + 1;
-            for (int x = tid; x < VCc * per; x += kRsThreads) {
-                int w, q;
-                rs_split(x, per, w, q);
-                const int pos = (q == h) ? 2 * h : (e ? h + q : q);
-                F[w * hs + q] = __ldcg(T2 + L.at(pos, jlo + w));
+        auto send_c = [&](int w, int i, double val) {
+            const int jj = jlo + w;
+#pragma unroll
+            for (int o = 0; o < 2; ++o) {
+                const int j0o = base + o * R, nro = max(0, min(R, m - j0o));
+                const int sho = (nro > 0 && j0o > 0) ? 1 : 0, hlo = (nro > 0 && j0o + nro < m) ? 1 : 0;
+                const int xo = jj - (j0o - sho);
+                if (nro > 0 && xo >= 0 && xo < sho + nro + hlo)
+                    EOr[o][((size_t)(2 * xo) + e) * hs + i] = val;
+            }
+        };
+        if (wq < VCc) {  // warp wq takes row jlo + wq: its half of the spectrum, and on
+            const int w = wq;  // rank 0 the middle sample (constant mode + alternating sum)
+            const double* row = T2 + L.at(e ? h : 0, jlo + w);
+            double as = 0.0;
+            for (int q = lane; q < h; q += 32) {
+                const double yq = __ldcg(row + q);
+                F[w * hs + q] = yq;
+                as += (q & 1) ? yq : -yq;
+            }
+            if (e == 0) {
+                as = warp_sum(as);
+                if (lane == 0) {
+                    const double dc = __ldcg(T2 + L.at(2 * h, jlo + w));
+                    F[w * hs + h] = dc;
+                    send_c(w, h, dc + 2.0 * as);
+                }
             }
         }
         if (tid == 0) s_stop = decv;
@@ -323,17 +360,7 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             return;
         }
         stamp(13);
-        dct3_half(VCc, F, [&](int w, int i, double val) {
-            const int jj = jlo + w;
-#pragma unroll
-            for (int o = 0; o < 2; ++o) {
-                const int j0o = base + o * R, nro = max(0, min(R, m - j0o));
-                const int sho = (nro > 0 && j0o > 0) ? 1 : 0, hlo = (nro > 0 && j0o + nro < m) ? 1 : 0;
-                const int xo = jj - (j0o - sho);
-                if (nro > 0 && xo >= 0 && xo < sho + nro + hlo)
-                    EOr[o][((size_t)(2 * xo) + e) * hs + i] = val;
-            }
-        });
+        dct3_half(VCc, F, send_c);
         cluster.sync();
         stamp(14);
         for (int x = 0; x < sh + nr + hl; ++x)
