@@ -271,6 +271,7 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
         if (wq < VC) {  // warp wq takes column base + wq (all its loads in flight together)
             const int w = wq;
             const double* col = T1 + L.at(0, base + w);
+            const double mid = __ldcg(col + h);  // requested with the other loads
             double ss = 0.0;
             for (int i = lane; i < h; i += 32) {
                 const double p = __ldcg(col + i), q = __ldcg(col + m - 1 - i);
@@ -280,7 +281,7 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             if (e == 0) {
                 ss = warp_sum(ss);
                 if (lane == 0) {
-                    F[w * hs + h] = __ldcg(col + h);
+                    F[w * hs + h] = mid;
                     F[w * hs + h + 1] = ss;
                 }
             }
@@ -333,6 +334,7 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
         if (wq < VCc) {  // warp wq takes row jlo + wq: its half of the spectrum, and on
             const int w = wq;  // rank 0 the middle sample (constant mode + alternating sum)
             const double* row = T2 + L.at(e ? h : 0, jlo + w);
+            const double dc = e ? 0.0 : __ldcg(T2 + L.at(2 * h, jlo + w));  // with the other loads
             double as = 0.0;
             for (int q = lane; q < h; q += 32) {
                 const double yq = __ldcg(row + q);
@@ -342,7 +344,6 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             if (e == 0) {
                 as = warp_sum(as);
                 if (lane == 0) {
-                    const double dc = __ldcg(T2 + L.at(2 * h, jlo + w));
                     F[w * hs + h] = dc;
                     send_c(w, h, dc + 2.0 * as);
                 }
