@@ -328,6 +328,15 @@ int w1mg_fp64_peak_probe(w1mg_ctx* ctx, long iters, double* tflops);
 int w1mg_rn_selftest(w1mg_ctx* ctx, long count, unsigned long long seed, double mu,
                      unsigned long long* bad);
 
+/* Diagnostics, host only (no GPU needed): checks the index tables of the
+ * register-stationary prime-factor DCT of the one-pair PDHG level m = n1 * n2
+ * (pdhg_rspf.cuh; instantiated for 27 x 19): the Makhoul + Good-Thomas input
+ * map and its inverse are bijections onto the column blocks, the CRT output
+ * map covers every k once, the W-build tables agree with it.  *bad = number of
+ * violated entries (0 expected); W1MG_EINVAL for a factor pair that is not
+ * instantiated. */
+int w1mg_pdhg_plan_check(int n1, int n2, long* bad);
+
 #ifdef __cplusplus
 }
 #endif

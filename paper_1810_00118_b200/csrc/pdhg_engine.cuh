@@ -1093,4 +1093,43 @@ int w1mg_ml_pdhg_run(w1mg_ctx* c, int n_finest, const double* rho_levels,
     });
 }
 
+int w1mg_pdhg_plan_check(int n1, int n2, long* bad) {
+    return guard([&] {
+        if (!bad) fail(W1MG_EINVAL, "w1mg_pdhg_plan_check: null output");
+        if (n1 != 27 || n2 != 19) fail(W1MG_EINVAL, "w1mg_pdhg_plan_check: factor pair not instantiated");
+        using P = w1mg_dev::PfGeo<27, 19>;
+        std::vector<short> t(P::NTAB);
+        w1mg_dev::rspf_tables<P>(t.data());
+        const int m = P::M;
+        const short* ginv = t.data();
+        const short* idxg = ginv + m;
+        const short* crtk = idxg + P::N2 * P::N1P;
+        const short* i0k = crtk + P::N1 * P::N2;
+        const short* i0d = i0k + P::NI0;
+        long b = 0;
+        std::vector<int> seen(P::N2 * P::N1P, 0), seenk(m, 0);
+        auto pos = [&](int n) { return n <= (m - 1) / 2 ? 2 * n : 2 * (m - 1 - n) + 1; };
+        for (int i = 0; i < m; ++i) {
+            const int g = ginv[i];
+            if (g < 0 || g >= P::N2 * P::N1P || g % P::N1P >= P::N1 || seen[g]++) ++b;
+            else if (idxg[g] != i) ++b;
+            else {  // x_i sits at v[(N2 n1 + N1 n2) mod m] after Makhoul's reordering
+                const int n1i = g % P::N1P, n2i = g / P::N1P;
+                if (pos((P::N2 * n1i + P::N1 * n2i) % m) != i) ++b;
+            }
+        }
+        for (int k1 = 0; k1 < P::N1; ++k1)
+            for (int k2 = 0; k2 < P::N2; ++k2) {
+                const int k = crtk[k1 * P::N2 + k2];
+                if (k < 0 || k >= m || k % P::N1 != k1 || k % P::N2 != k2 || seenk[k]++) ++b;
+            }
+        for (int k1 = 0; k1 < P::H1; ++k1)
+            for (int k2 = 0; k2 < P::N2; ++k2) {
+                const int it = k1 * P::N2 + k2;
+                if (i0k[it] != crtk[it] || i0d[it] != k1 * 2 * P::N2P + k2) ++b;
+            }
+        *bad = b;
+    });
+}
+
 }  // extern "C"

@@ -35,6 +35,20 @@ def test_library_nm_exports():
         assert s in exported, s
 
 
+def test_pdhg_prime_factor_plan_tables():
+    """Index tables of the register-stationary prime-factor DCT (513 = 27 x 19):
+    bijective input map (Makhoul + Good-Thomas), CRT output map, W-build tables."""
+    import ctypes as C
+
+    from paper_1810_00118_b200 import _lib
+
+    L = _lib.lib()
+    bad = C.c_long(-1)
+    assert L.w1mg_pdhg_plan_check(27, 19, C.byref(bad)) == 0
+    assert bad.value == 0
+    assert L.w1mg_pdhg_plan_check(13, 5, C.byref(bad)) != 0  # not instantiated
+
+
 def test_cpp_api_library_exports_reference_entry_points():
     so = os.path.join(ROOT, "paper_1810_00118_b200", "lib", "libw1mg.so")
     out = subprocess.run(["nm", "-DC", "--defined-only", so], capture_output=True, text=True).stdout
