@@ -651,7 +651,7 @@ bool launch_pdhg_rspf_q(w1mg_ctx* c, const PLevel& lv) {
         attr |= 1ull << (dev & 63);
     }
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdhg_rspf_kernel<Q, P>, kRsThreads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pdhg_rspf_kernel<Q, P>, kPfThreads, smem));
     if (occ < 1) return false;
     const std::string kt = "rspf.tab." + std::to_string(m);
     const bool ft = c->bufs.find(kt) == c->bufs.end();
@@ -686,7 +686,7 @@ bool launch_pdhg_rspf_q(w1mg_ctx* c, const PLevel& lv) {
     SweepArgs a = lv.args;
     const short* ctab = dtab;
     void* args[] = {(void*)&a, (void*)&ra, (void*)&ctab, (void*)&gb};
-    CK(cudaLaunchCooperativeKernel((const void*)pdhg_rspf_kernel<Q, P>, dim3(G + 1), dim3(kRsThreads), args,
+    CK(cudaLaunchCooperativeKernel((const void*)pdhg_rspf_kernel<Q, P>, dim3(G + 1), dim3(kPfThreads), args,
                                    smem, c->stream));
     ++c->launches;
     int herr = 0;

@@ -36,6 +36,11 @@
 
 namespace w1mg_dev {
 
+#ifndef W1MG_PF_THREADS
+#define W1MG_PF_THREADS 384  // 12 warps, <= 170 registers: measured 26.2 us per 513^2 iteration (512: 27.1, 448: 27.7, 256: 29.3)
+#endif
+constexpr int kPfThreads = W1MG_PF_THREADS;  // threads per CTA of the prime-factor engine
+
 template <int N1_, int N2_>
 struct PfGeo {
     static constexpr int N1 = N1_, N2 = N2_, M = N1 * N2;
@@ -88,12 +93,12 @@ inline void rspf_tables(short* t) {
 }
 
 template <int QN, class P>
-__global__ void __launch_bounds__(kRsThreads, 1)
+__global__ void __launch_bounds__(kPfThreads, 1)
 pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ gtab, GridBar gb) {
     extern __shared__ __align__(16) double rs_sm[];
     __shared__ int s_ok;
     __shared__ int s_stop;
-    __shared__ double red[kRsThreads / 32][3];
+    __shared__ double red[kPfThreads / 32][3];
     constexpr int N1 = P::N1, N2 = P::N2, H1 = P::H1, T1 = P::T1, H2 = P::H2, T2 = P::T2;
     constexpr int N1P = P::N1P, N2P = P::N2P, K1P = P::K1P, GS = P::GS, AS = P::AS, BS = P::BS;
     constexpr int m = P::M, n = m - 1, ms = m + 1;
@@ -149,17 +154,17 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
     }
 
     // ---- level prologue
-    for (int x = tid; x < m; x += kRsThreads) lam[x] = ra.lamq[x];
-    for (int x = tid; x <= m; x += kRsThreads) cq[x] = ra.cosq[x];
-    for (int x = tid; x < P::NTAB; x += kRsThreads) tab[x] = gtab[x];
-    for (int x = tid; x < 6 * (R + 1) * ms; x += kRsThreads) st[x] = 0.0;
-    for (int x = tid; x < (R + 2) * ms; x += kRsThreads) X[x] = 0.0;
-    for (int x = tid; x < (R + 2) * (P::GB + AS); x += kRsThreads) GBf[x] = 0.0;
+    for (int x = tid; x < m; x += kPfThreads) lam[x] = ra.lamq[x];
+    for (int x = tid; x <= m; x += kPfThreads) cq[x] = ra.cosq[x];
+    for (int x = tid; x < P::NTAB; x += kPfThreads) tab[x] = gtab[x];
+    for (int x = tid; x < 6 * (R + 1) * ms; x += kPfThreads) st[x] = 0.0;
+    for (int x = tid; x < (R + 2) * ms; x += kPfThreads) X[x] = 0.0;
+    for (int x = tid; x < (R + 2) * (P::GB + AS); x += kPfThreads) GBf[x] = 0.0;
     __syncthreads();
     {
         const int gs[6] = {P_MX, P_MY, P_PX, P_PY, P_BX, P_BY};
         const int rows = nr + sh;
-        for (int x = tid; x < 6 * rows * m; x += kRsThreads) {
+        for (int x = tid; x < 6 * rows * m; x += kPfThreads) {
             const int sl = x / (rows * m), rem = x - sl * rows * m, w = rem / m, i = rem - w * m;
             S(sl, w + 1 - sh)[i] = pslot(a, 0, gs[sl])[L.at(i, j0 - sh + w)];
         }
@@ -169,7 +174,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
     // ---- transform stages
     // N1 stage forward: column blocks GBf[v][n2][n1] -> A2[v][k1][re/im][n2]
     auto stage1_fwd = [&](int V) {
-        for (int col = warp; col < V * N2; col += kRsThreads / 32) {
+        for (int col = warp; col < V * N2; col += kPfThreads / 32) {
             int v, n2;
             rs_split(col, N2, v, n2);
             // the column as 16-byte pairs e[a] = (g[2a], g[2a+1]); t and N1 - t meet
@@ -195,7 +200,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
     // Cr, Ci, Sr, Si) with C = a_0 + sum (a_t + a_{N2-t}) cos, S = sum (a_t - a_{N2-t}) sin
     auto stage2 = [&](int V, auto emit) {
         const int ncol = V * H1;
-        for (int cb = warp * P::NU; cb < ncol; cb += (kRsThreads / 32) * P::NU) {
+        for (int cb = warp * P::NU; cb < ncol; cb += (kPfThreads / 32) * P::NU) {
             const int col = cb + u2;
             const bool on = u2 < P::NU && col < ncol;
             const int cc = on ? col : 0;
@@ -237,7 +242,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
     };
     // W build: natural-order spectra X[v][k] -> A2[v][k1][re/im][k2], k1 < H1
     auto build_w = [&](int V) {
-        for (int x = tid; x < V * P::NI0; x += kRsThreads) {
+        for (int x = tid; x < V * P::NI0; x += kPfThreads) {
             int v, it;
             rs_split(x, P::NI0, v, it);
             const int kk = i0k[it];
@@ -265,7 +270,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
     // inverse N1 stage: v[n1] = b_0 + 2 sum_k1 (Re b cos - Im b sin); the cos lane
     // a and the sin lane a + T1 swap their sums: out(v, i, y_i)
     auto stage1_inv = [&](int V, auto out) {
-        for (int col = warp; col < V * N2; col += kRsThreads / 32) {
+        for (int col = warp; col < V * N2; col += kPfThreads / 32) {
             int v, n2;
             rs_split(col, N2, v, n2);
             const double* br = GBf + v * P::GB + n2 * 2 * K1P;
@@ -311,7 +316,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
     for (;; ++iter) {
         stamp(0);
         // ---- A: r = A v - rho on the owned rows (poisson.cpp:113-115), DCT-II along i -> T1
-        for (int x = tid; x < nr * m; x += kRsThreads) {
+        for (int x = tid; x < nr * m; x += kPfThreads) {
             int v, i;
             rs_split(x, m, v, i);
             const int j = j0 + v, sv = v + 1;
@@ -336,7 +341,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
         stamp(12);
         // ---- B: columns k1 = j0 + v: DCT-II along j, divide by lambda_k1 +
         // lambda_k2 (poisson.cpp:84-89), DCT-III along j -> T2
-        for (int x = tid; x < nr * m; x += kRsThreads) {
+        for (int x = tid; x < nr * m; x += kPfThreads) {
             int v, j;
             rs_split(x, m, v, j);
             GBf[v * P::GB + ginv[j]] = __ldcg(T1p + L.at(j, j0 + v));
@@ -368,7 +373,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
         int decv = 0;  // the reducer's decision: requested now, consumed after the row loads
         if (iter > 0 && tid == 0) decv = __ldcg(ra.dec + (iter & 1));
         const int nh = sh + nr + hl;
-        for (int x = tid; x < nh * m; x += kRsThreads) {
+        for (int x = tid; x < nh * m; x += kPfThreads) {
             int w, kk;
             rs_split(x, m, w, kk);
             X[w * ms + kk] = __ldcg(T2p + L.at(kk, j0 - sh + w));
@@ -377,7 +382,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
         __syncthreads();
         if (iter > 0 && s_stop) {  // iteration iter-1 met the stop rule: its state is final
                 const int gs[6] = {P_MX, P_MY, P_PX, P_PY, P_BX, P_BY};
-                for (int x = tid; x < 6 * nr * m; x += kRsThreads) {
+                for (int x = tid; x < 6 * nr * m; x += kPfThreads) {
                     const int sl = x / (nr * m), rem = x - sl * nr * m, v = rem / m, i = rem - v * m;
                     pslot_w(a, 0, gs[sl])[L.at(i, j0 + v)] = S(sl, v + 1)[i];
                 }
@@ -396,7 +401,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
         // ---- D: post step (pdhg_post_kernel's arithmetic) on the shadow and
         // owned rows; Eq. 12 partial sums over the owned rows only
         double s_dm2 = 0.0, s_dp2 = 0.0, s_cr = 0.0;
-        for (int x = tid; x < (nr + sh) * m; x += kRsThreads) {
+        for (int x = tid; x < (nr + sh) * m; x += kPfThreads) {
             int w, i;
             rs_split(x, m, w, i);
             const int sv = w + 1 - sh, j = j0 + sv - 1;
@@ -455,7 +460,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
         __syncthreads();  // state rows and red[] complete
         if (tid == 0) {
             double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-            for (int w = 0; w < kRsThreads / 32; ++w) {
+            for (int w = 0; w < kPfThreads / 32; ++w) {
                 t0 += red[w][0];
                 t1 += red[w][1];
                 t2 += red[w][2];
