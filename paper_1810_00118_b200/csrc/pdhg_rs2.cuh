@@ -222,16 +222,19 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             if (w < V && i < h) send(w, i, e ? 2.0 * sum : src[w * hs + h] + 2.0 * sum);
         }
     };
-    // y of the owned vector x from its E / O rows: out(i, y_i)
-    auto combine = [&](int x, auto out) {
-        const double* E = EO + (size_t)(2 * x) * hs;
-        const double* O = E + hs;
-        for (int i = tid; i <= h; i += kRsThreads) {
+    // y of the owned vectors from their E / O rows
+    // the NX owned vectors at once (one flat loop: every thread busy): out(x, i, y_i)
+    auto combine = [&](int NX, auto out) {
+        for (int t = tid; t < NX * (h + 1); t += kRsThreads) {
+            int x, i;
+            rs_split(t, h + 1, x, i);
+            const double* E = EO + (size_t)(2 * x) * hs;
+            const double* O = E + hs;
             if (i < h) {
-                out(i, E[i] + O[i]);
-                out(m - 1 - i, E[i] - O[i]);
+                out(x, i, E[i] + O[i]);
+                out(x, m - 1 - i, E[i] - O[i]);
             } else {
-                out(h, E[h]);
+                out(x, h, E[h]);
             }
         }
     };
@@ -309,8 +312,7 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
         dct3_half(VC, FY, send_b);
         cluster.sync();
         stamp(8);
-        for (int v = 0; v < nr; ++v)
-            combine(v, [&](int j, double val) { T2[L.at(j0 + v, j)] = val; });
+        combine(nr, [&](int v, int j, double val) { T2[L.at(j0 + v, j)] = val; });
         stamp(9);
         stamp(11);
         if (!grid_barrier(gb, gen, &s_ok)) return;
@@ -364,8 +366,7 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
         dct3_half(VCc, F, send_c);
         cluster.sync();
         stamp(14);
-        for (int x = 0; x < sh + nr + hl; ++x)
-            combine(x, [&](int i, double val) { X[x * ms + i] = scale * val; });
+        combine(sh + nr + hl, [&](int x, int i, double val) { X[x * ms + i] = scale * val; });
         __syncthreads();
         stamp(16);
         // ---- D: post step (pdhg_post_kernel's arithmetic) on the shadow and
