@@ -36,9 +36,12 @@
 //     memory and one combine phase: two barriers per transform where the
 //     prime-factor transform of dct_kernels.cuh has five, and no table
 //     lookups.  h <= 16 TS with TS <= 4 covers m <= 129 in one CTA (16
-//     coefficient doubles per thread).  Larger levels use the prime-factor
-//     transforms of dct_kernels.cuh inside the same iteration structure
-//     (TS = 0), with the psi halo row taken from the neighbour CTA.
+//     coefficient doubles per thread).  Larger levels: pdhg_rs2.cuh (m <= 257:
+//     the matrix over two-CTA clusters, FP64 tensor cores), pdhg_rspf.cuh
+//     (m = 513: register-stationary prime-factor DCT); any other size whose
+//     rows fit runs the prime-factor transforms of dct_kernels.cuh inside the
+//     same iteration structure (TS = 0, vectors per transform a power of two,
+//     the v_y and psi halo rows taken from the neighbour CTAs by flags).
 //
 // Spectral data is kept in "position" order along a transformed axis: even
 // k = 2q+2 at q, odd k = 2q+1 at h+q, the constant mode at 2h (dense), or
