@@ -82,6 +82,32 @@ __device__ __forceinline__ int rs_row_odd(int HP) { return HP + 8; }
 __device__ __forceinline__ int rs_row_x(int HP) { return 2 * HP + 16; }
 __host__ __device__ inline int rs_part_doubles(int HP) { return (2 * HP + 17) * 17 + 1; }
 
+// project_unit_ball (prox.cpp:47-62) for the persistent PDHG engines: q = 2
+// scales by 1/sqrt(n2) through the MUFU rsqrt seed and one cubically convergent
+// correction (error below 2^-60 before rounding, like shrink2_fast) instead of
+// an IEEE square root and division -- a 260-cycle dependent chain per node of
+// the post step.  PDHG parity is to tolerance (1e-9 fields), never bit-exact:
+// the DCT already differs from the oracle's FFT in rounding.
+template <int Q>
+__device__ __forceinline__ void rs_proj_unit_ball(double vx, double vy, double& ox, double& oy) {
+    if constexpr (Q == 1) {
+        const double n2 = __fma_rn(vx, vx, vy * vy);
+        if (n2 <= 1.0) {
+            ox = vx;
+            oy = vy;
+        } else {
+            const double y = rsq64h(n2);
+            const double e = __fma_rn(-n2, y * y, 1.0);
+            const double t = __fma_rn(e, 0.375, 0.5);
+            const double r = __fma_rn(t, y * e, y);
+            ox = r * vx;
+            oy = r * vy;
+        }
+    } else {
+        proj_unit_ball<Q>(vx, vy, ox, oy);
+    }
+}
+
 // e -> (v, i) = (e / m, e % m) for the few vectors of a CTA (no integer division)
 __device__ __forceinline__ void rs_split(int e, int m, int& v, int& i) {
     v = 0;
@@ -589,7 +615,7 @@ pdhg_rs_kernel(const SweepArgs a, const DctPlan g, const RsArgs ra, GridBar gb) 
             const double wx = hx ? pox + tau * mnx : 0.0;
             const double wy = hy ? poy + tau * mny : 0.0;
             double qx, qy;
-            proj_unit_ball<QN>(wx, wy, qx, qy);
+            rs_proj_unit_ball<QN>(wx, wy, qx, qy);
             if (hx) {
                 S(S_MX, sv)[i] = mnx;
                 S(S_PX, sv)[i] = qx;

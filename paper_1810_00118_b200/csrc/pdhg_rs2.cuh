@@ -396,7 +396,7 @@ pdhg_rs2_kernel(const SweepArgs a, const RsArgs ra, GridBar gb) {
             const double wx = hx ? pox + tau * mnx : 0.0;
             const double wy = hy ? poy + tau * mny : 0.0;
             double qx, qy;
-            proj_unit_ball<QN>(wx, wy, qx, qy);
+            rs_proj_unit_ball<QN>(wx, wy, qx, qy);
             if (hx) {
                 S(S_MX, sv)[i] = mnx;
                 S(S_PX, sv)[i] = qx;

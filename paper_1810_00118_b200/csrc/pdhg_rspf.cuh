@@ -425,7 +425,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
             const double wx = hx ? pox + tau * mnx : 0.0;
             const double wy = hy ? poy + tau * mny : 0.0;
             double qx, qy;
-            proj_unit_ball<QN>(wx, wy, qx, qy);
+            rs_proj_unit_ball<QN>(wx, wy, qx, qy);
             if (hx) {
                 S(0, sv)[i] = mnx;
                 S(2, sv)[i] = qx;
