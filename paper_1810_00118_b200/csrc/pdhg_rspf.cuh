@@ -46,11 +46,16 @@ struct PfGeo {
     static constexpr int N1 = N1_, N2 = N2_, M = N1 * N2;
     static constexpr int H1 = N1 / 2 + 1, T1 = (N1 - 1) / 2, H2 = N2 / 2 + 1, T2 = (N2 - 1) / 2;
     static constexpr int N1P = (N1 + 2) & ~1;   // row of one column (vector, n2): n1 contiguous
-    static constexpr int N2P = (N2 + 3) & ~1;   // row of one (vector, k1, re/im): n2 or k2 contiguous
+    // rows of the stage buffers; the strides are chosen so that the lanes of a
+    // store (one row per lane) fall into different shared-memory banks: 2 N2P
+    // = 10 and B2R = 14 (mod 16 doubles) give at most two-way conflicts where
+    // 2 N2P = 12 / 2 K1P = 12 gave four-way ones (21 % of the wavefronts in ncu)
+    static constexpr int N2P = ((N2 + 2) & ~7) + 5;  // row of one (vector, k1, re/im): n2 or k2 contiguous (= 5 mod 8)
     static constexpr int K1P = (H1 + 1) & ~1;   // row of one (vector, n2, re/im): k1 contiguous
     static constexpr int GS = N2 * N1P;         // per-vector strides
     static constexpr int AS = H1 * 2 * N2P;
-    static constexpr int BS = N2 * 2 * K1P;
+    static constexpr int B2R = 2 * K1P + 2;     // (re | im) row pair of one (vector, n2), even
+    static constexpr int BS = N2 * B2R;
     static constexpr int GB = GS > BS ? GS : BS;
     static constexpr int NU = 32 / H2;          // columns per warp in the N2 stage
     static constexpr int NI0 = H1 * N2;         // items of the W build
@@ -257,11 +262,11 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
     // inverse N2 stage: b[n2] = C + iS, b[N2-n2] = C - iS -> GBf[v][n2][re/im][k1]
     auto stage2_inv = [&](int V) {
         stage2(V, [&](int v, int k1, double Cr, double Ci, double Sr, double Si) {
-            double* o = GBf + v * P::GB + kh * 2 * K1P + k1;
+            double* o = GBf + v * P::GB + kh * P::B2R + k1;
             o[0] = Cr - Si;
             o[K1P] = Ci + Sr;
             if (kh > 0) {
-                double* o2 = GBf + v * P::GB + (N2 - kh) * 2 * K1P + k1;
+                double* o2 = GBf + v * P::GB + (N2 - kh) * P::B2R + k1;
                 o2[0] = Cr + Si;
                 o2[K1P] = Ci - Sr;
             }
@@ -273,7 +278,7 @@ pdhg_rspf_kernel(const SweepArgs a, const RsArgs ra, const short* __restrict__ g
         for (int col = warp; col < V * N2; col += kPfThreads / 32) {
             int v, n2;
             rs_split(col, N2, v, n2);
-            const double* br = GBf + v * P::GB + n2 * 2 * K1P;
+            const double* br = GBf + v * P::GB + n2 * P::B2R;
             const double2* s2p = reinterpret_cast<const double2*>(isre ? br : br + K1P);
             double acc = 0.0;
             {
